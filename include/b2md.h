@@ -1,0 +1,306 @@
+/*
+ * b2md.h -- C ABI of libb2md.so: the B200 (sm_100a) kernels behind the `mdbench`
+ * per-step molecular-dynamics hot path (arXiv 2406.04210 artifact).
+ *
+ * The reference (`/root/reference/pkg/src/mdbench`, pure Python + numba) has no
+ * FFI.  Its replaceable seam is the chunk-kernel contract of
+ * `BackendSelector.run(kernel, n, *args)` (backend.py:63-73) underneath the
+ * module-level operator functions (neighbor.py, forces.py, integrate.py,
+ * observables.py).  Each entry point below replaces one such kernel / operator
+ * body; the reference line it stands in for is cited on the declaration.  The
+ * Python package `paper_2406_04210_b200` keeps the operator names and
+ * signatures and binds these symbols with ctypes.
+ *
+ * Conventions
+ *  - every pointer named d_* is a DEVICE pointer owned by the caller; the
+ *    library keeps no state between calls except inside an explicit
+ *    b2md_runner (the native step loop);
+ *  - every call takes the CUDA stream (cudaStream_t as void*) it enqueues on and
+ *    is asynchronous unless stated otherwise;
+ *  - return value: 0 = ok, >0 = cudaError_t, <0 = argument error
+ *    (b2md_last_error_string() describes the last failure of the calling thread);
+ *  - data-dependent conditions (row overflow, coincident pair, displacement)
+ *    are reported through a caller-owned device b2md_status, never by
+ *    truncating silently (neighbor.py:145-149, forces.py:113-116).
+ *
+ * Packed particle layout in HBM (one row per particle, row = physical index):
+ *   pos_hi float4 : x,y,z high words of the double-single position, w = species (int bits)
+ *   pos_lo float4 : x,y,z low words,                                 w = particle id (int bits)
+ *   vel    float4 : vx,vy,vz, w = mass
+ *   force  float4 : fx,fy,fz, w = per-particle potential energy (half-shares)
+ *   image  int4   : periodic image counters x,y,z, w unused
+ *   virial float  : per-particle virial half-share 1/2 sum_j fr*r^2
+ * A position is exactly (double)hi + (double)lo; that fp64 value is what the
+ * reference's fp64 arithmetic (cells, neighbour decisions) is applied to.
+ */
+#ifndef B2MD_H
+#define B2MD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2MD_VERSION 100
+
+/* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
+typedef struct b2md_status {
+    int32_t overflow;            /* 1 if some list row wanted more than `stride` entries */
+    int32_t max_count;           /* largest number of neighbours any row wanted (unclamped) */
+    uint64_t singular;           /* (i << 32) | j of the lowest i with a coincident partner; ~0 if none */
+    uint32_t max_disp2_bits;     /* float bits of max_i |r_i - r_i(build)|^2 (fast in-loop check) */
+    int32_t rebuild_flag;        /* set by the fused integrate kernel when max_disp2 > (skin/2)^2 */
+    uint64_t max_disp2_f64_bits; /* double bits of the exact fp64 displacement maximum */
+    int32_t n_boundary;          /* particles flagged as able to interact across a periodic face */
+    int32_t reserved[7];
+} b2md_status;
+
+/* Orthorhombic periodic box: edge lengths in fp64 (core.py:25-57).  Inverse
+ * edges are formed inside the library as 1.0/L in fp64 like the reference. */
+typedef struct b2md_box {
+    double edge[3];
+} b2md_box;
+
+/* Cell grid geometry (neighbor.py:67-71).  Filled on the host by b2md_grid_shape. */
+typedef struct b2md_grid {
+    int32_t ncell[3];
+    int32_t fallback;       /* any axis with fewer than 3 cells (neighbor.py:90) */
+    double cell_edge[3];
+    int64_t n_cells;
+} b2md_grid;
+
+int b2md_version(void);
+const char *b2md_last_error_string(void);
+
+/* ---------------------------------------------------------------- status */
+int b2md_status_reset(b2md_status *d_status, void *stream);
+/* Same, but keeps the `singular` word (used when a list is rebuilt mid-run). */
+int b2md_status_reset_list(b2md_status *d_status, void *stream);
+
+/* ------------------------------------------------- HOST <-> COMPUTE formats
+ * Replace TrackedBuffer's np.copyto between sides (core.py:131-137): the
+ * reference-format arrays (fp64 / int64 / int32, staged in device memory)
+ * are converted to / from the packed layout.  `d_ids` (pos_lo, may be NULL
+ * for identity) maps physical row r to logical particle id = pos_lo[r].w. */
+int b2md_pack_positions(const double *d_pos_f64, int64_t n, const void *d_ids_pos_lo,
+                        void *d_pos_hi, void *d_pos_lo, void *stream);
+int b2md_unpack_positions(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                          const void *d_ids_pos_lo, double *d_pos_f64, void *stream);
+int b2md_pack_vec3(const double *d_src_f64, int64_t n, const void *d_ids_pos_lo,
+                   void *d_dst_f4, void *stream);
+int b2md_unpack_vec3(const void *d_src_f4, int64_t n, const void *d_ids_pos_lo,
+                     double *d_dst_f64, void *stream);
+int b2md_pack_w_f64(const double *d_src_f64, int64_t n, const void *d_ids_pos_lo,
+                    void *d_dst_f4, void *stream);
+int b2md_unpack_w_f64(const void *d_src_f4, int64_t n, const void *d_ids_pos_lo,
+                      double *d_dst_f64, void *stream);
+int b2md_pack_w_i32(const int32_t *d_src_i32, int64_t n, const void *d_ids_pos_lo,
+                    void *d_dst_f4, void *stream);
+int b2md_unpack_w_i32(const void *d_src_f4, int64_t n, const void *d_ids_pos_lo,
+                      int32_t *d_dst_i32, void *stream);
+int b2md_pack_images(const int64_t *d_src_i64, int64_t n, const void *d_ids_pos_lo,
+                     void *d_image_i4, void *stream);
+int b2md_unpack_images(const void *d_image_i4, int64_t n, const void *d_ids_pos_lo,
+                       int64_t *d_dst_i64, void *stream);
+int b2md_pack_scalar_f32(const double *d_src_f64, int64_t n, const void *d_ids_pos_lo,
+                         float *d_dst_f32, void *stream);
+int b2md_unpack_scalar_f32(const float *d_src_f32, int64_t n, const void *d_ids_pos_lo,
+                           double *d_dst_f64, void *stream);
+int b2md_set_ids(void *d_pos_lo, int64_t n, void *stream);      /* pos_lo[r].w = r */
+int b2md_get_ids(const void *d_pos_lo, int64_t n, int32_t *d_ids, void *stream);
+
+/* ------------------------------------------------------------- cell binning
+ * bin_particles (neighbor.py:57-91).  b2md_grid_shape is host-only fp64.
+ * b2md_bin: atomic per-cell count -> warp-shuffle prefix sum -> scatter ->
+ * ascending order inside every cell (the reference's stable argsort).
+ * Outputs: d_cell_of (n) int32, d_cell_start (n_cells+1) int32,
+ * d_cell_particles (n) int32.  d_scratch: >= b2md_bin_scratch_bytes(). */
+int b2md_grid_shape(const b2md_box *box, double r_list, b2md_grid *grid_out);
+int64_t b2md_bin_scratch_bytes(int64_t n, int64_t n_cells);
+int b2md_bin(const void *d_pos_hi, const void *d_pos_lo, int64_t n, const b2md_grid *grid,
+             int32_t *d_cell_of, int32_t *d_cell_start, int32_t *d_cell_particles,
+             void *d_scratch, void *stream);
+
+/* ------------------------------------------------------ Verlet neighbour list
+ * build_neighbor_list (neighbor.py:185-240; kernels 112-182).  Decision
+ * r2 < rl2 in fp64 without FMA on (double)hi+(double)lo, 27-cell scan in the
+ * reference's order (or all-pairs when grid->fallback), rows ascending.
+ * Layout: column-major, entry k of particle i at d_nbr[k * pitch + i]
+ * (pitch >= n, multiple of 32) so that a warp's loads coalesce.  Rows wanting
+ * more than `stride` entries set status->overflow; status->max_count receives
+ * the largest unclamped count.  d_boundary (n) uint8 marks particles within
+ * `boundary_margin` of a periodic face (they may interact across it). */
+int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                     const b2md_box *box, const b2md_grid *grid,
+                     const int32_t *d_cell_of, const int32_t *d_cell_start,
+                     const int32_t *d_cell_particles, double r_list,
+                     int32_t stride, int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
+                     uint8_t *d_boundary, double boundary_margin,
+                     b2md_status *d_status, void *stream);
+
+/* Snapshot of the unwrapped positions a list was built from
+ * (neighbor.py:238, core.py:216-219): exact fp64 rows (n,3) and the fp32
+ * reference copy used by the in-loop displacement check. */
+int b2md_snapshot(const void *d_pos_hi, const void *d_pos_lo, const void *d_image_i4,
+                  int64_t n, const b2md_box *box, double *d_at_build_f64,
+                  void *d_ref_pos_f4, void *stream);
+
+/* needs_rebuild's reduction (neighbor.py:251-253), exact fp64:
+ * status->max_disp2_f64_bits = max_i |(pos + img*L) - at_build|^2. */
+int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void *d_image_i4,
+                          int64_t n, const b2md_box *box, const double *d_at_build_f64,
+                          b2md_status *d_status, void *stream);
+
+/* ------------------------------------------------------------- LJ forces
+ * compute_forces_truncated (forces.py:141-159; kernel 72-110), fp32 pair
+ * arithmetic on pos_hi, per-particle energy and virial in registers.
+ * table: HOST pointer to ntypes*ntypes rows {eps, sigma^2, rc^2, shift} (fp64;
+ * forces.py:119-126 for one type).  `stride` = rows of d_nbr per particle.
+ * d_boundary (may be NULL = all) selects the exact-image-shift path per warp.
+ * Writes force (xyz + e_pot in w) and virial.
+ * A coincident listed pair is reported in status->singular. */
+int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                  const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
+                  int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
+                  void *d_force_f4, float *d_virial, b2md_status *d_status, void *stream);
+
+/* compute_forces_all_to_all (forces.py:129-138; kernel 29-69): shared-memory
+ * tiled all-pairs scan, same outputs. */
+int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                            const double *table, int32_t ntypes, void *d_force_f4,
+                            float *d_virial, b2md_status *d_status, void *stream);
+
+/* --------------------------------------------------------- velocity Verlet
+ * vv_integrate (integrate.py:58-70 + core.py:72-93): half-kick, drift in
+ * double-single, wrap, image counters.  When d_ref_pos_f4 != NULL the kernel
+ * also reduces the squared displacement from the list snapshot into
+ * status->max_disp2_bits and raises status->rebuild_flag when it exceeds
+ * half_skin2 (neighbor.py:243-254, fp32 fast check; the exact test is
+ * b2md_max_displacement). */
+int b2md_vv_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel, const void *d_force_f4,
+                      void *d_image_i4, int64_t n, const b2md_box *box, double dt,
+                      void *d_ref_pos_f4, double half_skin2, b2md_status *d_status,
+                      void *stream);
+/* vv_finalize (integrate.py:73-79). */
+int b2md_vv_finalize(void *d_vel, const void *d_force_f4, int64_t n, double dt, void *stream);
+/* finalize of step s fused with integrate of step s+1 (one pass over the state). */
+int b2md_vv_finalize_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel,
+                               const void *d_force_f4, void *d_image_i4, int64_t n,
+                               const b2md_box *box, double dt, void *d_ref_pos_f4,
+                               double half_skin2, b2md_status *d_status, void *stream);
+
+/* ------------------------------------------------------------ observables
+ * reduce_sum (observables.py:43-74): the reference's fixed pairing tree
+ * (4096-value blocks, adjacent pairs, odd leftover carried), bit-exact in fp64.
+ * d_scratch: ceil(n/4096) doubles (+ further levels).  Result -> d_out[0]. */
+int64_t b2md_reduce_scratch_bytes(int64_t n);
+int b2md_reduce_sum_f64(const double *d_values, int64_t n, double *d_scratch,
+                        double *d_out, void *stream);
+/* measure() (sim.py:159-174; observables.py:77-98) in one pass over vel/force/
+ * virial with the same tree: d_out[0..7] = e_pot, e_kin, p_x, p_y, p_z,
+ * virial, mass, n.  d_scratch: 8 * ceil(n/4096) doubles (+ further levels). */
+int64_t b2md_thermo_scratch_bytes(int64_t n);
+int b2md_thermo(const void *d_vel, const void *d_force_f4, const float *d_virial, int64_t n,
+                double *d_scratch, double *d_out8, void *stream);
+
+/* -------------------------------------------- reorder (Hilbert / cell order)
+ * reorder_by_cell (neighbor.py:257-270) generalised: 64-bit keys, stable LSD
+ * radix sort, gather of every per-particle array.
+ * b2md_hilbert_keys: 3*bits-bit Hilbert index of floor(pos * 2^bits / L).
+ * b2md_cell_keys: key = flat cell index (exactly reorder_by_cell's order).
+ * b2md_sort_pairs_u64: stable; on return keys/values are in d_keys/d_vals.
+ * b2md_gather16 / b2md_gather4: dst[k] = src[perm[k]] for 16- / 4-byte rows. */
+int b2md_hilbert_keys(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                      const b2md_box *box, int32_t bits, uint64_t *d_keys, void *stream);
+int b2md_cell_keys(const int32_t *d_cell_of, int64_t n, uint64_t *d_keys, void *stream);
+int b2md_iota_i32(int32_t *d_vals, int64_t n, void *stream);
+int64_t b2md_sort_scratch_bytes(int64_t n);
+int b2md_sort_pairs_u64(uint64_t *d_keys, int32_t *d_vals, uint64_t *d_keys_tmp,
+                        int32_t *d_vals_tmp, int64_t n, int32_t key_bits,
+                        void *d_scratch, void *stream);
+int b2md_gather16(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
+int b2md_gather4(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
+
+/* ------------------------------------------------------------ native step loop
+ * Simulation.run / SignalEngine.run_steps (core.py:262-279) with the rebuild
+ * policy of Simulation._compute_forces/_rebuild (sim.py:114-149), driven from
+ * C++ so that a step costs two launches and no Python:
+ *
+ *   [finalize(s-1) + integrate(s) fused, folds the displacement check]
+ *   [async 64-byte status read-back]  [force(s), launched speculatively]
+ *   host looks at the flag while the force kernel runs; only if it is set:
+ *   bin -> (Hilbert/cell reorder) -> list build -> snapshot -> force again.
+ *
+ * All memory is caller-owned (PyTorch tensors); per-particle arrays come in
+ * pairs so a reorder can gather from one set into the other.  The runner never
+ * grows a list: when a build overflows `stride_rows` it stops with
+ * reason = B2MD_RUN_OVERFLOW and the caller re-creates it with bigger buffers
+ * (sim.py:141-149 semantics: grow and rebuild, never truncate). */
+typedef struct b2md_runner_config {
+    int64_t n;
+    int64_t capacity;            /* rows in every per-particle array, >= n */
+    b2md_box box;
+    double dt;
+    double r_cut;                /* largest pair cutoff */
+    double skin;
+    int32_t ntypes;
+    int32_t reorder_mode;        /* 0 none, 1 Hilbert, 2 cell order */
+    int32_t reorder_every;       /* reorder on every k-th rebuild (>= 1) */
+    int32_t hilbert_bits;
+    const double *table;         /* HOST, ntypes*ntypes*4, copied at create */
+    void *pos_hi[2], *pos_lo[2], *vel[2], *force[2], *image[2];
+    float *virial[2];
+    int32_t current;             /* which set of the pairs above is live */
+    int32_t stride;              /* neighbour budget per particle */
+    int32_t *nbr;                /* round_up(stride,4) * pitch */
+    int64_t pitch;
+    int32_t *counts;             /* pitch */
+    uint8_t *boundary;           /* pitch */
+    void *ref_pos;               /* float4[pitch] */
+    double *at_build;            /* n*3 fp64 snapshot, may be NULL */
+    int32_t *cell_of, *cell_start, *cell_particles;   /* n, n_cells+1, n */
+    void *bin_scratch;           /* b2md_bin_scratch_bytes(n, n_cells) */
+    uint64_t *keys, *keys_tmp;   /* n each (reorder only) */
+    int32_t *perm, *perm_tmp;    /* n each (reorder only) */
+    void *sort_scratch;          /* b2md_sort_scratch_bytes(n) */
+    b2md_status *status;         /* device */
+    void *stream;
+} b2md_runner_config;
+
+enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };
+
+typedef struct b2md_run_report {
+    int64_t steps_done;
+    int32_t reason;              /* B2MD_RUN_* */
+    int32_t rebuilds;            /* list builds during this call */
+    int32_t reorders;
+    int32_t current;             /* live buffer set after the call */
+    int32_t max_count;           /* largest row length wanted by the last build */
+    int32_t wasted_force_launches;
+    int64_t kernel_launches;     /* kernels enqueued by this call */
+    int32_t list_valid;          /* 0 if the call stopped before a usable list existed */
+    int32_t n_boundary;
+    double max_disp2;            /* last displacement maximum seen (fp32 check) */
+    uint64_t singular;           /* status->singular when reason == B2MD_RUN_SINGULAR */
+} b2md_run_report;
+
+typedef struct b2md_runner b2md_runner;
+
+b2md_runner *b2md_runner_create(const b2md_runner_config *cfg);
+void b2md_runner_destroy(b2md_runner *r);
+/* Swap in bigger list buffers after B2MD_RUN_OVERFLOW (nbr: round_up(stride,4)*pitch). */
+int b2md_runner_set_list(b2md_runner *r, int32_t *nbr, int32_t stride);
+/* (Re)build the list for the current positions and evaluate forces
+ * (Simulation.__init__'s initial _compute_forces, sim.py:90).  Synchronous. */
+int b2md_runner_prepare(b2md_runner *r, b2md_run_report *report);
+/* Advance n_steps.  finalize_at_end != 0 leaves velocities fully kicked
+ * (state as after the reference's finalize slot); otherwise the last half-kick
+ * is deferred into the next call's first fused kernel.  Synchronous on return. */
+int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finalize_at_end,
+                    b2md_run_report *report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2MD_H */

@@ -1,0 +1,338 @@
+// Truncated / shifted Lennard-Jones forces over the Verlet list: reference
+// compute_forces_truncated (forces.py:141-159), kernel _truncated_chunk (72-110);
+// plus the all-pairs kernel (_all_to_all_chunk, forces.py:29-69).
+//
+// One thread per particle, fp32 pair arithmetic on the position high words,
+// force / energy / virial accumulated in registers, one float4 + one float
+// store per particle.  Neighbour indices stream through the column-major list
+// (coalesced, evict-first); neighbour positions are 16-byte gathers served by
+// L1/L2 because particles are kept in Hilbert / cell order.
+//
+// Minimum image.  A literal fp32 transcription of d - L*rint(d/L) loses ~ulp(L)
+// on pairs that interact across a periodic face (r^-13 amplifies it past the 1e-5
+// budget).  Two paths, chosen per warp:
+//   * interior warps (no lane flagged `boundary` at list build): neighbours are
+//     on the same side of every face for the list's whole lifetime, so
+//     d = xi - xj needs no image shift at all (and is exact by Sterbenz' lemma
+//     away from the origin);
+//   * boundary warps: n = rint(d/L) via the 1.5*2^23 trick, then the box length
+//     (as L_hi + L_lo) is subtracted from whichever coordinate is the larger one,
+//     which is exact, before the difference is formed.
+//
+// Single-type systems defer the 24*eps, 2*eps, 12*eps prefactors to the end of the
+// row; tabulated systems (Kob-Andersen) read {sigma^2, rc^2, 24 eps, 2 eps, shift/2}
+// per species pair from shared memory.
+//
+// Coincident pairs (r2 == 0; forces.py:94-97) cost nothing in the loop: they
+// turn the row's accumulators non-finite, and only then is the row rescanned to
+// report (i, first j) through status->singular.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace b2md {
+
+constexpr int kForceThreads = 128;
+constexpr int kMaxTypes = 8;
+
+struct PairParams {   // one species pair, fp32
+    float sig2, rc2, c_f, c_u;   // sigma^2, rc^2, 24*eps, 2*eps
+    float half_shift, c_w;       // shift/2, 12*eps
+};
+
+struct ForceArgs {
+    BoxF box;
+    PairParams single;
+    int ntypes;
+    float4 tab_a[kMaxTypes * kMaxTypes];   // sig2, rc2, c_f, c_u
+    float2 tab_b[kMaxTypes * kMaxTypes];   // half_shift, c_w
+};
+
+__device__ __forceinline__ float rint_small(float q) {
+    // round-half-even for |q| < 2^22 on the FMA pipe (no FRND / conversion pipe)
+    const float magic = 12582912.0f;  // 1.5 * 2^23
+    return __fsub_rn(__fadd_rn(q, magic), magic);
+}
+
+template <bool CAREFUL>
+__device__ __forceinline__ float delta(float xi, float xj, float L_hi, float L_lo, float invL) {
+    if (!CAREFUL) return xi - xj;
+    const float d0 = xi - xj;
+    const float ns = rint_small(d0 * invL);            // -1, 0 or +1 for listed pairs
+    const float a = fmaf(-fmaxf(ns, 0.0f), L_hi, xi);  // shift the larger coordinate: exact
+    const float b = fmaf(-fmaxf(-ns, 0.0f), L_hi, xj);
+    return fmaf(-ns, L_lo, a - b);
+}
+
+struct RowAcc {
+    float fx, fy, fz, u, w;
+    int cnt;
+};
+
+// Single-type pair: prefactors deferred.  `in` false => contributes exact zeros.
+__device__ __forceinline__ void lj_pair_single(RowAcc &acc, float dx, float dy, float dz, float r2,
+                                               bool valid, const PairParams &p) {
+    const bool in = valid && (r2 < p.rc2);
+    const float ir2 = in ? __frcp_rn(r2) : 0.0f;
+    const float s2 = p.sig2 * ir2;
+    const float s6 = s2 * s2 * s2;
+    const float t = s6 * fmaf(2.0f, s6, -1.0f);        // s6*(2 s6 - 1) = fr*r2 / (24 eps)
+    const float g = t * ir2;
+    acc.fx = fmaf(g, dx, acc.fx);
+    acc.fy = fmaf(g, dy, acc.fy);
+    acc.fz = fmaf(g, dz, acc.fz);
+    acc.u = fmaf(s6, s6 - 1.0f, acc.u);                // (s12 - s6)
+    acc.w += t;
+    acc.cnt += in ? 1 : 0;
+}
+
+__device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, float dz, float r2,
+                                              bool valid, const float4 pa, const float2 pb) {
+    const bool in = valid && (r2 < pa.y);
+    const float ir2 = in ? __frcp_rn(r2) : 0.0f;
+    const float s2 = pa.x * ir2;
+    const float s6 = s2 * s2 * s2;
+    const float t = s6 * fmaf(2.0f, s6, -1.0f);
+    const float g = pa.z * t * ir2;
+    acc.fx = fmaf(g, dx, acc.fx);
+    acc.fy = fmaf(g, dy, acc.fy);
+    acc.fz = fmaf(g, dz, acc.fz);
+    acc.u = fmaf(pa.w * s6, s6 - 1.0f, acc.u);
+    acc.u += in ? pb.x : 0.0f;
+    acc.w = fmaf(pb.y, t, acc.w);
+}
+
+template <bool CAREFUL, bool TABLE>
+__device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int kmax,
+                                         int stride, const int32_t *__restrict__ col,
+                                         int64_t pitch, const float4 *__restrict__ pos,
+                                         const ForceArgs &a, const float4 *s_tab_a,
+                                         const float2 *s_tab_b, int ti_row) {
+    const BoxF &b = a.box;
+    for (int k = 0; k < kmax; k += 4) {
+        int j[4];
+        float4 pj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int kk = min(k + u, stride - 1);
+            j[u] = __ldcs(col + (int64_t)kk * pitch);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+            const float dy = delta<CAREFUL>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+            const float dz = delta<CAREFUL>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const bool valid = (k + u) < cnt;
+            if (TABLE) {
+                const int t = ti_row + __float_as_int(pj[u].w);
+                lj_pair_table(acc, dx, dy, dz, r2, valid, s_tab_a[t], s_tab_b[t]);
+            } else {
+                lj_pair_single(acc, dx, dy, dz, r2, valid, a.single);
+            }
+        }
+    }
+}
+
+// Rare path: find the first listed j at zero separation (forces.py:94-97).
+__device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
+                                             const int32_t *__restrict__ col, int64_t pitch,
+                                             const float4 *__restrict__ pos, const BoxF &b,
+                                             b2md_status *status) {
+    for (int k = 0; k < cnt; ++k) {
+        const int j = col[(int64_t)k * pitch];
+        const float4 pj = pos[j];
+        const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) == 0.0f) {
+            atomicMin((unsigned long long *)&status->singular,
+                      ((unsigned long long)(unsigned)i << 32) | (unsigned)j);
+            return;
+        }
+    }
+}
+
+template <bool TABLE>
+__global__ void __launch_bounds__(kForceThreads)
+k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
+           const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
+           int stride, const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
+           float *__restrict__ virial, b2md_status *status) {
+    __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    if (TABLE) {
+        for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
+            s_tab_a[t] = a.tab_a[t];
+            s_tab_b[t] = a.tab_b[t];
+        }
+        __syncthreads();
+    }
+    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    const float4 pi = pos[i];
+    const int cnt = active ? counts[i] : 0;
+    const int kmax = __reduce_max_sync(0xffffffffu, cnt);
+    const bool careful = boundary ? (__any_sync(0xffffffffu, active && boundary[i] != 0)) : true;
+    const int32_t *col = nbr + i;
+    const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
+
+    RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+    if (careful)
+        row_loop<true, TABLE>(acc, pi, cnt, kmax, stride, col, pitch, pos, a, s_tab_a, s_tab_b, ti_row);
+    else
+        row_loop<false, TABLE>(acc, pi, cnt, kmax, stride, col, pitch, pos, a, s_tab_a, s_tab_b, ti_row);
+
+    if (!active) return;
+    float fx, fy, fz, u, w;
+    if (TABLE) {
+        fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
+    } else {
+        const PairParams &p = a.single;
+        fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+        u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
+        w = p.c_w * acc.w;
+    }
+    force[i] = make_float4(fx, fy, fz, u);
+    if (virial) virial[i] = w;
+    if (!(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(u)))
+        report_singular((int)i, pi, cnt, col, pitch, pos, a.box, status);
+}
+
+// ---- all pairs, shared-memory tiles of 128 positions ------------------------
+template <bool TABLE>
+__global__ void __launch_bounds__(kForceThreads)
+k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
+                  float4 *__restrict__ force, float *__restrict__ virial, b2md_status *status) {
+    __shared__ float4 tile[kForceThreads];
+    __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    if (TABLE) {
+        for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
+            s_tab_a[t] = a.tab_a[t];
+            s_tab_b[t] = a.tab_b[t];
+        }
+    }
+    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    const float4 pi = pos[i];
+    const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
+    const BoxF &b = a.box;
+    RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+    long long first_bad = -1;
+    for (int64_t base = 0; base < n; base += kForceThreads) {
+        __syncthreads();
+        const int64_t jl = base + threadIdx.x;
+        tile[threadIdx.x] = pos[jl < n ? jl : n - 1];
+        __syncthreads();
+        const int lim = (int)min((int64_t)kForceThreads, n - base);
+#pragma unroll 4
+        for (int t = 0; t < lim; ++t) {
+            const float4 pj = tile[t];
+            const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+            const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+            const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const bool self = (base + t) == i;
+            if (!self && r2 == 0.0f && first_bad < 0) first_bad = base + t;
+            const bool valid = !self && r2 != 0.0f;
+            if (TABLE) {
+                const int tt = ti_row + __float_as_int(pj.w);
+                lj_pair_table(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
+            } else {
+                lj_pair_single(acc, dx, dy, dz, r2, valid, a.single);
+            }
+        }
+    }
+    if (!active) return;
+    float fx, fy, fz, u, w;
+    if (TABLE) {
+        fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
+    } else {
+        const PairParams &p = a.single;
+        fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+        u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
+        w = p.c_w * acc.w;
+    }
+    force[i] = make_float4(fx, fy, fz, u);
+    if (virial) virial[i] = w;
+    if (first_bad >= 0)
+        atomicMin((unsigned long long *)&status->singular,
+                  ((unsigned long long)(unsigned)i << 32) | (unsigned)first_bad);
+}
+
+static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int ntypes) {
+    if (!box || !table) { set_error("force: null box/table"); return -1; }
+    if (ntypes < 1 || ntypes > kMaxTypes) {
+        set_error("force: ntypes must be in [1, %d]", kMaxTypes);
+        return -2;
+    }
+    a.box = make_box_f(box);
+    a.ntypes = ntypes;
+    for (int t = 0; t < ntypes * ntypes; ++t) {
+        const double eps = table[4 * t], sig2 = table[4 * t + 1], rc2 = table[4 * t + 2],
+                     shift = table[4 * t + 3];
+        a.tab_a[t] = make_float4((float)sig2, (float)rc2, (float)(24.0 * eps), (float)(2.0 * eps));
+        a.tab_b[t] = make_float2((float)(0.5 * shift), (float)(12.0 * eps));
+    }
+    a.single.sig2 = a.tab_a[0].x;
+    a.single.rc2 = a.tab_a[0].y;
+    a.single.c_f = a.tab_a[0].z;
+    a.single.c_u = a.tab_a[0].w;
+    a.single.half_shift = a.tab_b[0].x;
+    a.single.c_w = a.tab_b[0].y;
+    return 0;
+}
+
+}  // namespace b2md
+
+using namespace b2md;
+
+B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                              const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
+                              int32_t stride, const uint8_t *d_boundary, const double *table,
+                              int32_t ntypes, void *d_force_f4, float *d_virial,
+                              b2md_status *d_status, void *stream) {
+    if (n <= 0 || !d_nbr || !d_counts || !d_status || stride < 1) {
+        set_error("b2md_force_lj: bad arguments");
+        return -1;
+    }
+    ForceArgs a;
+    int rc = fill_args(a, box, table, ntypes);
+    if (rc) return rc;
+    const unsigned blocks = blocks_for(n, kForceThreads);
+    cudaStream_t s = as_stream(stream);
+    if (ntypes == 1)
+        k_force_lj<false><<<blocks, kForceThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, stride, d_boundary,
+            (float4 *)d_force_f4, d_virial, d_status);
+    else
+        k_force_lj<true><<<blocks, kForceThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, stride, d_boundary,
+            (float4 *)d_force_f4, d_virial, d_status);
+    B2MD_CHECK_LAUNCH("b2md_force_lj");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                                        const double *table, int32_t ntypes, void *d_force_f4,
+                                        float *d_virial, b2md_status *d_status, void *stream) {
+    if (n <= 0 || !d_status) { set_error("b2md_force_lj_all_pairs: bad arguments"); return -1; }
+    ForceArgs a;
+    int rc = fill_args(a, box, table, ntypes);
+    if (rc) return rc;
+    const unsigned blocks = blocks_for(n, kForceThreads);
+    cudaStream_t s = as_stream(stream);
+    if (ntypes == 1)
+        k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, n, a, (float4 *)d_force_f4, d_virial, d_status);
+    else
+        k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, n, a, (float4 *)d_force_f4, d_virial, d_status);
+    B2MD_CHECK_LAUNCH("b2md_force_lj_all_pairs");
+    return 0;
+}

@@ -1,0 +1,302 @@
+// Verlet neighbour lists: reference build_neighbor_list (neighbor.py:185-240),
+// kernels _list_cells_chunk (112-152) and _list_brute_chunk (155-182), the
+// build-time snapshot (238) and needs_rebuild's reduction (243-254).
+//
+// The listing decision r2 < rl2 is taken in fp64 with the reference's exact
+// operation sequence (no FMA) on positions (double)hi + (double)lo, so the
+// neighbour SETS are bit-exact.  A cheap fp32 pre-test on the high words skips
+// the fp64 arithmetic for candidates that are far outside or far inside the
+// listing sphere; its guard band is wide enough that it can never change a
+// decision (bound derived below).
+//
+// Output layout is column-major and padded: entry k of particle i lives at
+// nbr[k * pitch + i], so the force kernel's per-k loads coalesce across a warp.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace b2md {
+
+constexpr int kBuildThreads = 128;
+
+struct ListGeom {
+    BoxD box;
+    int nc[3];
+    double rl2;
+    // fp32 pre-test:  r2f < rl2_in  => certainly listed,  r2f > rl2_out => certainly not.
+    float rl2_in, rl2_out;
+    float Lf[3], invLf[3];
+    float margin[3];   // boundary flag: within this distance of a periodic face
+    float Lhi[3];
+};
+
+// One fp64 candidate test, the reference's arithmetic verbatim
+// (neighbor.py:137-144): d = xi - xj; d -= L*rint(d*(1/L)); r2 = (dx*dx+dy*dy)+dz*dz.
+__device__ __forceinline__ bool listed_f64(const double pi[3], const float4 hj, const float4 lj,
+                                           const ListGeom &g) {
+    double dx = __dsub_rn(pi[0], ds_to_double(hj.x, lj.x));
+    double dy = __dsub_rn(pi[1], ds_to_double(hj.y, lj.y));
+    double dz = __dsub_rn(pi[2], ds_to_double(hj.z, lj.z));
+    dx = min_image_f64(dx, g.box.L[0], g.box.invL[0]);
+    dy = min_image_f64(dy, g.box.L[1], g.box.invL[1]);
+    dz = min_image_f64(dz, g.box.L[2], g.box.invL[2]);
+    double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return r2 < g.rl2;
+}
+
+// fp32 estimate of the same squared distance from the high words only.
+// Error budget (per component, box edge L, u = 2^-24):
+//   |hi - x| <= u*L for both particles, the fp32 subtraction adds <= u*L, the
+//   product d*invL and the fma with L_f32 (|L - L_f32| <= u*L) add <= 3*u*L more
+//   => |d_f32 - d| <= 8*u*L.  With |d| <= 1.5*r_list per component the squared
+//   distance is off by at most 3 * (2*1.5*r_list*8uL + (8uL)^2) plus 3 roundings of
+//   the sum (<= 4u * r2).  The host sets the band to 4x that figure.
+__device__ __forceinline__ float dist2_f32(const float4 hi_i, const float4 hj, const ListGeom &g) {
+    float dx = hi_i.x - hj.x, dy = hi_i.y - hj.y, dz = hi_i.z - hj.z;
+    dx = fmaf(-g.Lf[0], rintf(dx * g.invLf[0]), dx);
+    dy = fmaf(-g.Lf[1], rintf(dy * g.invLf[1]), dy);
+    dz = fmaf(-g.Lf[2], rintf(dz * g.invLf[2]), dz);
+    return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+// Sort the kept prefix ascending (neighbor.py:152), store the count, and fold the
+// row's wanted length into the status block with one atomic per warp.  Must be
+// called by every thread of the warp (inactive lanes pass active = false).
+__device__ __forceinline__ void finish_row(int32_t *__restrict__ nbr, int64_t pitch, int64_t i,
+                                           bool active, int found, int stride, int32_t *counts,
+                                           b2md_status *status) {
+    if (active) {
+        const int kept = found < stride ? found : stride;
+        counts[i] = kept;
+        for (int a = 1; a < kept; ++a) {  // rows arrive nearly sorted
+            int v = nbr[(int64_t)a * pitch + i];
+            int b = a - 1;
+            while (b >= 0) {
+                int w = nbr[(int64_t)b * pitch + i];
+                if (w <= v) break;
+                nbr[(int64_t)(b + 1) * pitch + i] = w;
+                --b;
+            }
+            if (b + 1 != a) nbr[(int64_t)(b + 1) * pitch + i] = v;
+        }
+    }
+    int mx = active ? found : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) {
+        if (mx > stride) atomicExch(&status->overflow, 1);
+        atomicMax(&status->max_count, mx);
+    }
+}
+
+__device__ __forceinline__ uint8_t boundary_flag(const float4 h, const ListGeom &g) {
+    bool near_face = false;
+    const float p[3] = {h.x, h.y, h.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        near_face |= (p[a] < g.margin[a]) | (p[a] > g.Lhi[a] - g.margin[a]);
+    return near_face ? 1 : 0;
+}
+
+template <bool PREFILTER>
+__global__ void __launch_bounds__(kBuildThreads)
+k_list_cells(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
+             ListGeom g, const int32_t *__restrict__ cell_of,
+             const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_particles,
+             int stride, int64_t pitch, int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
+             uint8_t *__restrict__ boundary, b2md_status *status) {
+    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
+    const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
+                          ds_to_double(hi_i.z, lo_i.z)};
+    const int ci = cell_of[i];
+    const int cz = ci % g.nc[2];
+    const int cy = (ci / g.nc[2]) % g.nc[1];
+    const int cx = ci / (g.nc[2] * g.nc[1]);
+    int found = 0;
+    for (int ox = -1; ox <= 1; ++ox) {
+        int jx = cx + ox;
+        jx = jx < 0 ? jx + g.nc[0] : (jx >= g.nc[0] ? jx - g.nc[0] : jx);
+        for (int oy = -1; oy <= 1; ++oy) {
+            int jy = cy + oy;
+            jy = jy < 0 ? jy + g.nc[1] : (jy >= g.nc[1] ? jy - g.nc[1] : jy);
+            for (int oz = -1; oz <= 1; ++oz) {
+                int jz = cz + oz;
+                jz = jz < 0 ? jz + g.nc[2] : (jz >= g.nc[2] ? jz - g.nc[2] : jz);
+                const int cj = (jx * g.nc[1] + jy) * g.nc[2] + jz;
+                const int p_end = active ? cell_start[cj + 1] : 0;
+                for (int p = cell_start[cj]; p < p_end; ++p) {
+                    const int j = cell_particles[p];
+                    if (j == (int)i) continue;
+                    const float4 hj = __ldg(&pos_hi[j]);
+                    bool hit;
+                    if (PREFILTER) {
+                        const float r2f = dist2_f32(hi_i, hj, g);
+                        if (r2f > g.rl2_out) continue;
+                        hit = (r2f < g.rl2_in) || listed_f64(pi, hj, __ldg(&pos_lo[j]), g);
+                    } else {
+                        hit = listed_f64(pi, hj, __ldg(&pos_lo[j]), g);
+                    }
+                    if (hit) {
+                        if (found < stride) nbr[(int64_t)found * pitch + i] = j;
+                        ++found;
+                    }
+                }
+            }
+        }
+    }
+    if (boundary && active) boundary[i] = boundary_flag(hi_i, g);
+    finish_row(nbr, pitch, i, active, found, stride, counts, status);
+}
+
+// All-pairs scan for grids with fewer than three cells on some axis.
+__global__ void __launch_bounds__(kBuildThreads)
+k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
+             ListGeom g, int stride, int64_t pitch, int32_t *__restrict__ nbr,
+             int32_t *__restrict__ counts, uint8_t *__restrict__ boundary, b2md_status *status) {
+    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
+    const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
+                          ds_to_double(hi_i.z, lo_i.z)};
+    int found = 0;
+    const int64_t j_end = active ? n : 0;
+    for (int64_t j = 0; j < j_end; ++j) {
+        if (j == i) continue;
+        if (listed_f64(pi, __ldg(&pos_hi[j]), __ldg(&pos_lo[j]), g)) {
+            if (found < stride) nbr[(int64_t)found * pitch + i] = (int)j;
+            ++found;
+        }
+    }
+    if (boundary && active) boundary[i] = 1;  // tiny boxes: every pair may cross a face
+    finish_row(nbr, pitch, i, active, found, stride, counts, status);
+}
+
+__global__ void k_count_boundary(const uint8_t *__restrict__ boundary, int64_t n,
+                                 b2md_status *status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int v = (i < n) ? boundary[i] : 0;
+    v = warp_sum_i(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&status->n_boundary, v);
+}
+
+// Unwrapped fp64 snapshot (pos + img*L, core.py:216-219) + fp32 reference copy.
+__global__ void k_snapshot(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
+                           const int4 *__restrict__ image, int64_t n, BoxD box,
+                           double *__restrict__ at_build, float4 *__restrict__ ref_pos) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 h = pos_hi[i], l = pos_lo[i];
+    if (at_build) {
+        const int4 im = image[i];
+        at_build[3 * i + 0] = __dadd_rn(ds_to_double(h.x, l.x), __dmul_rn((double)im.x, box.L[0]));
+        at_build[3 * i + 1] = __dadd_rn(ds_to_double(h.y, l.y), __dmul_rn((double)im.y, box.L[1]));
+        at_build[3 * i + 2] = __dadd_rn(ds_to_double(h.z, l.z), __dmul_rn((double)im.z, box.L[2]));
+    }
+    if (ref_pos) ref_pos[i] = make_float4(h.x, h.y, h.z, 0.f);
+}
+
+// Exact fp64 displacement maximum (neighbor.py:251-253).
+__global__ void k_max_disp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
+                           const int4 *__restrict__ image, int64_t n, BoxD box,
+                           const double *__restrict__ at_build, b2md_status *status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double s = 0.0;
+    if (i < n) {
+        const float4 h = pos_hi[i], l = pos_lo[i];
+        const int4 im = image[i];
+        double ux = __dadd_rn(ds_to_double(h.x, l.x), __dmul_rn((double)im.x, box.L[0]));
+        double uy = __dadd_rn(ds_to_double(h.y, l.y), __dmul_rn((double)im.y, box.L[1]));
+        double uz = __dadd_rn(ds_to_double(h.z, l.z), __dmul_rn((double)im.z, box.L[2]));
+        double dx = __dsub_rn(ux, at_build[3 * i + 0]);
+        double dy = __dsub_rn(uy, at_build[3 * i + 1]);
+        double dz = __dsub_rn(uz, at_build[3 * i + 2]);
+        s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    // non-negative doubles order like their bit patterns
+    if ((threadIdx.x & 31) == 0 && s > 0.0)
+        atomicMax((unsigned long long *)&status->max_disp2_f64_bits,
+                  (unsigned long long)__double_as_longlong(s));
+}
+
+}  // namespace b2md
+
+using namespace b2md;
+
+B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                 const b2md_box *box, const b2md_grid *grid,
+                                 const int32_t *d_cell_of, const int32_t *d_cell_start,
+                                 const int32_t *d_cell_particles, double r_list, int32_t stride,
+                                 int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
+                                 uint8_t *d_boundary, double boundary_margin,
+                                 b2md_status *d_status, void *stream) {
+    if (n <= 0 || !box || !grid || !d_status) { set_error("b2md_build_nlist: bad arguments"); return -1; }
+    if (stride < 1) { set_error("b2md_build_nlist: stride must be >= 1"); return -2; }
+    if (pitch < n) { set_error("b2md_build_nlist: pitch < n"); return -3; }
+    cudaStream_t s = as_stream(stream);
+    ListGeom g;
+    g.box = make_box_d(box);
+    g.rl2 = r_list * r_list;  // neighbor.py:215
+    double lmax = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        g.nc[a] = grid->ncell[a];
+        g.Lf[a] = (float)box->edge[a];
+        g.Lhi[a] = (float)box->edge[a];
+        g.invLf[a] = (float)(1.0 / box->edge[a]);
+        g.margin[a] = (float)boundary_margin;
+        lmax = fmax(lmax, box->edge[a]);
+    }
+    // guard band of the fp32 pre-test (see dist2_f32)
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double ed = 8.0 * u * lmax;
+    const double band = 4.0 * (3.0 * (2.0 * 1.5 * r_list * ed + ed * ed) + 4.0 * u * 3.0 * g.rl2);
+    g.rl2_in = (float)(g.rl2 - band) * (1.0f - 1e-6f);
+    g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
+    const bool prefilter = band < 0.05 * g.rl2;
+    const unsigned blocks = blocks_for(n, kBuildThreads);
+    if (grid->fallback) {
+        k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, stride, pitch, d_nbr,
+            d_counts, d_boundary, d_status);
+    } else if (prefilter) {
+        k_list_cells<true><<<blocks, kBuildThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_cell_of, d_cell_start,
+            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+    } else {
+        k_list_cells<false><<<blocks, kBuildThreads, 0, s>>>(
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_cell_of, d_cell_start,
+            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+    }
+    if (d_boundary)
+        k_count_boundary<<<blocks_for(n, 256), 256, 0, s>>>(d_boundary, n, d_status);
+    B2MD_CHECK_LAUNCH("b2md_build_nlist");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_snapshot(const void *d_pos_hi, const void *d_pos_lo, const void *d_image,
+                              int64_t n, const b2md_box *box, double *d_at_build_f64,
+                              void *d_ref_pos_f4, void *stream) {
+    if (n <= 0 || !box) { set_error("b2md_snapshot: bad arguments"); return -1; }
+    k_snapshot<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(
+        (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, (const int4 *)d_image, n,
+        make_box_d(box), d_at_build_f64, (float4 *)d_ref_pos_f4);
+    B2MD_CHECK_LAUNCH("b2md_snapshot");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo,
+                                      const void *d_image, int64_t n, const b2md_box *box,
+                                      const double *d_at_build_f64, b2md_status *d_status,
+                                      void *stream) {
+    if (n <= 0 || !box || !d_status) { set_error("b2md_max_displacement: bad arguments"); return -1; }
+    k_max_disp<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(
+        (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, (const int4 *)d_image, n,
+        make_box_d(box), d_at_build_f64, d_status);
+    B2MD_CHECK_LAUNCH("b2md_max_displacement");
+    return 0;
+}

@@ -1,0 +1,381 @@
+"""Simulation assembly on the B200 -- counterpart of reference sim.py.
+
+Same constructor arguments, attributes and policies as the reference
+``Simulation`` (sim.py:35-186): initial force evaluation at construction,
+``integrate -> force -> finalize -> sample`` per step, rebuild when any particle
+moved more than skin/2, stride growth on overflow (at most
+``STRIDE_GROWTH_LIMIT`` times), ``measure()``, ``reset_counters()``.
+
+Two drivers produce bit-identical trajectories:
+
+* ``native=True`` (default for truncated forces without thermostat): the C++
+  step loop of libb2md (csrc/runtime.cu) -- two kernel launches per step, the
+  rebuild test read back asynchronously while the force kernel runs.
+* ``native=False``: the reference's signal/slot loop calling the operator
+  functions one by one (same kernels, one Python call each) -- what the parity
+  tests exercise operator by operator.
+
+Extensions: ``reorder`` ("hilbert" | "cell" | None) re-sorts the device rows at
+rebuild time for gather locality (logical particle order on the HOST side is
+unaffected); ``lj`` may be a :class:`PairTable` (Kob-Andersen etc.).
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .backend import BackendSelector
+from .core import COMPUTE, DeviceState, ParticleState, SignalEngine, SimBox
+from .errors import ConfigError, NeighborOverflowError, SingularPairError
+from .forces import compute_forces_all_to_all, compute_forces_truncated
+from .integrate import IntegratorParams, vv_finalize, vv_integrate
+from .neighbor import (HILBERT_BITS, NeighborList, _round_up, bin_particles,
+                       build_neighbor_list, grid_shape, needs_rebuild, reorder_hilbert)
+from .observables import DETERMINISTIC, FAST, Sample, thermo
+from .potential import LJParams
+
+ALL_TO_ALL = "all_to_all"
+TRUNCATED = "truncated"
+FORCE_MODES = (ALL_TO_ALL, TRUNCATED)
+
+DEFAULT_STRIDE = 64
+DEFAULT_SKIN = 0.5
+STRIDE_GROWTH_LIMIT = 10
+
+_REORDER_MODES = {None: 0, "none": 0, "hilbert": 1, "cell": 2}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Simulation:
+    def __init__(self, state: ParticleState, box: SimBox, lj, dt: float,
+                 backend: BackendSelector | None = None, force_mode: str = ALL_TO_ALL,
+                 skin: float = DEFAULT_SKIN, stride: int = DEFAULT_STRIDE, thermostat=None,
+                 sample_interval: int = 100, deterministic: bool = True,
+                 sample_initial: bool = False, reorder: str | None = "hilbert",
+                 reorder_every: int = 1, native: bool | None = None,
+                 stride_policy: str = "fit"):
+        if force_mode not in FORCE_MODES:
+            raise ConfigError(f"unknown force_mode {force_mode!r}")
+        if force_mode == TRUNCATED and not lj.truncated:
+            raise ConfigError("truncated force mode needs a finite r_cut")
+        if skin < 0.0:
+            raise ConfigError("skin must be non-negative")
+        if thermostat is not None and getattr(thermostat, "rate", 0.0) > 0.0:
+            raise ConfigError("the Andersen thermostat is not part of the B200 hot path yet "
+                              "(SURVEY.md section 8 row f3); run NVE")
+        if reorder not in _REORDER_MODES:
+            raise ConfigError(f"unknown reorder mode {reorder!r}")
+        if stride_policy not in ("fit", "double"):
+            raise ConfigError("stride_policy must be 'fit' or 'double'")
+
+        self.state = state
+        self.box = box
+        self.lj = lj
+        self.integrator = IntegratorParams(dt)
+        self.backend = backend if backend is not None else BackendSelector()
+        self.force_mode = force_mode
+        self.skin = float(skin)
+        self.thermostat = None
+        self.reduction_mode = DETERMINISTIC if deterministic else FAST
+        self.reorder = reorder if force_mode == TRUNCATED else None
+        self.reorder_every = max(int(reorder_every), 1)
+        self.stride_policy = stride_policy
+        self.native = (force_mode == TRUNCATED) if native is None else bool(native)
+        if self.native and force_mode != TRUNCATED:
+            raise ConfigError("the native step loop drives truncated forces only")
+        if not self.native and self.reorder == "cell":
+            raise ConfigError("reorder='cell' is implemented by the native step loop only")
+
+        self._stride = int(stride)
+        self._nlist: NeighborList | None = None
+        self.overflow_events = 0
+        self.force_seconds = 0.0
+        self.nlist_seconds = 0.0
+        self._rebuild_base = 0
+        self._rebuild_total = 0
+        self.samples: list[Sample] = []
+        self.sampling_enabled = True
+        self.kernel_launches = 0
+        self.wasted_force_launches = 0
+        self.reorders = 0
+
+        self.engine = SignalEngine(sample_interval=sample_interval,
+                                   sample_initial=sample_initial)
+        self.engine.connect("integrate", self._integrate_slot)
+        self.engine.connect("force", self._force_slot)
+        self.engine.connect("finalize", self._finalize_slot)
+        self.engine.connect("sample", self._sample_slot)
+
+        self._runner = None
+        self._keep = {}
+        if self.native:
+            self._native_setup()
+        else:
+            self._compute_forces()
+
+    # ------------------------------------------------------------------ slots
+    def _integrate_slot(self):
+        vv_integrate(self.state, self.integrator, self.box)
+
+    def _finalize_slot(self):
+        vv_finalize(self.state, self.integrator)
+
+    def _force_slot(self):
+        self._compute_forces()
+
+    def _sample_slot(self):
+        if self.sampling_enabled:
+            self.samples.append(self.measure())
+
+    # ---------------------------------------------- operator-by-operator path
+    def _compute_forces(self):
+        if self.force_mode == ALL_TO_ALL:
+            t0 = time.perf_counter()
+            compute_forces_all_to_all(self.state, self.lj, self.box, self.backend)
+            self.force_seconds += time.perf_counter() - t0
+            return
+        t0 = time.perf_counter()
+        if self._nlist is None or needs_rebuild(self.state, self.box, self._nlist):
+            self._rebuild()
+        self.nlist_seconds += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        compute_forces_truncated(self.state, self.lj, self.box, self._nlist, self.backend)
+        self.force_seconds += time.perf_counter() - t0
+
+    def _grow_stride(self, max_count: int):
+        if self.stride_policy == "double":
+            self._stride *= 2                       # sim.py:149
+        else:
+            self._stride = max(self._stride + 1, _round_up(int(max_count * 1.125) + 1, 8))
+
+    def _rebuild(self):
+        """bin -> (reorder) -> build, growing the stride on overflow (sim.py:131-149)."""
+        r_list = self.lj.max_r_cut + self.skin
+        if self.reorder == "hilbert" and self._rebuild_total % self.reorder_every == 0:
+            reorder_hilbert(self.state, self.box, HILBERT_BITS, internal=True)
+            self.reorders += 1
+        growths = 0
+        while True:
+            grid = bin_particles(self.state, self.box, r_list)
+            nlist = build_neighbor_list(self.state, grid, r_list, self._stride,
+                                        r_cut=self.lj.max_r_cut, prev=self._nlist,
+                                        backend=self.backend)
+            self._nlist = nlist
+            self._rebuild_total += 1
+            if not nlist.overflow:
+                return
+            self.overflow_events += 1
+            growths += 1
+            if growths > STRIDE_GROWTH_LIMIT:
+                raise NeighborOverflowError(
+                    f"neighbor list still overflows after {growths - 1} "
+                    f"stride growths (stride {self._stride})")
+            self._grow_stride(nlist.max_count)
+
+    # ------------------------------------------------------- native step loop
+    def _alloc_list(self, dev: DeviceState):
+        torch = _torch()
+        pitch = _round_up(dev.n, 32)
+        rows = _round_up(self._stride, 4)
+        # zero-filled: padding entries must stay valid row indices
+        return torch.zeros((rows, pitch), dtype=torch.int32, device=dev.device), pitch
+
+    def _native_setup(self):
+        torch = _torch()
+        dev = self.state.sync_to_compute()
+        n = dev.n
+        r_list = self.lj.max_r_cut + self.skin
+        g = grid_shape(self.box, r_list)
+        d = dict(device=dev.device)
+        lib = _lib.load()
+        k = self._keep
+        k["sets"] = [
+            {name: getattr(dev, name) for name in DeviceState.ROW16 + ("virial",)},
+            {name: torch.zeros_like(getattr(dev, name)) for name in DeviceState.ROW16 + ("virial",)},
+        ]
+        k["sets"][1]["vel"][:, 3] = 1.0
+        k["current"] = 0
+        k["nbr"], pitch = self._alloc_list(dev)
+        k["pitch"] = pitch
+        k["counts"] = torch.zeros(pitch, dtype=torch.int32, **d)
+        k["boundary"] = torch.zeros(pitch, dtype=torch.uint8, **d)
+        k["ref_pos"] = torch.zeros((pitch, 4), dtype=torch.float32, **d)
+        k["at_build"] = torch.zeros((n, 3), dtype=torch.float64, **d)
+        k["cell_of"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["cell_start"] = torch.zeros(int(g.n_cells) + 1, dtype=torch.int32, **d)
+        k["cell_particles"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["bin_scratch"] = torch.zeros(int(lib.b2md_bin_scratch_bytes(n, g.n_cells)),
+                                       dtype=torch.uint8, **d)
+        k["keys"] = torch.zeros(n, dtype=torch.int64, **d)
+        k["keys_tmp"] = torch.zeros(n, dtype=torch.int64, **d)
+        k["perm"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["perm_tmp"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["sort_scratch"] = torch.zeros(int(lib.b2md_sort_scratch_bytes(n)), dtype=torch.uint8, **d)
+        k["table"] = np.ascontiguousarray(self.lj.table(), dtype=np.float64)
+        if self.lj.ntypes > 1:
+            sp = self.state.species.acquire_read("host")
+            if sp.min() < 0 or sp.max() >= self.lj.ntypes:
+                raise ValueError("species out of range for the pair table")
+
+        cfg = _lib.RunnerConfig()
+        cfg.n, cfg.capacity = n, dev.capacity
+        cfg.box = _lib.make_box(self.box.edge_lengths)
+        cfg.dt, cfg.r_cut, cfg.skin = self.integrator.dt, self.lj.max_r_cut, self.skin
+        cfg.ntypes = self.lj.ntypes
+        cfg.reorder_mode = _REORDER_MODES[self.reorder]
+        cfg.reorder_every = self.reorder_every
+        cfg.hilbert_bits = HILBERT_BITS
+        cfg.table = k["table"].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        for name in DeviceState.ROW16 + ("virial",):
+            arr = getattr(cfg, name)
+            arr[0] = k["sets"][0][name].data_ptr()
+            arr[1] = k["sets"][1][name].data_ptr()
+        cfg.current = 0
+        cfg.stride = self._stride
+        cfg.nbr, cfg.pitch = k["nbr"].data_ptr(), pitch
+        for name in ("counts", "boundary", "ref_pos", "at_build", "cell_of", "cell_start",
+                     "cell_particles", "bin_scratch", "keys", "keys_tmp", "perm", "perm_tmp",
+                     "sort_scratch"):
+            setattr(cfg, name, k[name].data_ptr())
+        cfg.status = dev.status.data_ptr()
+        cfg.stream = dev.stream
+        k["cfg"] = cfg
+        dev.reset_status()
+        handle = lib.b2md_runner_create(ctypes.byref(cfg))
+        if not handle:
+            raise _lib.B2mdError("b2md_runner_create failed: "
+                                 + lib.b2md_last_error_string().decode())
+        self._runner = ctypes.c_void_p(handle)
+        self._native_call("b2md_runner_prepare")
+
+    def _native_call(self, name, *args):
+        """Invoke the runner, handling overflow (grow + resume) and singular pairs."""
+        dev = self.state.device_state()
+        done = 0
+        growths = 0
+        while True:
+            rep = _lib.RunReport()
+            t0 = time.perf_counter()
+            if name == "b2md_runner_run":
+                n_steps, finalize = args
+                _lib.call(name, self._runner, n_steps - done, finalize, ctypes.byref(rep))
+            else:
+                _lib.call(name, self._runner, ctypes.byref(rep))
+            self.force_seconds += time.perf_counter() - t0
+            done += rep.steps_done
+            self._absorb(rep, dev)
+            if rep.reason == _lib.RUN_SINGULAR:
+                i, j = rep.singular >> 32, rep.singular & 0xFFFFFFFF
+                ids = dev.particle_ids()
+                i, j = sorted((int(ids[i]), int(ids[j])))
+                raise SingularPairError(i, j)
+            if rep.reason == _lib.RUN_OVERFLOW:
+                self.overflow_events += 1
+                growths += 1
+                if growths > STRIDE_GROWTH_LIMIT:
+                    raise NeighborOverflowError(
+                        f"neighbor list still overflows after {growths - 1} "
+                        f"stride growths (stride {self._stride})")
+                self._grow_stride(rep.max_count)
+                self._keep["nbr"], _ = self._alloc_list(dev)
+                _lib.call("b2md_runner_set_list", self._runner, self._keep["nbr"].data_ptr(),
+                          self._stride)
+                continue
+            return
+
+    def _absorb(self, rep, dev: DeviceState):
+        """Fold a run report into the Python-side bookkeeping."""
+        k = self._keep
+        self._rebuild_total += rep.rebuilds
+        self.reorders += rep.reorders
+        self.kernel_launches += rep.kernel_launches
+        self.wasted_force_launches += rep.wasted_force_launches
+        if rep.reorders:
+            dev.identity_order = False
+        if rep.current != k["current"]:
+            k["current"] = rep.current
+            for name, t in k["sets"][rep.current].items():
+                setattr(dev, name, t)
+        self._max_count = rep.max_count
+        self._n_boundary = rep.n_boundary
+        # the kernels rewrote these buffers in HBM
+        self.state.mark_compute_written("positions", "images", "velocities", "forces",
+                                        "per_particle_potential", "virial")
+
+    def _run_native(self, n_steps: int):
+        eng = self.engine
+        eng._check_ready(n_steps)
+        if n_steps == 0:
+            return
+        # make sure host-side edits since the last call reach the device
+        self.state.sync_to_compute()
+        eng.emit_initial_sample()
+        left = n_steps
+        while left > 0:
+            to_sample = eng.sample_interval - (eng.step_count % eng.sample_interval)
+            chunk = min(left, to_sample)
+            self._native_call("b2md_runner_run", chunk, 1)
+            eng.step_count += chunk
+            left -= chunk
+            if eng.step_count % eng.sample_interval == 0:
+                eng.emit("sample")
+
+    # ------------------------------------------------------------ observation
+    @property
+    def rebuild_count(self) -> int:
+        """Rebuilds since the last counter reset."""
+        return self._rebuild_total - self._rebuild_base
+
+    @property
+    def stride(self) -> int:
+        return self._stride
+
+    def measure(self) -> Sample:
+        """Observe the system now: one device reduction pass, 8 doubles read back."""
+        t = thermo(self.state)
+        return Sample(
+            step=self.engine.step_count,
+            time=self.engine.step_count * self.integrator.dt,
+            potential_energy=t.potential_energy,
+            kinetic_energy=t.kinetic_energy,
+            total_energy=t.potential_energy + t.kinetic_energy,
+            temperature=t.temperature,
+            total_momentum=t.momentum,
+            rebuild_count=self.rebuild_count,
+            virial=t.virial,
+            pressure=t.pressure(self.box.volume),
+            com_velocity=t.com_velocity,
+        )
+
+    def reset_counters(self):
+        """Zero phase timers, overflow events and the rebuild baseline."""
+        self.force_seconds = 0.0
+        self.nlist_seconds = 0.0
+        self.overflow_events = 0
+        self.kernel_launches = 0
+        self.wasted_force_launches = 0
+        self._rebuild_base = self._rebuild_total
+
+    def run(self, n_steps: int):
+        if self.native:
+            self._run_native(n_steps)
+        else:
+            self.engine.run_steps(n_steps)
+
+    def close(self):
+        if self._runner is not None:
+            _lib.load().b2md_runner_destroy(self._runner)
+            self._runner = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass

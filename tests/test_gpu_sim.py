@@ -1,0 +1,187 @@
+"""GPU tests of the assembled step loop (`-m gpu`): the native C++ runner against
+the operator-by-operator loop (bitwise), both against the CPU oracle, energy
+conservation, stride growth, reordering invariance, and size-independent
+properties at a larger N."""
+import numpy as np
+import pytest
+
+import paper_2406_04210_b200 as b2
+from conftest import load_golden
+from helpers import fluid_state, quantize_ds, quantize_f32
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+LJ = b2.make_shifted(1.0, 1.0, 2.5)
+
+
+def lattice_sim(n, native, reorder="hilbert", dt=0.001, skin=0.3, every=20, seed=42, **kw):
+    st, box = b2.init_lattice_any(n, 0.75)
+    b2.init_velocities(st, 1.2, seed)
+    sim = b2.Simulation(st, box, LJ, dt, force_mode=b2.TRUNCATED, skin=skin,
+                        sample_interval=every, sample_initial=True, native=native,
+                        reorder=reorder, **kw)
+    return sim
+
+
+def series(sim):
+    return np.array([[s.potential_energy, s.kinetic_energy, *s.total_momentum, s.virial]
+                     for s in sim.samples])
+
+
+def test_native_loop_equals_operator_loop_bitwise():
+    runs = {}
+    for native in (True, False):
+        sim = lattice_sim(2048, native, reorder=None)
+        sim.run(130)      # not a multiple of the sample interval: exercises the deferred kick
+        sim.run(70)
+        runs[native] = (series(sim), np.array(sim.state.positions.acquire_read(b2.HOST)),
+                        np.array(sim.state.velocities.acquire_read(b2.HOST)),
+                        np.array(sim.state.images.acquire_read(b2.HOST)), sim.rebuild_count)
+        sim.close()
+    for a, b in zip(runs[True][:4], runs[False][:4]):
+        assert np.array_equal(a, b)
+    # the in-loop fp32 displacement test may fire one step before the exact fp64 one
+    assert runs[True][4] >= 2 and abs(runs[True][4] - runs[False][4]) <= 1
+
+
+def test_reordering_does_not_change_the_physics():
+    """Hilbert / cell reordering only permutes rows: energies agree to fp32
+    summation-order noise and the host view stays in logical order."""
+    out = {}
+    for reorder in (None, "hilbert", "cell"):
+        sim = lattice_sim(2048, True, reorder=reorder, every=50)
+        sim.run(100)
+        out[reorder] = (series(sim), np.array(sim.state.positions.acquire_read(b2.HOST)))
+        if reorder:
+            assert sim.reorders >= 1
+            assert not np.array_equal(sim.state.particle_ids(), np.arange(2048))
+        sim.close()
+    for mode in ("hilbert", "cell"):
+        assert np.allclose(out[mode][0][:, :2], out[None][0][:, :2], rtol=2e-6)
+        assert np.max(np.abs(out[mode][1] - out[None][1])) < 1e-3
+
+
+def test_trajectory_tracks_the_reference_run():
+    """Same initial state as the golden reference trajectory (N=500): the first
+    samples agree to fp32 accuracy, the whole series to the chaotic-divergence
+    bound, and total energy is conserved as well as the reference conserves it."""
+    G = load_golden("trajectory")
+    st = b2.ParticleState(G["pos0"], velocities=G["vel0"])
+    box = b2.SimBox(G["edges"])
+    sim = b2.Simulation(st, box, LJ, float(G["dt"]), force_mode=b2.TRUNCATED,
+                        skin=float(G["skin"]), sample_interval=int(G["every"]),
+                        sample_initial=True)
+    sim.run(int(G["steps"]))
+    s = sim.samples
+    assert [x.step for x in s] == list(G["step"])
+    pe = np.array([x.potential_energy for x in s])
+    ke = np.array([x.kinetic_energy for x in s])
+    e_ref = G["pe"] + G["ke"]
+    assert abs(pe[0] - G["pe"][0]) <= 2e-6 * abs(G["pe"][0])
+    assert abs(ke[0] - G["ke"][0]) <= 2e-6 * abs(G["ke"][0])
+    assert np.max(np.abs(pe - G["pe"])) <= 2e-3 * np.abs(G["pe"]).max()
+    drift_ref = np.max(np.abs(e_ref - e_ref[0])) / abs(e_ref[0])
+    drift = np.max(np.abs((pe + ke) - (pe + ke)[0])) / abs((pe + ke)[0])
+    assert drift <= max(3.0 * drift_ref, 2e-5)
+    mom = np.array([x.total_momentum for x in s])
+    assert np.max(np.abs(mom)) <= 1e-3
+    assert abs(sim.samples[-1].rebuild_count - int(G["rebuilds"][-1])) <= 3
+    sim.close()
+
+
+def test_nve_energy_conservation_n4096():
+    """BASELINE config 1 (N=4096, rho=0.75, T0=1.2, rc=2.5, dt=0.001, 1000 steps):
+    the reference drifts 7.6e-06 over this run; bound 3e-5."""
+    sim = lattice_sim(4096, True, every=100)
+    sim.run(1000)
+    e = np.array([s.total_energy for s in sim.samples])
+    assert np.max(np.abs(e - e[0])) / abs(e[0]) <= 3e-5
+    t_end = sim.samples[-1].temperature
+    assert 0.5 < t_end < 1.0          # lattice melts: T relaxes towards ~0.66
+    assert 15 <= sim.rebuild_count <= 40      # reference: 24 per 1000 steps
+    p = np.array(sim.samples[-1].total_momentum)
+    assert np.max(np.abs(p)) <= 1e-2
+    assert sim.kernel_launches >= 2000
+    sim.close()
+
+
+def test_stride_growth_recovers_from_overflow():
+    # DEFAULT_STRIDE-like start that is too small: the list must grow, not truncate
+    for policy, native in (("fit", True), ("double", True), ("fit", False)):
+        sim = lattice_sim(1372, native, stride=16, stride_policy=policy, every=10)
+        assert sim.overflow_events >= 1 and sim.stride >= 66
+        if policy == "double":
+            assert sim.stride in (128,)
+        sim.run(30)
+        e = np.array([s.total_energy for s in sim.samples])
+        assert np.max(np.abs(e - e[0])) / abs(e[0]) <= 1e-5
+        sim.close()
+
+
+def test_stride_growth_limit_raises(monkeypatch):
+    import paper_2406_04210_b200.sim as simmod
+    monkeypatch.setattr(simmod, "STRIDE_GROWTH_LIMIT", 0)      # test_bench.py:207-216 analogue
+    with pytest.raises(b2.NeighborOverflowError):
+        lattice_sim(500, True, stride=8)
+    with pytest.raises(b2.NeighborOverflowError):
+        lattice_sim(500, False, stride=8)
+
+
+def test_singular_pair_surfaces_from_the_native_loop():
+    pos = np.array([[1.0, 1.0, 1.0], [5.0, 5.0, 5.0], [1.0, 1.0, 1.0], [8.0, 2.0, 3.0]])
+    st = b2.ParticleState(pos)
+    with pytest.raises(b2.SingularPairError) as exc:
+        b2.Simulation(st, b2.SimBox.cubic(12.0), LJ, 0.001, force_mode=b2.TRUNCATED, skin=0.3)
+    assert (exc.value.i, exc.value.j) == (0, 2)
+
+
+def test_kob_andersen_mixture_conserves_energy():
+    n = 4000
+    st, box = b2.init_lattice_any(n, 1.2)
+    species = (np.random.default_rng(42).permutation(n) < n // 5).astype(np.int32)
+    st = b2.ParticleState(st.positions.acquire_read(b2.HOST), species=species)
+    b2.init_velocities(st, 1.0, 7)
+    ka = b2.PairTable.kob_andersen()
+    sim = b2.Simulation(st, box, ka, 0.001, force_mode=b2.TRUNCATED, skin=0.3,
+                        sample_interval=50, sample_initial=True)
+    sim.run(400)
+    e = np.array([s.total_energy for s in sim.samples])
+    assert np.max(np.abs(e - e[0])) / abs(e[0]) <= 5e-5
+    # species travel with their particles through every reorder
+    assert np.array_equal(sim.state.species.acquire_read(b2.HOST), species)
+    # against the oracle's fp64 evaluation of the same final configuration
+    pos = np.array(sim.state.positions.acquire_read(b2.HOST))
+    og = orc.bin_particles(pos, box.edge_lengths, ka.max_r_cut + 0.3)
+    onl = orc.build_neighbor_list(pos, np.zeros_like(pos, dtype=np.int64), og,
+                                  ka.max_r_cut + 0.3, 512, r_cut=ka.max_r_cut,
+                                  threads=orc.host_threads())
+    _, rpe, rw = orc.forces_truncated(pos, box.edge_lengths, ka.table(), onl, species=species,
+                                      threads=orc.host_threads())
+    last = sim.samples[-1]
+    assert last.potential_energy == pytest.approx(rpe.sum(), rel=2e-5)
+    assert last.virial == pytest.approx(rw.sum(), rel=2e-4)
+    sim.close()
+
+
+def test_large_system_properties():
+    """Size-independent invariants at N=256k (no oracle run needed): Hilbert keys
+    sorted after a reorder, list symmetric in aggregate, total force ~ 0,
+    momentum conserved, energies finite and extensive."""
+    n = 262_144
+    sim = lattice_sim(n, True, every=50)
+    dev = sim.state.device_state()
+    keys = b2.hilbert_keys(sim.state, sim.box).cpu().numpy()
+    assert np.all(np.diff(keys.astype(np.uint64).astype(np.float64)) >= 0)
+    sim.run(100)
+    s0, s1 = sim.samples[0], sim.samples[-1]
+    assert abs(s1.total_energy - s0.total_energy) <= 2e-5 * abs(s0.total_energy)
+    assert -8.0 * n < s0.potential_energy < -5.0 * n
+    assert np.max(np.abs(s1.total_momentum)) <= 0.05
+    f = sim.state.forces.acquire_read(b2.HOST)
+    assert np.all(np.isfinite(f))
+    assert np.max(np.abs(f.sum(axis=0))) <= 1e-4 * np.abs(f).max() * np.sqrt(n)
+    counts = sim._keep["counts"][:n].cpu().numpy()
+    assert counts.sum() % 2 == 0 and counts.min() > 30 and counts.max() <= sim.stride
+    assert sorted(sim.state.particle_ids().tolist()) == list(range(n))
+    sim.close()

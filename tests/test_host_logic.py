@@ -1,0 +1,163 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+and the host-side mirror of the reference API behaves like the reference
+(error behaviour, residency bookkeeping, signal order).  No kernels run here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2406_04210_b200 as b2
+from paper_2406_04210_b200 import _lib
+from conftest import ROOT, load_golden
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    assert lib.b2md_version() == 100
+    header = open(os.path.join(ROOT, "include", "b2md.h")).read()
+    declared = set(re.findall(r"\b(b2md_[a-z0-9_]+)\(", header))
+    declared -= {"b2md_box", "b2md_grid", "b2md_status"}
+    assert declared, "no declarations parsed"
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in b2md.h but not exported"
+    # and the binding table covers the header
+    assert declared <= set(_lib.exported_symbols()) | {"b2md_runner"}
+
+
+def test_struct_layouts_match_the_header():
+    assert ctypes.sizeof(_lib.Status) == 64
+    assert ctypes.sizeof(_lib.Box) == 24
+    assert ctypes.sizeof(_lib.Grid) == 48
+
+
+def test_grid_shape_host_arithmetic():
+    # test_neighbor.py:30-45 : box (10,8,6), r_list 2 -> 5x4x3 cells
+    from paper_2406_04210_b200.neighbor import grid_shape
+    g = grid_shape(b2.SimBox((10.0, 8.0, 6.0)), 2.0)
+    assert list(g.ncell) == [5, 4, 3] and g.fallback == 0 and g.n_cells == 60
+    assert list(g.cell_edge) == [2.0, 2.0, 2.0]
+    assert grid_shape(b2.SimBox.cubic(5.0), 2.0).fallback == 1
+    NB = load_golden("neighbor")
+    for name in [str(x) for x in NB["names"]]:
+        g = grid_shape(b2.SimBox(NB[f"{name}.edges"]), float(NB[f"{name}.r_list"]))
+        assert list(g.ncell) == list(NB[f"{name}.ncells"])
+        assert np.array_equal(np.array(list(g.cell_edge)), NB[f"{name}.cell_edge"])
+        assert bool(g.fallback) == bool(NB[f"{name}.fallback"])
+    with pytest.raises(b2.ConfigError):
+        grid_shape(b2.SimBox((4.0, 10.0, 10.0)), 4.5)     # test_neighbor.py:76-82
+    with pytest.raises(ValueError):
+        grid_shape(b2.SimBox.cubic(10.0), -1.0)
+
+
+def test_box_validation_and_helpers():
+    with pytest.raises(ValueError):
+        b2.SimBox((1.0, 2.0))
+    with pytest.raises(ValueError):
+        b2.SimBox((1.0, -2.0, 3.0))
+    box = b2.SimBox.cubic(10.0)
+    assert box.volume == 1000.0
+    G = load_golden("integrate")
+    w, k = b2.wrap_position(G["wrap_in"], G["wrap_img"], box)
+    assert np.array_equal(w, G["wrap_out"]) and np.array_equal(k, G["wrap_img_out"])
+    assert np.array_equal(b2.minimum_image(G["mi_in"], box), G["mi_out"])
+
+
+def test_particle_state_validation_and_host_residency():
+    with pytest.raises(ValueError):
+        b2.ParticleState(np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        b2.ParticleState(np.zeros((2, 3)), masses=[1.0, 0.0])
+    st = b2.ParticleState(np.array([[1.0, 2.0, 3.0]]))
+    assert st.n == 1 and set(st.buffers()) >= {
+        "positions", "images", "velocities", "forces", "masses", "species",
+        "per_particle_potential"}
+    buf = st.positions
+    assert buf.valid_on == b2.HOST and buf.version == 0 and buf.copy_count == 0
+    view = buf.acquire_read(b2.HOST)
+    assert not view.flags.writeable
+    buf.acquire_write(b2.HOST)[0, 0] = 4.0
+    assert buf.version == 1 and buf.acquire_read(b2.HOST)[0, 0] == 4.0
+    with pytest.raises(ValueError):
+        buf.acquire_read("gpu")
+    with pytest.raises(ValueError):
+        st.validate(b2.SimBox.cubic(3.5))   # x=4.0 outside [0, 3.5)
+
+
+def test_compute_side_fails_loudly_without_a_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    st = b2.ParticleState(np.zeros((4, 3)))
+    with pytest.raises(_lib.B2mdError):
+        st.positions.acquire_read(b2.COMPUTE)
+    with pytest.raises(_lib.B2mdError):
+        b2.bin_particles(st, b2.SimBox.cubic(10.0), 2.5)
+
+
+def test_backend_selector_rejects_other_kinds():
+    # the reference pins that unknown kinds raise ConfigError (test_backend.py:25-30)
+    assert b2.BackendSelector().kind == "b200"
+    for kind in ("sequential", "parallel", "gpu", "cpu"):
+        with pytest.raises(b2.ConfigError):
+            b2.BackendSelector(kind=kind)
+
+
+def test_potential_shift_and_tables():
+    lj = b2.make_shifted(1.0, 1.0, 2.5)
+    assert lj.energy_shift == pytest.approx(0.016316891136, abs=1e-12)   # test_potential.py:19-23
+    assert lj.energy_shift == float(load_golden("forces")["shift_2p5"])
+    e, f = b2.lj_eval(np.array([1.0, 6.25, 9.0]), lj)
+    assert e[1] == 0.0 and f[2] == 0.0 and e[0] == pytest.approx(lj.energy_shift)
+    with pytest.raises(ValueError):
+        b2.make_shifted(1.0, 1.0, 0.9)
+    ka = b2.PairTable.kob_andersen()
+    tab = ka.table()
+    assert tab.shape == (4, 4) and ka.max_r_cut == 2.5
+    assert np.array_equal(tab[1], tab[2])                      # AB == BA
+    assert tab[1, 0] == 1.5 and tab[3, 1] == pytest.approx(0.88 ** 2)
+    assert np.array_equal(lj.table()[0], b2.PairTable([[1.0]], [[1.0]], [[2.5]]).table()[0])
+    with pytest.raises(ValueError):
+        b2.PairTable([[1.0, 2.0], [3.0, 1.0]], np.ones((2, 2)), 2.5 * np.ones((2, 2)))
+
+
+def test_signal_engine_order_and_sampling():
+    eng = b2.SignalEngine(sample_interval=2, sample_initial=True)
+    trace = []
+    for sig in b2.SignalEngine.SIGNALS:
+        eng.connect(sig, lambda s=sig: trace.append(s))
+    eng.run_steps(3)
+    assert trace == ["sample", "integrate", "force", "finalize",
+                     "integrate", "force", "finalize", "sample",
+                     "integrate", "force", "finalize"]
+    with pytest.raises(b2.ConfigError):
+        b2.SignalEngine(sample_interval=0)
+    with pytest.raises(b2.ConfigError):
+        b2.SignalEngine().run_steps(1)          # no mandatory slots
+    with pytest.raises(b2.ConfigError):
+        eng.connect("nope", lambda: None)
+
+
+def test_initial_conditions_match_reference_generators():
+    G = load_golden("trajectory")
+    st, box = b2.init_lattice_any(int(G["n"]), float(G["density"]))
+    b2.init_velocities(st, 1.2, 42)
+    assert np.array_equal(st.positions.acquire_read(b2.HOST), G["pos0"])
+    assert np.array_equal(st.velocities.acquire_read(b2.HOST), G["vel0"])
+    assert np.array_equal(box.edge_lengths, G["edges"])
+    st, _ = b2.init_lattice_any(256, 0.8)
+    assert np.array_equal(st.positions.acquire_read(b2.HOST), G["lat256"])
+    with pytest.raises(ValueError):
+        b2.init_lattice(100, 0.8)
+
+
+def test_simulation_argument_validation():
+    st, box = b2.init_lattice_any(32, 0.5)
+    lj = b2.make_shifted(1.0, 1.0, 2.5)
+    with pytest.raises(b2.ConfigError):
+        b2.Simulation(st, box, lj, 0.001, force_mode="nope")
+    with pytest.raises(b2.ConfigError):
+        b2.Simulation(st, box, b2.make_shifted(1.0, 1.0), 0.001, force_mode=b2.TRUNCATED)
+    with pytest.raises(b2.ConfigError):
+        b2.Simulation(st, box, lj, 0.001, force_mode=b2.TRUNCATED, skin=-0.1)
