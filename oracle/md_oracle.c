@@ -343,3 +343,45 @@ ORC_API double orc_max_disp2(int64_t n, const double *pos, const int64_t *img,
     }
     return best;
 }
+
+/* Error-scale helper for the fp32 parity metrics (not part of the reference):
+ * per particle, the sums of ABSOLUTE pair contributions over the listed,
+ * in-range neighbours: sum |f_ij| (force magnitude), sum |u_ij|/2, sum |fr*r2|/2.
+ * Dividing an absolute error by these gives a backward-error style relative
+ * error that is insensitive to cancellation between neighbours. */
+ORC_API void orc_pair_scales(int64_t n, const double *pos, const double *edges,
+                             const int32_t *species, int ntypes, const double *table,
+                             int64_t stride, const int32_t *nbr, const int32_t *counts,
+                             double *f_scale, double *u_scale, double *w_scale,
+                             int nthreads) {
+    const double lx = edges[0], ly = edges[1], lz = edges[2];
+    const double ilx = 1.0 / lx, ily = 1.0 / ly, ilz = 1.0 / lz;
+    (void)nthreads;
+#pragma omp parallel for schedule(static, 256) num_threads(nthreads)
+    for (int64_t i = 0; i < n; ++i) {
+        const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+        const int ti = species ? species[i] : 0;
+        const int32_t *row = nbr + i * stride;
+        double fs = 0.0, us = 0.0, ws = 0.0;
+        for (int32_t k = 0; k < counts[i]; ++k) {
+            const int64_t j = row[k];
+            double dx = nearest_image(xi - pos[3 * j], lx, ilx);
+            double dy = nearest_image(yi - pos[3 * j + 1], ly, ily);
+            double dz = nearest_image(zi - pos[3 * j + 2], lz, ilz);
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            const int tj = species ? species[j] : 0;
+            const double *tab = table + 4 * (ti * ntypes + tj);
+            if (r2 >= tab[2] || r2 == 0.0) continue;
+            const double ir2 = 1.0 / r2;
+            const double s6 = (tab[1] * ir2) * (tab[1] * ir2) * (tab[1] * ir2);
+            const double s12 = s6 * s6;
+            const double fr = 24.0 * tab[0] * (2.0 * s12 + s6) * ir2;   /* |repulsive| + |attractive| */
+            fs += fr * sqrt(r2);
+            us += 0.5 * (4.0 * tab[0] * (s12 + s6) + fabs(tab[3]));
+            ws += 0.5 * fr * r2;
+        }
+        f_scale[i] = fs;
+        u_scale[i] = us;
+        w_scale[i] = ws;
+    }
+}

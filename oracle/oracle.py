@@ -317,6 +317,24 @@ def forces_truncated(pos, edges, table, nlist: NList, species=None,
     return f, pe, w
 
 
+def pair_scales(pos, edges, table, nlist: NList, species=None, threads: int = 1):
+    """Per-particle sums of absolute pair contributions (|f|, |u|/2, |w|/2) --
+    the denominators of the backward-error metrics used for the fp32 kernels."""
+    pos = _c(pos, np.float64)
+    n = pos.shape[0]
+    edges = _c(edges, np.float64)
+    table = _c(table, np.float64)
+    ntypes = int(round(math.sqrt(table.shape[0])))
+    sp = None if species is None else _c(species, np.int32)
+    fs, us, ws = (np.zeros(n) for _ in range(3))
+    lib().orc_pair_scales(
+        ctypes.c_int64(n), _p(pos, _f64p), _p(edges, _f64p),
+        _p(sp, _i32p) if sp is not None else None, ctypes.c_int(ntypes), _p(table, _f64p),
+        ctypes.c_int64(nlist.stride), _p(nlist.indices, _i32p), _p(nlist.counts, _i32p),
+        _p(fs, _f64p), _p(us, _f64p), _p(ws, _f64p), ctypes.c_int(threads))
+    return fs, us, ws
+
+
 def forces_all_pairs(pos, edges, table, species=None, threads: int = 1):
     """forces.py:129-138 -> (forces, pe, virial)."""
     pos = _c(pos, np.float64)

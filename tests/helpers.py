@@ -41,25 +41,12 @@ def scalar_rel_error(got, ref, floor_fraction=1e-3):
     return float(np.max(np.abs(got - ref) / np.maximum(denom, np.finfo(np.float64).tiny)))
 
 
-def pair_force_scale(pos, edges, table, nlist_indices, counts, species=None):
-    """sum_j |f_ij| per particle in fp64 (denominator of metric M2)."""
-    pos = np.asarray(pos, dtype=np.float64)
-    edges = np.asarray(edges, dtype=np.float64)
-    n = pos.shape[0]
-    nt = int(round(np.sqrt(table.shape[0])))
-    out = np.zeros(n)
-    for i in range(n):
-        js = nlist_indices[i, :counts[i]].astype(np.int64)
-        d = pos[i] - pos[js]
-        d -= edges * np.rint(d / edges)
-        r2 = (d * d).sum(axis=1)
-        t = (0 if species is None else species[i]) * nt + (0 if species is None else species[js])
-        eps, sig2, rc2 = table[t, 0], table[t, 1], table[t, 2]
-        inside = r2 < rc2
-        s6 = (sig2 / r2) ** 3
-        fr = np.where(inside, 24.0 * eps * (2.0 * s6 * s6 - s6) / r2, 0.0)
-        out[i] = np.sum(np.abs(fr) * np.sqrt(r2))
-    return out
+def backward_error(got, ref, scale):
+    """max_i |got_i - ref_i| / scale_i (vector rows use the max component)."""
+    err = np.abs(np.asarray(got, dtype=np.float64) - np.asarray(ref, dtype=np.float64))
+    if err.ndim == 2:
+        err = err.max(axis=1)
+    return float(np.max(err / np.maximum(scale, 1e-300)))
 
 
 def fluid_state(n, density=0.75, temperature=1.2, seed=42, jitter=0.08):
