@@ -243,10 +243,10 @@ def run_gpu_arm(args):
     def launch_force():
         _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), n, box.c_box(), k["nbr"].data_ptr(),
                   k["counts"].data_ptr(), k["pitch"], rows, k["boundary"].data_ptr(), tab_ptr, 1,
-                  dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
+                  _lib.FORCE_SKIP_THERMO, dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
 
     force_ms = time_kernel(launch_force, 50, torch, stream)
-    force_bytes = n * (36.0 + 4.0 * cbar)          # pos 16 + idx 4*c + force 16 + virial 4
+    force_bytes = n * (32.0 + 4.0 * cbar)          # pos 16 + idx 4*c + force 16 (no-thermo variant)
     peak, peak_src = measured_peak()
     achieved = force_bytes / (force_ms * 1e-3) / 1e9
 

@@ -156,14 +156,18 @@ int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void
  * compute_forces_truncated (forces.py:141-159; kernel 72-110), fp32 pair
  * arithmetic on pos_hi, per-particle energy and virial in registers.
  * table: HOST pointer to ntypes*ntypes rows {eps, sigma^2, rc^2, shift} (fp64;
- * forces.py:119-126 for one type).  `stride` = rows of d_nbr per particle.
+ * forces.py:119-126 for one type).  `stride` = rows of d_nbr per particle (a
+ * multiple of 4).  flags: B2MD_FORCE_SKIP_THERMO leaves e_pot / virial unwritten
+ * (intermediate steps of the native loop, where nobody can observe them).
  * d_boundary (may be NULL = all) selects the exact-image-shift path per warp.
  * Writes force (xyz + e_pot in w) and virial.
  * A coincident listed pair is reported in status->singular. */
+#define B2MD_FORCE_SKIP_THERMO 1
 int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                   const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
                   int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
-                  void *d_force_f4, float *d_virial, b2md_status *d_status, void *stream);
+                  int32_t flags, void *d_force_f4, float *d_virial, b2md_status *d_status,
+                  void *stream);
 
 /* compute_forces_all_to_all (forces.py:129-138; kernel 29-69): shared-memory
  * tiled all-pairs scan, same outputs. */

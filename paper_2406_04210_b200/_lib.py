@@ -78,6 +78,7 @@ class RunReport(Structure):
 
 
 RUN_DONE, RUN_OVERFLOW, RUN_SINGULAR = 0, 1, 2
+FORCE_SKIP_THERMO = 1
 
 _P = c_void_p
 _SIGNATURES = {
@@ -108,7 +109,7 @@ _SIGNATURES = {
     "b2md_snapshot": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),
     "b2md_max_displacement": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),
     "b2md_force_lj": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, c_int32, _P,
-                                POINTER(c_double), c_int32, _P, _P, _P, _P]),
+                                POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_force_lj_all_pairs": (c_int32, [_P, c_int64, POINTER(Box), POINTER(c_double), c_int32,
                                           _P, _P, _P, _P]),
     "b2md_vv_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,

@@ -48,6 +48,13 @@ struct ForceArgs {
     float2 tab_b[kMaxTypes * kMaxTypes];   // half_shift, c_w
 };
 
+// 1/x to 1 ulp on the SFU (MUFU.RCP), no IEEE slow path
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float rint_small(float q) {
     // round-half-even for |q| < 2^22 on the FMA pipe (no FRND / conversion pipe)
     const float magic = 12582912.0f;  // 1.5 * 2^23
@@ -70,10 +77,14 @@ struct RowAcc {
 };
 
 // Single-type pair: prefactors deferred.  `in` false => contributes exact zeros.
+// THERMO = false drops the energy / virial / count accumulators (intermediate
+// steps of the native loop, whose per-particle energies nobody can observe).
+template <bool THERMO>
 __device__ __forceinline__ void lj_pair_single(RowAcc &acc, float dx, float dy, float dz, float r2,
                                                bool valid, const PairParams &p) {
     const bool in = valid && (r2 < p.rc2);
-    const float ir2 = in ? __frcp_rn(r2) : 0.0f;
+    const float rc = rcp_fast(r2);
+    const float ir2 = in ? rc : 0.0f;
     const float s2 = p.sig2 * ir2;
     const float s6 = s2 * s2 * s2;
     const float t = s6 * fmaf(2.0f, s6, -1.0f);        // s6*(2 s6 - 1) = fr*r2 / (24 eps)
@@ -81,15 +92,19 @@ __device__ __forceinline__ void lj_pair_single(RowAcc &acc, float dx, float dy, 
     acc.fx = fmaf(g, dx, acc.fx);
     acc.fy = fmaf(g, dy, acc.fy);
     acc.fz = fmaf(g, dz, acc.fz);
-    acc.u = fmaf(s6, s6 - 1.0f, acc.u);                // (s12 - s6)
-    acc.w += t;
-    acc.cnt += in ? 1 : 0;
+    if (THERMO) {
+        acc.u = fmaf(s6, s6 - 1.0f, acc.u);            // (s12 - s6)
+        acc.w += t;
+        acc.cnt += in ? 1 : 0;
+    }
 }
 
+template <bool THERMO>
 __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, float dz, float r2,
                                               bool valid, const float4 pa, const float2 pb) {
     const bool in = valid && (r2 < pa.y);
-    const float ir2 = in ? __frcp_rn(r2) : 0.0f;
+    const float rc = rcp_fast(r2);
+    const float ir2 = in ? rc : 0.0f;
     const float s2 = pa.x * ir2;
     const float s6 = s2 * s2 * s2;
     const float t = s6 * fmaf(2.0f, s6, -1.0f);
@@ -97,43 +112,58 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
     acc.fx = fmaf(g, dx, acc.fx);
     acc.fy = fmaf(g, dy, acc.fy);
     acc.fz = fmaf(g, dz, acc.fz);
-    acc.u = fmaf(pa.w * s6, s6 - 1.0f, acc.u);
-    acc.u += in ? pb.x : 0.0f;
-    acc.w = fmaf(pb.y, t, acc.w);
+    if (THERMO) {
+        acc.u = fmaf(pa.w * s6, s6 - 1.0f, acc.u);
+        acc.u += in ? pb.x : 0.0f;
+        acc.w = fmaf(pb.y, t, acc.w);
+    }
 }
 
-template <bool CAREFUL, bool TABLE>
-__device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int kmax,
-                                         int stride, const int32_t *__restrict__ col,
+// Four neighbours per trip: indices first (coalesced, streaming), then the four
+// position gathers, then the arithmetic.  CHECK = false is used for the leading
+// trips in which every lane of the warp still has valid entries.
+template <bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
+__device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, int k,
+                                         const int32_t *__restrict__ col, int64_t pitch,
+                                         const float4 *__restrict__ pos, const ForceArgs &a,
+                                         const float4 *s_tab_a, const float2 *s_tab_b,
+                                         int ti_row) {
+    const BoxF &b = a.box;
+    int j[4];
+    float4 pj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) j[u] = __ldcs(col + (int64_t)u * pitch);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<CAREFUL>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<CAREFUL>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const bool valid = CHECK ? (k + u) < cnt : true;
+        if (TABLE) {
+            const int t = ti_row + __float_as_int(pj[u].w);
+            lj_pair_table<THERMO>(acc, dx, dy, dz, r2, valid, s_tab_a[t], s_tab_b[t]);
+        } else {
+            lj_pair_single<THERMO>(acc, dx, dy, dz, r2, valid, a.single);
+        }
+    }
+}
+
+template <bool CAREFUL, bool TABLE, bool THERMO>
+__device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int kmin4,
+                                         int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
                                          const ForceArgs &a, const float4 *s_tab_a,
                                          const float2 *s_tab_b, int ti_row) {
-    const BoxF &b = a.box;
-    for (int k = 0; k < kmax; k += 4) {
-        int j[4];
-        float4 pj[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int kk = min(k + u, stride - 1);
-            j[u] = __ldcs(col + (int64_t)kk * pitch);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-            const float dy = delta<CAREFUL>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-            const float dz = delta<CAREFUL>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const bool valid = (k + u) < cnt;
-            if (TABLE) {
-                const int t = ti_row + __float_as_int(pj[u].w);
-                lj_pair_table(acc, dx, dy, dz, r2, valid, s_tab_a[t], s_tab_b[t]);
-            } else {
-                lj_pair_single(acc, dx, dy, dz, r2, valid, a.single);
-            }
-        }
-    }
+    int k = 0;
+    for (; k < kmin4; k += 4, col += 4 * pitch)
+        row_trip<CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, k, col, pitch, pos, a, s_tab_a,
+                                                s_tab_b, ti_row);
+    for (; k < kmax; k += 4, col += 4 * pitch)
+        row_trip<CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, k, col, pitch, pos, a, s_tab_a,
+                                               s_tab_b, ti_row);
 }
 
 // Rare path: find the first listed j at zero separation (forces.py:94-97).
@@ -155,11 +185,11 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
-template <bool TABLE>
+template <bool TABLE, bool THERMO>
 __global__ void __launch_bounds__(kForceThreads)
 k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
-           int stride, const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
+           const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
            float *__restrict__ virial, b2md_status *status) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
@@ -176,15 +206,19 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ Fo
     const float4 pi = pos[i];
     const int cnt = active ? counts[i] : 0;
     const int kmax = __reduce_max_sync(0xffffffffu, cnt);
+    // trips in which no lane needs a validity test (inactive lanes do not count)
+    const int kmin4 = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff) & ~3;
     const bool careful = boundary ? (__any_sync(0xffffffffu, active && boundary[i] != 0)) : true;
     const int32_t *col = nbr + i;
     const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     if (careful)
-        row_loop<true, TABLE>(acc, pi, cnt, kmax, stride, col, pitch, pos, a, s_tab_a, s_tab_b, ti_row);
+        row_loop<true, TABLE, THERMO>(acc, pi, cnt, min(kmin4, kmax), kmax, col, pitch, pos, a,
+                                      s_tab_a, s_tab_b, ti_row);
     else
-        row_loop<false, TABLE>(acc, pi, cnt, kmax, stride, col, pitch, pos, a, s_tab_a, s_tab_b, ti_row);
+        row_loop<false, TABLE, THERMO>(acc, pi, cnt, min(kmin4, kmax), kmax, col, pitch, pos, a,
+                                       s_tab_a, s_tab_b, ti_row);
 
     if (!active) return;
     float fx, fy, fz, u, w;
@@ -197,8 +231,8 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ Fo
         w = p.c_w * acc.w;
     }
     force[i] = make_float4(fx, fy, fz, u);
-    if (virial) virial[i] = w;
-    if (!(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(u)))
+    if (THERMO && virial) virial[i] = w;
+    if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
         report_singular((int)i, pi, cnt, col, pitch, pos, a.box, status);
 }
 
@@ -242,9 +276,9 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
             const bool valid = !self && r2 != 0.0f;
             if (TABLE) {
                 const int tt = ti_row + __float_as_int(pj.w);
-                lj_pair_table(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
+                lj_pair_table<true>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
             } else {
-                lj_pair_single(acc, dx, dy, dz, r2, valid, a.single);
+                lj_pair_single<true>(acc, dx, dy, dz, r2, valid, a.single);
             }
         }
     }
@@ -295,25 +329,32 @@ using namespace b2md;
 B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                               const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
                               int32_t stride, const uint8_t *d_boundary, const double *table,
-                              int32_t ntypes, void *d_force_f4, float *d_virial,
+                              int32_t ntypes, int32_t flags, void *d_force_f4, float *d_virial,
                               b2md_status *d_status, void *stream) {
     if (n <= 0 || !d_nbr || !d_counts || !d_status || stride < 1) {
         set_error("b2md_force_lj: bad arguments");
         return -1;
+    }
+    if (stride % 4 != 0) {
+        set_error("b2md_force_lj: the list must be allocated with a multiple of 4 rows");
+        return -3;
     }
     ForceArgs a;
     int rc = fill_args(a, box, table, ntypes);
     if (rc) return rc;
     const unsigned blocks = blocks_for(n, kForceThreads);
     cudaStream_t s = as_stream(stream);
-    if (ntypes == 1)
-        k_force_lj<false><<<blocks, kForceThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, stride, d_boundary,
-            (float4 *)d_force_f4, d_virial, d_status);
-    else
-        k_force_lj<true><<<blocks, kForceThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, stride, d_boundary,
-            (float4 *)d_force_f4, d_virial, d_status);
+    const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
+#define B2MD_LAUNCH_FORCE(TABLE, THERMO)                                                     \
+    k_force_lj<TABLE, THERMO><<<blocks, kForceThreads, 0, s>>>(                              \
+        (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary,                  \
+        (float4 *)d_force_f4, d_virial, d_status)
+    if (ntypes == 1) {
+        if (thermo) B2MD_LAUNCH_FORCE(false, true); else B2MD_LAUNCH_FORCE(false, false);
+    } else {
+        if (thermo) B2MD_LAUNCH_FORCE(true, true); else B2MD_LAUNCH_FORCE(true, false);
+    }
+#undef B2MD_LAUNCH_FORCE
     B2MD_CHECK_LAUNCH("b2md_force_lj");
     return 0;
 }

@@ -151,6 +151,130 @@ k_list_cells(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_l
     finish_row(nbr, pitch, i, active, found, stride, counts, status);
 }
 
+// ---------------------------------------------------------------------------
+// Production build kernel: one warp per cell, lane = particle of that cell.
+//
+// The 27 neighbour cells are visited in the reference's order; each neighbour
+// cell's occupants are staged 32 at a time in shared memory as fp32 high words
+// already shifted by the periodic image of that cell (so the inner loop needs no
+// minimum-image arithmetic), then every lane walks the staged candidates by
+// shared-memory broadcast.  The fp32 squared distance only pre-sorts candidates
+// into certainly-out / certainly-in / in-band; in-band candidates (a shell a few
+// 1e-5 sigma thick) take the exact fp64 test of listed_f64, so rows are
+// bit-identical to the reference.  Rows are collected in shared memory
+// ([k][lane] layout, conflict-free), sorted there, and written to the
+// column-major list with all lanes storing the same k together.
+constexpr int kCellWarps = 4;
+
+struct CellShift { float x, y, z; };
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
+                  ListGeom g, int64_t n_cells, const int32_t *__restrict__ cell_start,
+                  const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
+                  int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
+                  uint8_t *__restrict__ boundary, b2md_status *status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4 *s_cand = reinterpret_cast<float4 *>(smem_raw) + warp * 32;
+    int32_t *s_rows = reinterpret_cast<int32_t *>(smem_raw + WARPS * 32 * sizeof(float4)) +
+                      (size_t)warp * stride * 32;
+    const int64_t c = (int64_t)blockIdx.x * WARPS + warp;
+    int wanted_max = 0;
+    if (c < n_cells) {
+        const int cz = (int)(c % g.nc[2]);
+        const int cy = (int)((c / g.nc[2]) % g.nc[1]);
+        const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
+        const int i_begin = cell_start[c], i_end = cell_start[c + 1];
+        for (int i0 = i_begin; i0 < i_end; i0 += 32) {
+            const bool active = i0 + lane < i_end;
+            const int i = active ? cell_particles[i0 + lane] : -1;
+            const float4 hi_i = active ? pos_hi[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            int found = 0;
+            for (int ox = -1; ox <= 1; ++ox) {
+                int jx = cx + ox;
+                float sx = 0.f;
+                if (jx < 0) { jx += g.nc[0]; sx = -g.Lf[0]; }
+                else if (jx >= g.nc[0]) { jx -= g.nc[0]; sx = g.Lf[0]; }
+                for (int oy = -1; oy <= 1; ++oy) {
+                    int jy = cy + oy;
+                    float sy = 0.f;
+                    if (jy < 0) { jy += g.nc[1]; sy = -g.Lf[1]; }
+                    else if (jy >= g.nc[1]) { jy -= g.nc[1]; sy = g.Lf[1]; }
+                    for (int oz = -1; oz <= 1; ++oz) {
+                        int jz = cz + oz;
+                        float sz = 0.f;
+                        if (jz < 0) { jz += g.nc[2]; sz = -g.Lf[2]; }
+                        else if (jz >= g.nc[2]) { jz -= g.nc[2]; sz = g.Lf[2]; }
+                        const int cj = (jx * g.nc[1] + jy) * g.nc[2] + jz;
+                        const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
+                        for (int p0 = p_begin; p0 < p_end; p0 += 32) {
+                            const int m = min(32, p_end - p0);
+                            __syncwarp();
+                            if (lane < m) {
+                                const int j = cell_particles[p0 + lane];
+                                const float4 hj = __ldg(&pos_hi[j]);
+                                s_cand[lane] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
+                                                           __int_as_float(j));
+                            }
+                            __syncwarp();
+                            if (active) {
+                                for (int t = 0; t < m; ++t) {
+                                    const float4 cnd = s_cand[t];
+                                    const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y,
+                                                dz = hi_i.z - cnd.z;
+                                    const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                                    if (r2f <= g.rl2_out) {
+                                        const int j = __float_as_int(cnd.w);
+                                        if (j != i) {
+                                            bool hit = r2f < g.rl2_in;
+                                            if (!hit) {   // in the guard band: exact decision
+                                                const float4 lo_i = pos_lo[i];
+                                                const double pi[3] = {ds_to_double(hi_i.x, lo_i.x),
+                                                                      ds_to_double(hi_i.y, lo_i.y),
+                                                                      ds_to_double(hi_i.z, lo_i.z)};
+                                                hit = listed_f64(pi, pos_hi[j], pos_lo[j], g);
+                                            }
+                                            if (hit) {
+                                                if (found < stride) s_rows[found * 32 + lane] = j;
+                                                ++found;
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            // ---- sort the kept prefix (neighbor.py:152) and publish the rows
+            const int kept = min(found, stride);
+            for (int a = 1; a < kept; ++a) {
+                const int v = s_rows[a * 32 + lane];
+                int b = a - 1;
+                while (b >= 0 && s_rows[b * 32 + lane] > v) {
+                    s_rows[(b + 1) * 32 + lane] = s_rows[b * 32 + lane];
+                    --b;
+                }
+                s_rows[(b + 1) * 32 + lane] = v;
+            }
+            const int kmax = __reduce_max_sync(0xffffffffu, kept);
+            for (int k = 0; k < kmax; ++k)
+                if (k < kept) nbr[(int64_t)k * pitch + i] = s_rows[k * 32 + lane];
+            if (active) {
+                counts[i] = kept;
+                if (boundary) boundary[i] = boundary_flag(hi_i, g);
+            }
+            wanted_max = max(wanted_max, __reduce_max_sync(0xffffffffu, found));
+        }
+    }
+    if (lane == 0 && wanted_max > 0) {
+        if (wanted_max > stride) atomicExch(&status->overflow, 1);
+        atomicMax(&status->max_count, wanted_max);
+    }
+}
+
 // All-pairs scan for grids with fewer than three cells on some axis.
 __global__ void __launch_bounds__(kBuildThreads)
 k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
@@ -259,10 +383,37 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
     g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n, kBuildThreads);
+    const size_t warp_smem = 32 * sizeof(float4) + (size_t)stride * 32 * sizeof(int32_t);
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, stride, pitch, d_nbr,
             d_counts, d_boundary, d_status);
+    } else if (prefilter && warp_smem * 2 <= 200 * 1024) {
+        // warp-per-cell kernel; fewer warps per CTA when rows are long
+        const int64_t nc = grid->n_cells;
+        if (warp_smem * kCellWarps <= 96 * 1024) {
+            const size_t smem = warp_smem * kCellWarps;
+            static bool attr4 = false;
+            if (!attr4) {
+                cudaFuncSetAttribute(k_list_cells_warp<kCellWarps>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                attr4 = true;
+            }
+            k_list_cells_warp<kCellWarps><<<blocks_for(nc, kCellWarps), kCellWarps * 32, smem, s>>>(
+                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, nc, d_cell_start,
+                d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+        } else {
+            const size_t smem = warp_smem * 2;
+            static bool attr2 = false;
+            if (!attr2) {
+                cudaFuncSetAttribute(k_list_cells_warp<2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                attr2 = true;
+            }
+            k_list_cells_warp<2><<<blocks_for(nc, 2), 64, smem, s>>>(
+                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, nc, d_cell_start,
+                d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+        }
     } else if (prefilter) {
         k_list_cells<true><<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_cell_of, d_cell_start,

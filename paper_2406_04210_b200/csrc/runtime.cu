@@ -61,12 +61,14 @@ int read_status(b2md_runner *r) {
     return check_cuda(cudaStreamSynchronize(s), "status sync");
 }
 
-int launch_force(b2md_runner *r) {
+// thermo = false on steps whose per-particle energies cannot be observed
+int launch_force(b2md_runner *r, bool thermo) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     r->launches += 1;
     return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, (c.stride + 3) / 4 * 4,
-                         c.boundary, r->table.data(), c.ntypes, a.force, a.virial, c.status,
+                         c.boundary, r->table.data(), c.ntypes,
+                         thermo ? 0 : B2MD_FORCE_SKIP_THERMO, a.force, a.virial, c.status,
                          c.stream);
 }
 
@@ -201,7 +203,7 @@ B2MD_EXPORT int b2md_runner_prepare(b2md_runner *r, b2md_run_report *rep) {
         finish_report(r, rep, before);
         return 0;
     }
-    if ((rc = launch_force(r))) return rc;
+    if ((rc = launch_force(r, true))) return rc;
     if ((rc = read_status(r))) return rc;
     r->mid_step = false;
     rep->singular = r->h_status->singular;
@@ -230,7 +232,7 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
             finish_report(r, rep, before);
             return 0;
         }
-        if ((rc = launch_force(r))) return rc;
+        if ((rc = launch_force(r, rep->steps_done + 1 >= n_steps))) return rc;
         r->mid_step = false;
         r->pending_kick = true;
         rep->steps_done += 1;
@@ -250,7 +252,9 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
                                              cudaMemcpyDeviceToHost, s), "flag read-back")))
             return rc;
         if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
-        if ((rc = launch_force(r))) return rc;             // speculative
+        // energies / virial only on the step the caller can observe (the last one)
+        const bool thermo = rep->steps_done + 1 >= n_steps;
+        if ((rc = launch_force(r, thermo))) return rc;     // speculative
         if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
         rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
         if (r->h_status->singular != ~0ull) {
@@ -273,7 +277,7 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
                 finish_report(r, rep, before);
                 return 0;
             }
-            if ((rc = launch_force(r))) return rc;
+            if ((rc = launch_force(r, thermo))) return rc;
         }
         r->pending_kick = true;
         rep->steps_done += 1;

@@ -67,7 +67,7 @@ def compute_forces_truncated(state: ParticleState, params, box: SimBox, nlist: N
         dev.reset_status()
     _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), dev.n, box.c_box(),
               nlist.d_nbr.data_ptr(), nlist.d_counts.data_ptr(), nlist.pitch,
-              nlist.d_nbr.shape[0], nlist.d_boundary.data_ptr(), tab_ptr, nt,
+              nlist.d_nbr.shape[0], nlist.d_boundary.data_ptr(), tab_ptr, nt, 0,
               dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
     state.mark_compute_written("forces", "per_particle_potential", "virial")
     if check:

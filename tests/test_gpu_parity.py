@@ -311,8 +311,8 @@ def check_forces(pos, edges, params, r_list, species=None, stride=256):
     fs, us, ws = orc.pair_scales(pos, edges, table, onl, species=species,
                                  threads=orc.host_threads())
     m = force_error_metrics(f, rf, fs)
-    assert m["M2"] <= FORCE_TOL, m
-    assert m["M3"] <= FORCE_TOL, m
+    assert m["M2"] <= FORCE_TOL, m      # error / sum_j |f_ij|
+    assert m["M1"] <= FORCE_TOL, m      # error / max(|F_i|, 1e-3 max_j |F_j|)
     assert backward_error(pe, rpe, us) <= FORCE_TOL
     assert backward_error(w, rw, ws) <= FORCE_TOL
     # totals (what measure() reports) are far tighter
