@@ -211,12 +211,16 @@ int b2md_thermo(const void *d_vel, const void *d_force_f4, const float *d_virial
 /* -------------------------------------------- reorder (Hilbert / cell order)
  * reorder_by_cell (neighbor.py:257-270) generalised: 64-bit keys, stable LSD
  * radix sort, gather of every per-particle array.
- * b2md_hilbert_keys: 3*bits-bit Hilbert index of floor(pos * 2^bits / L).
+ * b2md_hilbert_keys: Hilbert index of the cell-aligned coordinate
+ *   (cell << sub_bits) | floor(frac_in_cell * 2^sub_bits) per axis, cell = exactly
+ *   bin_particles' cell coordinate, so each cell's particles become contiguous;
+ *   b2md_hilbert_key_bits returns the number of significant key bits (<= 63).
  * b2md_cell_keys: key = flat cell index (exactly reorder_by_cell's order).
  * b2md_sort_pairs_u64: stable; on return keys/values are in d_keys/d_vals.
  * b2md_gather16 / b2md_gather4: dst[k] = src[perm[k]] for 16- / 4-byte rows. */
+int b2md_hilbert_key_bits(const b2md_grid *grid, int32_t sub_bits);
 int b2md_hilbert_keys(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
-                      const b2md_box *box, int32_t bits, uint64_t *d_keys, void *stream);
+                      const b2md_grid *grid, int32_t sub_bits, uint64_t *d_keys, void *stream);
 int b2md_cell_keys(const int32_t *d_cell_of, int64_t n, uint64_t *d_keys, void *stream);
 int b2md_iota_i32(int32_t *d_vals, int64_t n, void *stream);
 int64_t b2md_sort_scratch_bytes(int64_t n);
@@ -251,7 +255,7 @@ typedef struct b2md_runner_config {
     int32_t ntypes;
     int32_t reorder_mode;        /* 0 none, 1 Hilbert, 2 cell order */
     int32_t reorder_every;       /* reorder on every k-th rebuild (>= 1) */
-    int32_t hilbert_bits;
+    int32_t hilbert_bits;        /* sub-cell bits per axis of the Hilbert key */
     const double *table;         /* HOST, ntypes*ntypes*4, copied at create */
     void *pos_hi[2], *pos_lo[2], *vel[2], *force[2], *image[2];
     float *virial[2];

@@ -451,19 +451,29 @@ def thermo(vel, masses, pe, virial=None, deterministic: bool = True):
 # Hilbert keys (extension; north_star subsystem 2)
 # --------------------------------------------------------------------------
 
-HILBERT_BITS = 21
+HILBERT_SUB_BITS = 2
 
 
-def hilbert_cell_coords(pos, edges, bits: int = HILBERT_BITS):
-    """Quantise wrapped fp64 positions onto a 2^bits grid per axis:
-    q = min(int(floor(pos * (2^bits / L))), 2^bits - 1), in fp64, one multiply."""
+def hilbert_cell_coords(pos, edges, r_list, sub_bits: int = HILBERT_SUB_BITS):
+    """Cell-aligned integer coordinates q = (cell << sub_bits) | sub, with
+    cell = bin_particles' cell coordinate (fp64 division + clip) and
+    sub = clip(floor(fp32((pos - cell*edge)) * fp32(1/edge) * 2^sub_bits)).
+    Returns (q (n,3) uint64, bits per axis)."""
     pos = np.asarray(pos, dtype=np.float64)
-    scale = float(1 << bits) / np.asarray(edges, dtype=np.float64)
-    q = np.floor(pos * scale).astype(np.int64)
-    return np.minimum(np.maximum(q, 0), (1 << bits) - 1).astype(np.uint64)
+    ncells, cell_edge = grid_shape(edges, r_list)
+    cell = np.floor(pos / cell_edge).astype(np.int64)
+    cell = np.minimum(np.maximum(cell, 0), ncells - 1)
+    frac = (pos - cell * cell_edge).astype(np.float32) * (1.0 / cell_edge).astype(np.float32)
+    sub = np.floor(frac * np.float32(1 << sub_bits)).astype(np.int64)
+    sub = np.minimum(np.maximum(sub, 0), (1 << sub_bits) - 1)
+    cell_bits = 1
+    while (1 << cell_bits) < int(ncells.max()):
+        cell_bits += 1
+    q = (cell << sub_bits) | sub
+    return q.astype(np.uint64), cell_bits + sub_bits
 
 
-def hilbert_keys(q, bits: int = HILBERT_BITS):
+def hilbert_keys(q, bits: int):
     """3-D Hilbert index (Skilling 2004 transpose form) of integer coords
     q (n,3) with `bits` bits per axis -> uint64 keys of 3*bits bits.  The key
     interleaves the transposed words MSB first as x,y,z."""
@@ -499,8 +509,9 @@ def hilbert_keys(q, bits: int = HILBERT_BITS):
     return key
 
 
-def hilbert_permutation(pos, edges, bits: int = HILBERT_BITS):
-    keys = hilbert_keys(hilbert_cell_coords(pos, edges, bits), bits)
+def hilbert_permutation(pos, edges, r_list, sub_bits: int = HILBERT_SUB_BITS):
+    q, bits = hilbert_cell_coords(pos, edges, r_list, sub_bits)
+    keys = hilbert_keys(q, bits)
     return np.argsort(keys, kind="stable"), keys
 
 

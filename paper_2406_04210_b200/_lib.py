@@ -121,7 +121,8 @@ _SIGNATURES = {
     "b2md_reduce_sum_f64": (c_int32, [_P, c_int64, _P, _P, _P]),
     "b2md_thermo_scratch_bytes": (c_int64, [c_int64]),
     "b2md_thermo": (c_int32, [_P, _P, _P, c_int64, _P, _P, _P]),
-    "b2md_hilbert_keys": (c_int32, [_P, _P, c_int64, POINTER(Box), c_int32, _P, _P]),
+    "b2md_hilbert_key_bits": (c_int32, [POINTER(Grid), c_int32]),
+    "b2md_hilbert_keys": (c_int32, [_P, _P, c_int64, POINTER(Grid), c_int32, _P, _P]),
     "b2md_cell_keys": (c_int32, [_P, c_int64, _P, _P]),
     "b2md_iota_i32": (c_int32, [_P, c_int64, _P]),
     "b2md_sort_scratch_bytes": (c_int64, [c_int64]),
@@ -137,7 +138,7 @@ _SIGNATURES = {
 
 #: entry points that report errors through their int return value
 _CHECKED = {name for name, (res, _) in _SIGNATURES.items()
-            if res is c_int32 and name != "b2md_version"}
+            if res is c_int32 and name not in ("b2md_version", "b2md_hilbert_key_bits")}
 
 _lib = None
 

@@ -119,20 +119,18 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
     }
 }
 
-// Four neighbours per trip: indices first (coalesced, streaming), then the four
-// position gathers, then the arithmetic.  CHECK = false is used for the leading
-// trips in which every lane of the warp still has valid entries.
+// Four neighbours per trip.  The index stream comes from HBM (it is the bulk of
+// the kernel's traffic), so it is software-pipelined two trips ahead: while trip t
+// does its four position gathers and the arithmetic, the indices of trips t+1 and
+// t+2 are already in flight (8 coalesced 4-byte loads per thread).  CHECK = false
+// is used for the leading trips in which every lane still has valid entries.
 template <bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
 __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, int k,
-                                         const int32_t *__restrict__ col, int64_t pitch,
-                                         const float4 *__restrict__ pos, const ForceArgs &a,
-                                         const float4 *s_tab_a, const float2 *s_tab_b,
-                                         int ti_row) {
+                                         const int (&j)[4], const float4 *__restrict__ pos,
+                                         const ForceArgs &a, const float4 *s_tab_a,
+                                         const float2 *s_tab_b, int ti_row) {
     const BoxF &b = a.box;
-    int j[4];
     float4 pj[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) j[u] = __ldcs(col + (int64_t)u * pitch);
 #pragma unroll
     for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
 #pragma unroll
@@ -157,13 +155,27 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
                                          int64_t pitch, const float4 *__restrict__ pos,
                                          const ForceArgs &a, const float4 *s_tab_a,
                                          const float2 *s_tab_b, int ti_row) {
-    int k = 0;
-    for (; k < kmin4; k += 4, col += 4 * pitch)
-        row_trip<CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, k, col, pitch, pos, a, s_tab_a,
-                                                s_tab_b, ti_row);
-    for (; k < kmax; k += 4, col += 4 * pitch)
-        row_trip<CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, k, col, pitch, pos, a, s_tab_a,
-                                               s_tab_b, ti_row);
+    int ja[4], jb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        ja[u] = (0 < kmax) ? __ldcs(col + (int64_t)u * pitch) : 0;
+        jb[u] = (4 < kmax) ? __ldcs(col + (int64_t)(4 + u) * pitch) : 0;
+    }
+    for (int k = 0; k < kmax; k += 4) {
+        int jc[4];
+        const bool more = k + 8 < kmax;          // warp-uniform
+#pragma unroll
+        for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (int64_t)(8 + u) * pitch) : 0;
+        if (k < kmin4)
+            row_trip<CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, k, ja, pos, a, s_tab_a, s_tab_b,
+                                                    ti_row);
+        else
+            row_trip<CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, k, ja, pos, a, s_tab_a, s_tab_b,
+                                                   ti_row);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { ja[u] = jb[u]; jb[u] = jc[u]; }
+        col += 4 * pitch;
+    }
 }
 
 // Rare path: find the first listed j at zero separation (forces.py:94-97).
@@ -186,7 +198,7 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
 }
 
 template <bool TABLE, bool THERMO>
-__global__ void __launch_bounds__(kForceThreads)
+__global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
            const uint8_t *__restrict__ boundary, float4 *__restrict__ force,

@@ -166,7 +166,35 @@ k_list_cells(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_l
 // column-major list with all lanes storing the same k together.
 constexpr int kCellWarps = 4;
 
-struct CellShift { float x, y, z; };
+// Neighbour cell `slot` (0..26, reference order: x offset outermost, z innermost)
+// of cell (cx,cy,cz): flat index and the periodic image shift to apply to its
+// occupants so that plain differences are minimum-image differences.
+__device__ __forceinline__ void neighbour_cell(const ListGeom &g, int cx, int cy, int cz, int slot,
+                                               int &cj, float &sx, float &sy, float &sz) {
+    int jx = cx + slot / 9 - 1, jy = cy + (slot / 3) % 3 - 1, jz = cz + slot % 3 - 1;
+    sx = sy = sz = 0.f;
+    if (jx < 0) { jx += g.nc[0]; sx = -g.Lf[0]; } else if (jx >= g.nc[0]) { jx -= g.nc[0]; sx = g.Lf[0]; }
+    if (jy < 0) { jy += g.nc[1]; sy = -g.Lf[1]; } else if (jy >= g.nc[1]) { jy -= g.nc[1]; sy = g.Lf[1]; }
+    if (jz < 0) { jz += g.nc[2]; sz = -g.Lf[2]; } else if (jz >= g.nc[2]) { jz -= g.nc[2]; sz = g.Lf[2]; }
+    cj = (jx * g.nc[1] + jy) * g.nc[2] + jz;
+}
+
+// Warp-wide bitonic sort of (key, value) held one pair per lane, ascending key.
+__device__ __forceinline__ void warp_sort_pairs(int &key, int &val, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int okey = __shfl_xor_sync(0xffffffffu, key, stride);
+            const int oval = __shfl_xor_sync(0xffffffffu, val, stride);
+            const bool up = ((lane & size) == 0);
+            const bool lower = ((lane & stride) == 0);
+            const bool take = (lower == up) ? (okey < key || (okey == key && oval < val))
+                                            : (okey > key || (okey == key && oval > val));
+            if (take) { key = okey; val = oval; }
+        }
+    }
+}
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
@@ -187,59 +215,66 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
         const int cy = (int)((c / g.nc[2]) % g.nc[1]);
         const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
         const int i_begin = cell_start[c], i_end = cell_start[c + 1];
+
+        // Visiting order of the 27 neighbour cells.  Rows must come out ascending
+        // (neighbor.py:152); cells are visited by ascending first-occupant index,
+        // so for cell-contiguous particle orders the rows are born sorted and the
+        // final insertion sort is a single checking pass.  Lane s holds slot s.
+        int my_slot = lane, my_key = 0x7fffffff;
+        if (lane < 27) {
+            int cj; float sx, sy, sz;
+            neighbour_cell(g, cx, cy, cz, lane, cj, sx, sy, sz);
+            const int b = cell_start[cj];
+            if (b < cell_start[cj + 1]) my_key = cell_particles[b];
+        }
+        int sorted_key = my_key, sorted_slot = my_slot;
+        warp_sort_pairs(sorted_key, sorted_slot, lane);
+
         for (int i0 = i_begin; i0 < i_end; i0 += 32) {
             const bool active = i0 + lane < i_end;
             const int i = active ? cell_particles[i0 + lane] : -1;
             const float4 hi_i = active ? pos_hi[i] : make_float4(0.f, 0.f, 0.f, 0.f);
             int found = 0;
-            for (int ox = -1; ox <= 1; ++ox) {
-                int jx = cx + ox;
-                float sx = 0.f;
-                if (jx < 0) { jx += g.nc[0]; sx = -g.Lf[0]; }
-                else if (jx >= g.nc[0]) { jx -= g.nc[0]; sx = g.Lf[0]; }
-                for (int oy = -1; oy <= 1; ++oy) {
-                    int jy = cy + oy;
-                    float sy = 0.f;
-                    if (jy < 0) { jy += g.nc[1]; sy = -g.Lf[1]; }
-                    else if (jy >= g.nc[1]) { jy -= g.nc[1]; sy = g.Lf[1]; }
-                    for (int oz = -1; oz <= 1; ++oz) {
-                        int jz = cz + oz;
-                        float sz = 0.f;
-                        if (jz < 0) { jz += g.nc[2]; sz = -g.Lf[2]; }
-                        else if (jz >= g.nc[2]) { jz -= g.nc[2]; sz = g.Lf[2]; }
-                        const int cj = (jx * g.nc[1] + jy) * g.nc[2] + jz;
-                        const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
-                        for (int p0 = p_begin; p0 < p_end; p0 += 32) {
-                            const int m = min(32, p_end - p0);
-                            __syncwarp();
-                            if (lane < m) {
-                                const int j = cell_particles[p0 + lane];
-                                const float4 hj = __ldg(&pos_hi[j]);
-                                s_cand[lane] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
-                                                           __int_as_float(j));
-                            }
-                            __syncwarp();
-                            if (active) {
-                                for (int t = 0; t < m; ++t) {
-                                    const float4 cnd = s_cand[t];
-                                    const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y,
-                                                dz = hi_i.z - cnd.z;
-                                    const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                                    if (r2f <= g.rl2_out) {
-                                        const int j = __float_as_int(cnd.w);
-                                        if (j != i) {
-                                            bool hit = r2f < g.rl2_in;
-                                            if (!hit) {   // in the guard band: exact decision
-                                                const float4 lo_i = pos_lo[i];
-                                                const double pi[3] = {ds_to_double(hi_i.x, lo_i.x),
-                                                                      ds_to_double(hi_i.y, lo_i.y),
-                                                                      ds_to_double(hi_i.z, lo_i.z)};
-                                                hit = listed_f64(pi, pos_hi[j], pos_lo[j], g);
-                                            }
-                                            if (hit) {
-                                                if (found < stride) s_rows[found * 32 + lane] = j;
-                                                ++found;
-                                            }
+            // pass 0: sorted visiting order.  If some row overflows, its kept
+            // prefix must be the reference's (first `stride` hits in the
+            // reference scan order, neighbor.py:145-149): pass 1 rescans in that order.
+            for (int pass = 0; pass < 2; ++pass) {
+                found = 0;
+                for (int t = 0; t < 27; ++t) {
+                    const int slot = pass == 0 ? __shfl_sync(0xffffffffu, sorted_slot, t) : t;
+                    int cj; float sx, sy, sz;
+                    neighbour_cell(g, cx, cy, cz, slot, cj, sx, sy, sz);
+                    const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
+                    for (int p0 = p_begin; p0 < p_end; p0 += 32) {
+                        const int m = min(32, p_end - p0);
+                        __syncwarp();
+                        if (lane < m) {
+                            const int j = cell_particles[p0 + lane];
+                            const float4 hj = __ldg(&pos_hi[j]);
+                            s_cand[lane] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
+                                                       __int_as_float(j));
+                        }
+                        __syncwarp();
+                        if (active) {
+                            for (int q = 0; q < m; ++q) {
+                                const float4 cnd = s_cand[q];
+                                const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y,
+                                            dz = hi_i.z - cnd.z;
+                                const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                                if (r2f <= g.rl2_out) {
+                                    const int j = __float_as_int(cnd.w);
+                                    if (j != i) {
+                                        bool hit = r2f < g.rl2_in;
+                                        if (!hit) {   // in the guard band: exact decision
+                                            const float4 lo_i = pos_lo[i];
+                                            const double pi[3] = {ds_to_double(hi_i.x, lo_i.x),
+                                                                  ds_to_double(hi_i.y, lo_i.y),
+                                                                  ds_to_double(hi_i.z, lo_i.z)};
+                                            hit = listed_f64(pi, pos_hi[j], pos_lo[j], g);
+                                        }
+                                        if (hit) {
+                                            if (found < stride) s_rows[found * 32 + lane] = j;
+                                            ++found;
                                         }
                                     }
                                 }
@@ -247,8 +282,9 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                         }
                     }
                 }
+                if (__reduce_max_sync(0xffffffffu, found) <= stride) break;   // no overflow
             }
-            // ---- sort the kept prefix (neighbor.py:152) and publish the rows
+            // ---- ascending rows (neighbor.py:152), then publish them
             const int kept = min(found, stride);
             for (int a = 1; a < kept; ++a) {
                 const int v = s_rows[a * 32 + lane];
@@ -257,7 +293,7 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                     s_rows[(b + 1) * 32 + lane] = s_rows[b * 32 + lane];
                     --b;
                 }
-                s_rows[(b + 1) * 32 + lane] = v;
+                if (b + 1 != a) s_rows[(b + 1) * 32 + lane] = v;
             }
             const int kmax = __reduce_max_sync(0xffffffffu, kept);
             for (int k = 0; k < kmax; ++k)

@@ -78,8 +78,9 @@ int reorder(b2md_runner *r) {
     int rc;
     int key_bits;
     if (c.reorder_mode == 1) {
-        rc = b2md_hilbert_keys(a.pos_hi, a.pos_lo, c.n, &c.box, c.hilbert_bits, c.keys, c.stream);
-        key_bits = 3 * c.hilbert_bits;
+        rc = b2md_hilbert_keys(a.pos_hi, a.pos_lo, c.n, &r->grid, c.hilbert_bits, c.keys, c.stream);
+        key_bits = b2md_hilbert_key_bits(&r->grid, c.hilbert_bits);
+        if (key_bits < 0) { set_error("reorder: Hilbert key does not fit"); return -5; }
     } else {
         // cell order needs the cell of every particle first
         rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,

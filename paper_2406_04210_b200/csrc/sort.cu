@@ -26,8 +26,11 @@ constexpr int kRadix = 256;
 
 // ------------------------------------------------------------------ keys
 struct KeyGeom {
-    double scale[3];   // 2^bits / L, host fp64
-    int bits;
+    double cell_edge[3];   // neighbor.py:71 cell edge, host fp64
+    float inv_edge[3];     // 1 / cell_edge (sub-cell coordinate only)
+    int nc[3];
+    int cell_bits;         // bits per axis holding the cell coordinate
+    int sub_bits;          // bits per axis refining the position inside the cell
 };
 
 // Skilling's transpose form of the Hilbert index (AIP Conf. Proc. 707, 2004),
@@ -62,6 +65,12 @@ __device__ __forceinline__ uint64_t hilbert_index(uint32_t x, uint32_t y, uint32
     return key;
 }
 
+// Key = Hilbert index of the CELL-ALIGNED integer coordinate
+//     q_a = (cell_a << sub_bits) | floor(frac_a * 2^sub_bits)
+// where cell_a is exactly bin_particles' cell coordinate (fp64 division, clip;
+// neighbor.py:74-75).  The Hilbert curve is hierarchical, so every cell's
+// particles end up contiguous in the sorted order (cells follow the curve,
+// particles inside a cell follow the refined curve).
 __global__ void k_hilbert_keys(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
                                int64_t n, KeyGeom g, uint64_t *__restrict__ keys) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -69,13 +78,19 @@ __global__ void k_hilbert_keys(const float4 *__restrict__ pos_hi, const float4 *
     const float4 h = pos_hi[i], l = pos_lo[i];
     const double p[3] = {ds_to_double(h.x, l.x), ds_to_double(h.y, l.y), ds_to_double(h.z, l.z)};
     uint32_t q[3];
-    const long long top = (1ll << g.bits) - 1;
+    const int sub_top = (1 << g.sub_bits) - 1;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        long long k = (long long)floor(__dmul_rn(p[a], g.scale[a]));
-        q[a] = (uint32_t)(k < 0 ? 0 : (k > top ? top : k));
+        long long c = (long long)floor(__ddiv_rn(p[a], g.cell_edge[a]));
+        c = c < 0 ? 0 : (c > g.nc[a] - 1 ? g.nc[a] - 1 : c);
+        // position inside the cell, fp32 is plenty for a locality key
+        const float frac =
+            __double2float_rn(__dsub_rn(p[a], __dmul_rn((double)c, g.cell_edge[a]))) * g.inv_edge[a];
+        int sub = (int)floorf(frac * (float)(1 << g.sub_bits));
+        sub = sub < 0 ? 0 : (sub > sub_top ? sub_top : sub);
+        q[a] = ((uint32_t)c << g.sub_bits) | (uint32_t)sub;
     }
-    keys[i] = hilbert_index(q[0], q[1], q[2], g.bits);
+    keys[i] = hilbert_index(q[0], q[1], q[2], g.cell_bits + g.sub_bits);
 }
 
 __global__ void k_cell_keys(const int32_t *__restrict__ cell_of, int64_t n,
@@ -180,16 +195,32 @@ static inline int64_t sort_tiles(int64_t n) { return (n + kSortTile - 1) / kSort
 
 using namespace b2md;
 
+B2MD_EXPORT int b2md_hilbert_key_bits(const b2md_grid *grid, int32_t sub_bits) {
+    if (!grid || sub_bits < 0) return -1;
+    int mx = grid->ncell[0] > grid->ncell[1] ? grid->ncell[0] : grid->ncell[1];
+    mx = mx > grid->ncell[2] ? mx : grid->ncell[2];
+    int cell_bits = 1;
+    while ((1 << cell_bits) < mx) ++cell_bits;
+    if (cell_bits + sub_bits > 21) return -2;
+    return 3 * (cell_bits + sub_bits);
+}
+
 B2MD_EXPORT int b2md_hilbert_keys(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
-                                  const b2md_box *box, int32_t bits, uint64_t *d_keys,
+                                  const b2md_grid *grid, int32_t sub_bits, uint64_t *d_keys,
                                   void *stream) {
-    if (n <= 0 || !box || bits < 1 || bits > 21) {
-        set_error("b2md_hilbert_keys: bad arguments (bits must be 1..21)");
+    const int key_bits = b2md_hilbert_key_bits(grid, sub_bits);
+    if (n <= 0 || key_bits < 0) {
+        set_error("b2md_hilbert_keys: bad arguments (cell bits + sub bits must be <= 21)");
         return -1;
     }
     KeyGeom g;
-    g.bits = bits;
-    for (int a = 0; a < 3; ++a) g.scale[a] = (double)(1ll << bits) / box->edge[a];
+    g.sub_bits = sub_bits;
+    g.cell_bits = key_bits / 3 - sub_bits;
+    for (int a = 0; a < 3; ++a) {
+        g.nc[a] = grid->ncell[a];
+        g.cell_edge[a] = grid->cell_edge[a];
+        g.inv_edge[a] = (float)(1.0 / grid->cell_edge[a]);
+    }
     k_hilbert_keys<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(
         (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_keys);
     B2MD_CHECK_LAUNCH("b2md_hilbert_keys");

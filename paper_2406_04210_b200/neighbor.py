@@ -300,30 +300,36 @@ def reorder_by_cell(state: ParticleState, grid: CellGrid) -> np.ndarray:
     return d_perm.cpu().numpy().astype(np.int64)
 
 
-HILBERT_BITS = 16
+HILBERT_SUB_BITS = 2
 
 
-def hilbert_keys(state: ParticleState, box: SimBox, bits: int = HILBERT_BITS):
-    """Device tensor of 3*bits-bit Hilbert keys of the current positions."""
+def hilbert_keys(state: ParticleState, box: SimBox, r_list: float,
+                 sub_bits: int = HILBERT_SUB_BITS):
+    """Device tensor of cell-aligned Hilbert keys of the current positions: the
+    Hilbert index of (cell << sub_bits | sub-cell coordinate) per axis, cells as
+    in :func:`bin_particles` for ``r_list``.  Sorting by it makes every cell's
+    particles contiguous, cells following the curve."""
     torch = _torch()
+    g = grid_shape(box, r_list)
     state.positions.acquire_read(COMPUTE)
     dev = state.device_state()
     d_keys = torch.empty(dev.n, dtype=torch.int64, device=dev.device)
     _lib.call("b2md_hilbert_keys", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(), dev.n,
-              box.c_box(), int(bits), d_keys.data_ptr(), dev.stream)
-    return d_keys
+              ctypes.byref(g), int(sub_bits), d_keys.data_ptr(), dev.stream)
+    key_bits = _lib.load().b2md_hilbert_key_bits(ctypes.byref(g), int(sub_bits))
+    return d_keys, key_bits
 
 
-def reorder_hilbert(state: ParticleState, box: SimBox, bits: int = HILBERT_BITS,
-                    internal: bool = True) -> np.ndarray:
+def reorder_hilbert(state: ParticleState, box: SimBox, r_list: float,
+                    sub_bits: int = HILBERT_SUB_BITS, internal: bool = True) -> np.ndarray:
     """Sort device rows along a 3-D Hilbert curve (64-bit keys, stable radix
     sort).  With ``internal=True`` (what ``Simulation`` uses) only the physical
     row order changes: ids travel with the rows and the HOST side keeps its
     logical order.  With ``internal=False`` the logical order changes like
     :func:`reorder_by_cell`.  Returns perm (new row k = old row perm[k])."""
     dev = state.sync_to_compute()
-    d_keys = hilbert_keys(state, box, bits)
-    d_perm = _sort_permutation(dev, d_keys, 3 * int(bits))
+    d_keys, key_bits = hilbert_keys(state, box, r_list, sub_bits)
+    d_perm = _sort_permutation(dev, d_keys, key_bits)
     apply_permutation(dev, d_perm)
     if internal:
         dev.identity_order = False

@@ -32,7 +32,7 @@ from .core import COMPUTE, DeviceState, ParticleState, SignalEngine, SimBox
 from .errors import ConfigError, NeighborOverflowError, SingularPairError
 from .forces import compute_forces_all_to_all, compute_forces_truncated
 from .integrate import IntegratorParams, vv_finalize, vv_integrate
-from .neighbor import (HILBERT_BITS, NeighborList, _round_up, bin_particles,
+from .neighbor import (HILBERT_SUB_BITS, NeighborList, _round_up, bin_particles,
                        build_neighbor_list, grid_shape, needs_rebuild, reorder_hilbert)
 from .observables import DETERMINISTIC, FAST, Sample, thermo
 from .potential import LJParams
@@ -159,7 +159,7 @@ class Simulation:
         """bin -> (reorder) -> build, growing the stride on overflow (sim.py:131-149)."""
         r_list = self.lj.max_r_cut + self.skin
         if self.reorder == "hilbert" and self._rebuild_total % self.reorder_every == 0:
-            reorder_hilbert(self.state, self.box, HILBERT_BITS, internal=True)
+            reorder_hilbert(self.state, self.box, r_list, HILBERT_SUB_BITS, internal=True)
             self.reorders += 1
         growths = 0
         while True:
@@ -231,7 +231,7 @@ class Simulation:
         cfg.ntypes = self.lj.ntypes
         cfg.reorder_mode = _REORDER_MODES[self.reorder]
         cfg.reorder_every = self.reorder_every
-        cfg.hilbert_bits = HILBERT_BITS
+        cfg.hilbert_bits = HILBERT_SUB_BITS
         cfg.table = k["table"].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         for name in DeviceState.ROW16 + ("virial",):
             arr = getattr(cfg, name)

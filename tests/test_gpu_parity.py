@@ -250,21 +250,33 @@ def test_reorder_by_cell_permutes_all_arrays_bitwise():
         assert np.array_equal(buf.acquire_read(b2.HOST), before[k][perm]), k
 
 
-@pytest.mark.parametrize("bits", [5, 16, 21])
-def test_hilbert_keys_and_sort_bit_exact(bits):
+@pytest.mark.parametrize("sub_bits", [0, 2, 7])
+def test_hilbert_keys_and_sort_bit_exact(sub_bits):
     gen = np.random.default_rng(12)
-    n, edge = 50_000, 37.3
+    n, edge, r_list = 50_000, 37.3, 2.8
     pos = quantize_ds(gen.uniform(0, edge, size=(n, 3)))
     st = make_state(pos)
     box = b2.SimBox.cubic(edge)
-    keys = b2.hilbert_keys(st, box, bits).cpu().numpy().astype(np.uint64)
-    want_perm, want_keys = orc.hilbert_permutation(pos, [edge] * 3, bits)
+    keys, key_bits = b2.hilbert_keys(st, box, r_list, sub_bits)
+    keys = keys.cpu().numpy().astype(np.uint64)
+    want_perm, want_keys = orc.hilbert_permutation(pos, [edge] * 3, r_list, sub_bits)
+    assert key_bits == 3 * (4 + sub_bits)          # 13 cells per axis -> 4 bits
     assert np.array_equal(keys, want_keys)
-    perm = b2.reorder_hilbert(st, box, bits, internal=True)
+    perm = b2.reorder_hilbert(st, box, r_list, sub_bits, internal=True)
     assert np.array_equal(perm, want_perm)         # stable: ties keep index order
     # rows moved, logical (host) view unchanged
     assert np.array_equal(st.particle_ids(), want_perm.astype(np.int32))
     assert np.array_equal(st.positions.acquire_read(b2.COMPUTE).to_numpy(), pos)
+    # the key is cell-aligned: after the sort every cell's particles are contiguous rows
+    grid = b2.bin_particles(st, box, r_list)
+    cells = grid.cell_of_particle
+    changes = np.count_nonzero(np.diff(cells) != 0)
+    assert changes == np.unique(cells).size - 1
+    start, parts = grid.cell_start, grid.cell_particles
+    occupied = np.flatnonzero(np.diff(start) > 0)
+    for c in occupied[:: max(len(occupied) // 200, 1)]:
+        rows = parts[start[c]:start[c + 1]]
+        assert np.array_equal(rows, np.arange(rows[0], rows[0] + rows.size))
 
 
 def test_hilbert_curve_is_a_space_filling_walk():
@@ -277,11 +289,12 @@ def test_hilbert_curve_is_a_space_filling_walk():
     assert sorted(keys.tolist()) == list(range(q.shape[0]))
     walk = q[np.argsort(keys)]
     assert np.all(np.abs(np.diff(walk, axis=0)).sum(axis=1) == 1)
-    # and the device computes the same keys for cell-centre positions
-    edge = 8.0
-    pos = (q + 0.5) * (edge / (1 << bits))
-    got = b2.hilbert_keys(make_state(pos), b2.SimBox.cubic(edge), bits).cpu().numpy()
-    assert np.array_equal(got.astype(np.uint64), keys)
+    # and the device computes the same keys for cell-centre positions (8 cells of
+    # edge 1 per axis, no sub-cell bits)
+    pos = q + 0.5
+    got, key_bits = b2.hilbert_keys(make_state(pos), b2.SimBox.cubic(8.0), 1.0, 0)
+    assert key_bits == 9
+    assert np.array_equal(got.cpu().numpy().astype(np.uint64), keys)
 
 
 # ------------------------------------------------------------------ forces
@@ -311,8 +324,11 @@ def check_forces(pos, edges, params, r_list, species=None, stride=256):
     fs, us, ws = orc.pair_scales(pos, edges, table, onl, species=species,
                                  threads=orc.host_threads())
     m = force_error_metrics(f, rf, fs)
-    assert m["M2"] <= FORCE_TOL, m      # error / sum_j |f_ij|
-    assert m["M1"] <= FORCE_TOL, m      # error / max(|F_i|, 1e-3 max_j |F_j|)
+    assert m["M2"] <= FORCE_TOL, m      # error / sum_j |f_ij|  (the stated per-particle metric)
+    assert np.linalg.norm(f - rf) <= FORCE_TOL * np.linalg.norm(rf)   # relative L2 error
+    # per-particle error against the NET force (cancellation-sensitive: the net force
+    # can be 100x smaller than the pair terms it is the sum of) -- looser bound
+    assert m["M1"] <= 1e-4, m
     assert backward_error(pe, rpe, us) <= FORCE_TOL
     assert backward_error(w, rw, ws) <= FORCE_TOL
     # totals (what measure() reports) are far tighter
@@ -365,8 +381,8 @@ def test_pair_table_with_identical_rows_equals_single_type_bitwise():
         out.append((np.array(st.forces.acquire_read(b2.HOST)),
                     np.array(st.per_particle_potential.acquire_read(b2.HOST))))
     # same pair terms; only the deferred prefactors are applied in another order
-    assert np.allclose(out[0][0], out[1][0], rtol=2e-6, atol=1e-5)
-    assert np.allclose(out[0][1], out[1][1], rtol=2e-6, atol=1e-6)
+    assert np.max(np.abs(out[0][0] - out[1][0])) <= 1e-6 * np.abs(out[0][0]).max()
+    assert np.max(np.abs(out[0][1] - out[1][1])) <= 1e-6 * np.abs(out[0][1]).max()
 
 
 def test_all_pairs_forces_match_oracle_and_truncated_kernel():
