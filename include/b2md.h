@@ -157,7 +157,7 @@ int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void
  * arithmetic on pos_hi, per-particle energy and virial in registers.
  * table: HOST pointer to ntypes*ntypes rows {eps, sigma^2, rc^2, shift} (fp64;
  * forces.py:119-126 for one type).  `stride` = rows of d_nbr per particle (a
- * multiple of 4).  flags: B2MD_FORCE_SKIP_THERMO leaves e_pot / virial unwritten
+ * multiple of 16, zero-filled).  flags: B2MD_FORCE_SKIP_THERMO leaves e_pot / virial unwritten
  * (intermediate steps of the native loop, where nobody can observe them).
  * d_boundary (may be NULL = all) selects the exact-image-shift path per warp.
  * Writes force (xyz + e_pot in w) and virial.
@@ -261,7 +261,7 @@ typedef struct b2md_runner_config {
     float *virial[2];
     int32_t current;             /* which set of the pairs above is live */
     int32_t stride;              /* neighbour budget per particle */
-    int32_t *nbr;                /* round_up(stride,4) * pitch */
+    int32_t *nbr;                /* round_up(stride,16) * pitch, zero-filled */
     int64_t pitch;
     int32_t *counts;             /* pitch */
     uint8_t *boundary;           /* pitch */
@@ -297,7 +297,7 @@ typedef struct b2md_runner b2md_runner;
 
 b2md_runner *b2md_runner_create(const b2md_runner_config *cfg);
 void b2md_runner_destroy(b2md_runner *r);
-/* Swap in bigger list buffers after B2MD_RUN_OVERFLOW (nbr: round_up(stride,4)*pitch). */
+/* Swap in bigger list buffers after B2MD_RUN_OVERFLOW (nbr: round_up(stride,16)*pitch, zero-filled). */
 int b2md_runner_set_list(b2md_runner *r, int32_t *nbr, int32_t stride);
 /* (Re)build the list for the current positions and evaluate forces
  * (Simulation.__init__'s initial _compute_forces, sim.py:90).  Synchronous. */

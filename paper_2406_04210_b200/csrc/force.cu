@@ -27,6 +27,7 @@
 // turn the row's accumulators non-finite, and only then is the row rescanned to
 // report (i, first j) through status->singular.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -119,12 +120,19 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
     }
 }
 
-// Four neighbours per trip.  The index stream comes from HBM (it is the bulk of
-// the kernel's traffic), so it is software-pipelined two trips ahead: while trip t
-// does its four position gathers and the arithmetic, the indices of trips t+1 and
-// t+2 are already in flight (8 coalesced 4-byte loads per thread).  CHECK = false
-// is used for the leading trips in which every lane still has valid entries.
-template <bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
+// SUB lanes cooperate on one particle ("subwarp per particle"): lane `sub` owns
+// entries k = sub, sub+SUB, sub+2*SUB, ... of the row and the partial sums are
+// combined with shuffles at the end.  A warp therefore covers 32/SUB consecutive
+// particles and, per load instruction, SUB consecutive entries of each of them --
+// a much tighter set of cache lines for the position gathers than 32 different
+// particles' k-th entries (L1 wavefronts per gather were the limiter at SUB = 1).
+//
+// Four entries per lane per trip.  The index stream comes from HBM (it is the
+// bulk of the kernel's traffic), so it is software-pipelined two trips ahead:
+// while trip t does its four position gathers and the arithmetic, the indices of
+// trips t+1 and t+2 are already in flight.  CHECK = false is used for the leading
+// trips in which every lane still has valid entries.
+template <int SUB, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
 __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, int k,
                                          const int (&j)[4], const float4 *__restrict__ pos,
                                          const ForceArgs &a, const float4 *s_tab_a,
@@ -139,7 +147,7 @@ __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, 
         const float dy = delta<CAREFUL>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
         const float dz = delta<CAREFUL>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
         const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const bool valid = CHECK ? (k + u) < cnt : true;
+        const bool valid = CHECK ? (k + u * SUB) < cnt : true;
         if (TABLE) {
             const int t = ti_row + __float_as_int(pj[u].w);
             lj_pair_table<THERMO>(acc, dx, dy, dz, r2, valid, s_tab_a[t], s_tab_b[t]);
@@ -149,32 +157,37 @@ __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, 
     }
 }
 
-template <bool CAREFUL, bool TABLE, bool THERMO>
-__device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int kmin4,
+// k0 = this lane's first entry (= sub); kmin / kmax = smallest / largest row
+// length among the particles of the warp.  Rows are allocated in multiples of 16
+// and zero-filled, so reads past a row's end stay inside the allocation.
+template <int SUB, bool CAREFUL, bool TABLE, bool THERMO>
+__device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
                                          const ForceArgs &a, const float4 *s_tab_a,
                                          const float2 *s_tab_b, int ti_row) {
+    constexpr int kTrip = 4 * SUB;            // entries of one particle consumed per trip
+    const int64_t step = (int64_t)SUB * pitch;
     int ja[4], jb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        ja[u] = (0 < kmax) ? __ldcs(col + (int64_t)u * pitch) : 0;
-        jb[u] = (4 < kmax) ? __ldcs(col + (int64_t)(4 + u) * pitch) : 0;
+        ja[u] = (0 < kmax) ? __ldcs(col + u * step) : 0;
+        jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
     }
-    for (int k = 0; k < kmax; k += 4) {
+    for (int base = 0; base < kmax; base += kTrip) {
         int jc[4];
-        const bool more = k + 8 < kmax;          // warp-uniform
+        const bool more = base + 2 * kTrip < kmax;          // warp-uniform
 #pragma unroll
-        for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (int64_t)(8 + u) * pitch) : 0;
-        if (k < kmin4)
-            row_trip<CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, k, ja, pos, a, s_tab_a, s_tab_b,
-                                                    ti_row);
+        for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (8 + u) * step) : 0;
+        if (base + kTrip <= kmin)
+            row_trip<SUB, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, ja, pos, a,
+                                                         s_tab_a, s_tab_b, ti_row);
         else
-            row_trip<CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, k, ja, pos, a, s_tab_a, s_tab_b,
-                                                   ti_row);
+            row_trip<SUB, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, ja, pos, a,
+                                                        s_tab_a, s_tab_b, ti_row);
 #pragma unroll
         for (int u = 0; u < 4; ++u) { ja[u] = jb[u]; jb[u] = jc[u]; }
-        col += 4 * pitch;
+        col += 4 * step;
     }
 }
 
@@ -197,7 +210,7 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
-template <bool TABLE, bool THERMO>
+template <int SUB, bool TABLE, bool THERMO>
 __global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
@@ -212,27 +225,38 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ Fo
         }
         __syncthreads();
     }
-    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    constexpr int kPerBlock = kForceThreads / SUB;
+    const int sub = threadIdx.x % SUB;
+    const int64_t i_raw = blockIdx.x * (int64_t)kPerBlock + threadIdx.x / SUB;
     const bool active = i_raw < n;
     const int64_t i = active ? i_raw : n - 1;
     const float4 pi = pos[i];
     const int cnt = active ? counts[i] : 0;
     const int kmax = __reduce_max_sync(0xffffffffu, cnt);
-    // trips in which no lane needs a validity test (inactive lanes do not count)
-    const int kmin4 = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff) & ~3;
+    const int kmin = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff);
     const bool careful = boundary ? (__any_sync(0xffffffffu, active && boundary[i] != 0)) : true;
-    const int32_t *col = nbr + i;
+    const int32_t *col = nbr + (int64_t)sub * pitch + i;
     const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     if (careful)
-        row_loop<true, TABLE, THERMO>(acc, pi, cnt, min(kmin4, kmax), kmax, col, pitch, pos, a,
-                                      s_tab_a, s_tab_b, ti_row);
+        row_loop<SUB, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, a,
+                                           s_tab_a, s_tab_b, ti_row);
     else
-        row_loop<false, TABLE, THERMO>(acc, pi, cnt, min(kmin4, kmax), kmax, col, pitch, pos, a,
-                                       s_tab_a, s_tab_b, ti_row);
-
-    if (!active) return;
+        row_loop<SUB, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, a,
+                                            s_tab_a, s_tab_b, ti_row);
+#pragma unroll
+    for (int o = SUB >> 1; o > 0; o >>= 1) {
+        acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
+        acc.fy += __shfl_xor_sync(0xffffffffu, acc.fy, o);
+        acc.fz += __shfl_xor_sync(0xffffffffu, acc.fz, o);
+        if (THERMO) {
+            acc.u += __shfl_xor_sync(0xffffffffu, acc.u, o);
+            acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+            acc.cnt += __shfl_xor_sync(0xffffffffu, acc.cnt, o);
+        }
+    }
+    if (!active || sub != 0) return;
     float fx, fy, fz, u, w;
     if (TABLE) {
         fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
@@ -245,7 +269,7 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ Fo
     force[i] = make_float4(fx, fy, fz, u);
     if (THERMO && virial) virial[i] = w;
     if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-        report_singular((int)i, pi, cnt, col, pitch, pos, a.box, status);
+        report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
 }
 
 // ---- all pairs, shared-memory tiles of 128 positions ------------------------
@@ -347,25 +371,40 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         set_error("b2md_force_lj: bad arguments");
         return -1;
     }
-    if (stride % 4 != 0) {
-        set_error("b2md_force_lj: the list must be allocated with a multiple of 4 rows");
+    if (stride % 16 != 0) {
+        set_error("b2md_force_lj: the list must be allocated with a multiple of 16 rows");
         return -3;
     }
     ForceArgs a;
     int rc = fill_args(a, box, table, ntypes);
     if (rc) return rc;
-    const unsigned blocks = blocks_for(n, kForceThreads);
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
-#define B2MD_LAUNCH_FORCE(TABLE, THERMO)                                                     \
-    k_force_lj<TABLE, THERMO><<<blocks, kForceThreads, 0, s>>>(                              \
-        (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary,                  \
-        (float4 *)d_force_f4, d_virial, d_status)
-    if (ntypes == 1) {
-        if (thermo) B2MD_LAUNCH_FORCE(false, true); else B2MD_LAUNCH_FORCE(false, false);
-    } else {
-        if (thermo) B2MD_LAUNCH_FORCE(true, true); else B2MD_LAUNCH_FORCE(true, false);
+    static int sub = 0;     // lanes per particle; B2MD_FORCE_SUBWARP overrides (1, 2 or 4)
+    if (sub == 0) {
+        const char *env = getenv("B2MD_FORCE_SUBWARP");
+        const int v = env ? atoi(env) : 4;
+        sub = (v == 1 || v == 2 || v == 4) ? v : 4;
     }
+#define B2MD_LAUNCH_FORCE(SUB, TABLE, THERMO)                                                \
+    k_force_lj<SUB, TABLE, THERMO>                                                           \
+        <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
+            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary,              \
+            (float4 *)d_force_f4, d_virial, d_status)
+#define B2MD_DISPATCH_FORCE(SUB)                                                             \
+    do {                                                                                     \
+        if (ntypes == 1) {                                                                   \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, false, true);                                 \
+            else B2MD_LAUNCH_FORCE(SUB, false, false);                                       \
+        } else {                                                                             \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, true, true);                                  \
+            else B2MD_LAUNCH_FORCE(SUB, true, false);                                        \
+        }                                                                                    \
+    } while (0)
+    if (sub == 1) B2MD_DISPATCH_FORCE(1);
+    else if (sub == 2) B2MD_DISPATCH_FORCE(2);
+    else B2MD_DISPATCH_FORCE(4);
+#undef B2MD_DISPATCH_FORCE
 #undef B2MD_LAUNCH_FORCE
     B2MD_CHECK_LAUNCH("b2md_force_lj");
     return 0;

@@ -66,7 +66,7 @@ int launch_force(b2md_runner *r, bool thermo) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     r->launches += 1;
-    return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, (c.stride + 3) / 4 * 4,
+    return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, (c.stride + 15) / 16 * 16,
                          c.boundary, r->table.data(), c.ntypes,
                          thermo ? 0 : B2MD_FORCE_SKIP_THERMO, a.force, a.virial, c.status,
                          c.stream);

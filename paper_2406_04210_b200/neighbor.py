@@ -189,7 +189,7 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
     dev = state.device_state()
     n = dev.n
     pitch = _round_up(n, 32)
-    rows = _round_up(stride, 4)
+    rows = _round_up(stride, 16)
     reuse = prev is not None and prev.d_nbr.shape == (rows, pitch) and prev._dev is dev
     if reuse:
         d_nbr, d_counts, d_boundary = prev.d_nbr, prev.d_counts, prev.d_boundary

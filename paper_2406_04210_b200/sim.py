@@ -183,7 +183,7 @@ class Simulation:
     def _alloc_list(self, dev: DeviceState):
         torch = _torch()
         pitch = _round_up(dev.n, 32)
-        rows = _round_up(self._stride, 4)
+        rows = _round_up(self._stride, 16)
         # zero-filled: padding entries must stay valid row indices
         return torch.zeros((rows, pitch), dtype=torch.int32, device=dev.device), pitch
 
