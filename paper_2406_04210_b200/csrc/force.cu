@@ -383,8 +383,8 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     static int sub = 0;     // lanes per particle; B2MD_FORCE_SUBWARP overrides (1, 2 or 4)
     if (sub == 0) {
         const char *env = getenv("B2MD_FORCE_SUBWARP");
-        const int v = env ? atoi(env) : 4;
-        sub = (v == 1 || v == 2 || v == 4) ? v : 4;
+        const int v = env ? atoi(env) : 1;
+        sub = (v == 1 || v == 2 || v == 4) ? v : 1;
     }
 #define B2MD_LAUNCH_FORCE(SUB, TABLE, THERMO)                                                \
     k_force_lj<SUB, TABLE, THERMO>                                                           \

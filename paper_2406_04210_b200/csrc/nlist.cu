@@ -196,18 +196,33 @@ __device__ __forceinline__ void warp_sort_pairs(int &key, int &val, int lane) {
     }
 }
 
+// Exact listing decision for particle pair (i, j), kept out of line so that the
+// hot loops do not carry its registers.
+__device__ __noinline__ bool listed_exact(const float4 *__restrict__ pos_hi,
+                                          const float4 *__restrict__ pos_lo, int i, int j,
+                                          const ListGeom &g) {
+    const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
+    const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
+                          ds_to_double(hi_i.z, lo_i.z)};
+    return listed_f64(pi, pos_hi[j], pos_lo[j], g);
+}
+
+constexpr int kBandTag = (int)0x80000000;
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
-                  ListGeom g, int64_t n_cells, const int32_t *__restrict__ cell_start,
+                  const __grid_constant__ ListGeom g, int64_t n_cells,
+                  const int32_t *__restrict__ cell_start,
                   const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
                   int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
                   uint8_t *__restrict__ boundary, b2md_status *status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float4 *s_cand = reinterpret_cast<float4 *>(smem_raw) + warp * 32;
+    // rows: [k][lane], k = 0 .. stride+1 (two spare slots: "one too many" + scratch)
     int32_t *s_rows = reinterpret_cast<int32_t *>(smem_raw + WARPS * 32 * sizeof(float4)) +
-                      (size_t)warp * stride * 32;
+                      (size_t)warp * (stride + 2) * 32 + lane;
     const int64_t c = (int64_t)blockIdx.x * WARPS + warp;
     int wanted_max = 0;
     if (c < n_cells) {
@@ -215,6 +230,7 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
         const int cy = (int)((c / g.nc[2]) % g.nc[1]);
         const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
         const int i_begin = cell_start[c], i_end = cell_start[c + 1];
+        const float rl2_in = g.rl2_in, rl2_out = g.rl2_out;
 
         // Visiting order of the 27 neighbour cells.  Rows must come out ascending
         // (neighbor.py:152); cells are visited by ascending first-occupant index,
@@ -233,17 +249,69 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
         for (int i0 = i_begin; i0 < i_end; i0 += 32) {
             const bool active = i0 + lane < i_end;
             const int i = active ? cell_particles[i0 + lane] : -1;
-            const float4 hi_i = active ? pos_hi[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-            int found = 0;
-            // pass 0: sorted visiting order.  If some row overflows, its kept
-            // prefix must be the reference's (first `stride` hits in the
-            // reference scan order, neighbor.py:145-149): pass 1 rescans in that order.
-            for (int pass = 0; pass < 2; ++pass) {
+            // inactive lanes sit at +1e30: every distance test fails
+            const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+
+            // ---- pass 0 (fast): sorted visiting order, branch-free compaction.
+            // Every candidate is stored at the row's next free slot and the slot
+            // advances only when the fp32 distance is inside the outer radius (a
+            // later candidate overwrites a miss).  Entries inside the guard band
+            // carry a tag bit and are settled exactly afterwards.
+            int32_t *slot = s_rows;
+            int32_t *const slot_cap = s_rows + (stride + 1) * 32;
+            for (int t = 0; t < 27; ++t) {
+                const int nslot = __shfl_sync(0xffffffffu, sorted_slot, t);
+                int cj; float sx, sy, sz;
+                neighbour_cell(g, cx, cy, cz, nslot, cj, sx, sy, sz);
+                const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
+                const int self = (cj == (int)c) ? i : -2;      // only the own cell holds j == i
+                for (int p0 = p_begin; p0 < p_end; p0 += 32) {
+                    const int m = min(32, p_end - p0);
+                    __syncwarp();
+                    if (lane < m) {
+                        const int j = cell_particles[p0 + lane];
+                        const float4 hj = __ldg(&pos_hi[j]);
+                        s_cand[lane] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
+                                                   __int_as_float(j));
+                    }
+                    __syncwarp();
+#pragma unroll 4
+                    for (int q = 0; q < m; ++q) {
+                        const float4 cnd = s_cand[q];
+                        const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y, dz = hi_i.z - cnd.z;
+                        const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        const int j = __float_as_int(cnd.w);
+                        const bool take = (r2f <= rl2_out) && (j != self);
+                        *slot = (r2f >= rl2_in) ? (j | kBandTag) : j;
+                        int32_t *next = slot + (take ? 32 : 0);
+                        slot = next < slot_cap ? next : slot_cap;
+                    }
+                }
+            }
+            int found = (int)((slot - s_rows) >> 5);
+            // settle guard-band entries exactly (rare) and compact the row
+            {
+                int w = 0;
+                for (int k = 0; k < found; ++k) {
+                    int v = s_rows[k * 32];
+                    bool keep = true;
+                    if (v < 0) {
+                        v &= ~kBandTag;
+                        keep = listed_exact(pos_hi, pos_lo, i, v, g);
+                    }
+                    if (keep) { s_rows[w * 32] = v; ++w; }
+                }
+                // a row that filled all stride+1 slots may have lost entries: redo exactly
+                if (found <= stride) found = w;
+            }
+            // ---- pass 1 (only if some row may exceed the budget): reference scan
+            // order with exact in-loop decisions, so that the kept prefix is the
+            // reference's (first `stride` hits in its order, neighbor.py:145-149).
+            if (__any_sync(0xffffffffu, found > stride)) {
                 found = 0;
                 for (int t = 0; t < 27; ++t) {
-                    const int slot = pass == 0 ? __shfl_sync(0xffffffffu, sorted_slot, t) : t;
                     int cj; float sx, sy, sz;
-                    neighbour_cell(g, cx, cy, cz, slot, cj, sx, sy, sz);
+                    neighbour_cell(g, cx, cy, cz, t, cj, sx, sy, sz);
                     const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
                     for (int p0 = p_begin; p0 < p_end; p0 += 32) {
                         const int m = min(32, p_end - p0);
@@ -255,49 +323,38 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                                                        __int_as_float(j));
                         }
                         __syncwarp();
-                        if (active) {
-                            for (int q = 0; q < m; ++q) {
-                                const float4 cnd = s_cand[q];
-                                const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y,
-                                            dz = hi_i.z - cnd.z;
-                                const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                                if (r2f <= g.rl2_out) {
-                                    const int j = __float_as_int(cnd.w);
-                                    if (j != i) {
-                                        bool hit = r2f < g.rl2_in;
-                                        if (!hit) {   // in the guard band: exact decision
-                                            const float4 lo_i = pos_lo[i];
-                                            const double pi[3] = {ds_to_double(hi_i.x, lo_i.x),
-                                                                  ds_to_double(hi_i.y, lo_i.y),
-                                                                  ds_to_double(hi_i.z, lo_i.z)};
-                                            hit = listed_f64(pi, pos_hi[j], pos_lo[j], g);
-                                        }
-                                        if (hit) {
-                                            if (found < stride) s_rows[found * 32 + lane] = j;
-                                            ++found;
-                                        }
-                                    }
+                        for (int q = 0; q < m; ++q) {
+                            const float4 cnd = s_cand[q];
+                            const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y,
+                                        dz = hi_i.z - cnd.z;
+                            const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                            const int j = __float_as_int(cnd.w);
+                            if (r2f <= rl2_out && j != i) {
+                                bool hit = r2f < rl2_in;
+                                if (!hit) hit = listed_exact(pos_hi, pos_lo, i, j, g);
+                                if (hit) {
+                                    if (found < stride) s_rows[found * 32] = j;
+                                    ++found;
                                 }
                             }
                         }
                     }
                 }
-                if (__reduce_max_sync(0xffffffffu, found) <= stride) break;   // no overflow
             }
             // ---- ascending rows (neighbor.py:152), then publish them
             const int kept = min(found, stride);
             for (int a = 1; a < kept; ++a) {
-                const int v = s_rows[a * 32 + lane];
+                const int v = s_rows[a * 32];
                 int b = a - 1;
-                while (b >= 0 && s_rows[b * 32 + lane] > v) {
-                    s_rows[(b + 1) * 32 + lane] = s_rows[b * 32 + lane];
+                while (b >= 0 && s_rows[b * 32] > v) {
+                    s_rows[(b + 1) * 32] = s_rows[b * 32];
                     --b;
                 }
-                if (b + 1 != a) s_rows[(b + 1) * 32 + lane] = v;
+                if (b + 1 != a) s_rows[(b + 1) * 32] = v;
             }
             const int kmax = __reduce_max_sync(0xffffffffu, kept);
             for (int k = 0; k < kmax; ++k)
-                if (k < kept) nbr[(int64_t)k * pitch + i] = s_rows[k * 32 + lane];
+                if (k < kept) nbr[(int64_t)k * pitch + i] = s_rows[k * 32];
             if (active) {
                 counts[i] = kept;
                 if (boundary) boundary[i] = boundary_flag(hi_i, g);
@@ -419,7 +476,7 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
     g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n, kBuildThreads);
-    const size_t warp_smem = 32 * sizeof(float4) + (size_t)stride * 32 * sizeof(int32_t);
+    const size_t warp_smem = 32 * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, stride, pitch, d_nbr,
