@@ -130,13 +130,15 @@ int b2md_bin(const void *d_pos_hi, const void *d_pos_lo, int64_t n, const b2md_g
  * (pitch >= n, multiple of 32) so that a warp's loads coalesce.  Rows wanting
  * more than `stride` entries set status->overflow; status->max_count receives
  * the largest unclamped count.  d_boundary (n) uint8 marks particles within
- * `boundary_margin` of a periodic face (they may interact across it). */
+ * `boundary_margin` of a periodic face (they may interact across it).  Rows are
+ * built for particles [0, n_rows) only (n_rows = n, or the owned count when rows
+ * [n_rows, n) are ghosts of a slab decomposition). */
 int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                      const b2md_box *box, const b2md_grid *grid,
                      const int32_t *d_cell_of, const int32_t *d_cell_start,
                      const int32_t *d_cell_particles, double r_list,
                      int32_t stride, int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
-                     uint8_t *d_boundary, double boundary_margin,
+                     uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
                      b2md_status *d_status, void *stream);
 
 /* Snapshot of the unwrapped positions a list was built from
@@ -229,6 +231,26 @@ int b2md_sort_pairs_u64(uint64_t *d_keys, int32_t *d_vals, uint64_t *d_keys_tmp,
                         void *d_scratch, void *stream);
 int b2md_gather16(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
 int b2md_gather4(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
+
+/* ---------------------------------------------- slab decomposition (multi-GPU)
+ * No counterpart in the reference; SURVEY.md section 8e.  A rank
+ * owns the x-slab of half-width `half` around `centre` of the global periodic
+ * box and keeps ghost rows of neighbour ranks behind its owned rows, all in
+ * global coordinates.
+ * b2md_slab_classify: d = x - centre wrapped into [-L/2, L/2) (fp64, no FMA);
+ *   flag_left[i] = d < lo_cut, flag_right[i] = d >= hi_cut.  Migration uses
+ *   (-half, half); ghost selection (-half + r_ghost, half - r_ghost).
+ * b2md_compact_indices: stable stream compaction of the indices whose flag is 1.
+ * b2md_flag_neither: out = !(a | b) (rows that stay).
+ * Records are then moved with b2md_gather16 and exchanged with NCCL send/recv. */
+int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n, double centre,
+                       double box_x, double lo_cut, double hi_cut, int32_t *d_flag_left,
+                       int32_t *d_flag_right, void *stream);
+int64_t b2md_compact_scratch_bytes(int64_t n);
+int b2md_compact_indices(const int32_t *d_flags, int64_t n, int32_t *d_out_idx, int32_t *d_count,
+                         void *d_scratch, void *stream);
+int b2md_flag_neither(const int32_t *d_a, const int32_t *d_b, int64_t n, int32_t *d_out,
+                      void *stream);
 
 /* ------------------------------------------------------------ native step loop
  * Simulation.run / SignalEngine.run_steps (core.py:262-279) with the rebuild

@@ -1,0 +1,97 @@
+// Slab decomposition support (no counterpart in the reference, SPEC.md:131 lists
+// spatial decomposition as a non-goal): classification of
+// owned particles against the slab faces, stable stream compaction of the
+// selected rows, and packing of migration / ghost records.
+//
+// A rank owns x in [x_lo, x_hi) of the global periodic box and keeps, behind its
+// owned rows, ghost copies of neighbour-rank particles within r_ghost of its
+// faces -- all in GLOBAL coordinates, so the cell, list and force kernels (which
+// wrap periodically over the global box) run unchanged on owned + ghost rows.
+#include "common.cuh"
+
+namespace b2md {
+
+int exclusive_scan_i32(const int32_t *d_in, int32_t *d_out, int64_t n, int32_t *d_tiles,
+                       cudaStream_t stream);
+
+constexpr int kThreads = 256;
+
+// Offset of x from the slab centre, the short way round the periodic axis, in
+// fp64 without contraction (a numpy restatement reproduces it bit for bit):
+//     d = x - centre;  d -= L * floor(d / L + 0.5)          in [-L/2, L/2)
+// A particle is inside the slab iff -half <= d < half.
+//   lo_cut / hi_cut: flag_left = d < lo_cut, flag_right = d >= hi_cut
+//   (migration: lo_cut = -half, hi_cut = half; ghosts: -half + r_ghost, half - r_ghost).
+__global__ void k_slab_classify(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
+                                int64_t n, double centre, double Lx, double lo_cut, double hi_cut,
+                                int32_t *__restrict__ left, int32_t *__restrict__ right) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = ds_to_double(pos_hi[i].x, pos_lo[i].x);
+    double d = __dsub_rn(x, centre);
+    d = __dsub_rn(d, __dmul_rn(Lx, floor(__dadd_rn(__ddiv_rn(d, Lx), 0.5))));
+    left[i] = d < lo_cut;
+    right[i] = d >= hi_cut;
+}
+
+__global__ void k_compact_scatter(const int32_t *__restrict__ flags,
+                                  const int32_t *__restrict__ offsets, int64_t n,
+                                  int32_t *__restrict__ out_idx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && flags[i]) out_idx[offsets[i]] = (int32_t)i;
+}
+
+__global__ void k_flag_not_either(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
+                                  int64_t n, int32_t *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (a[i] | b[i]) ? 0 : 1;
+}
+
+}  // namespace b2md
+
+using namespace b2md;
+
+B2MD_EXPORT int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                   double centre, double box_x, double lo_cut, double hi_cut,
+                                   int32_t *d_flag_left, int32_t *d_flag_right, void *stream) {
+    if (n < 0 || !(box_x > 0.0)) { set_error("b2md_slab_classify: bad arguments"); return -1; }
+    if (n == 0) return 0;
+    k_slab_classify<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, centre, box_x, lo_cut, hi_cut,
+        d_flag_left, d_flag_right);
+    B2MD_CHECK_LAUNCH("b2md_slab_classify");
+    return 0;
+}
+
+B2MD_EXPORT int64_t b2md_compact_scratch_bytes(int64_t n) {
+    const int64_t tiles = ((n < 1 ? 1 : n) + 4095) / 4096 + 2;
+    return (int64_t)sizeof(int32_t) * ((n < 1 ? 1 : n) + 1 + tiles) + 256;
+}
+
+// Stable stream compaction: d_out_idx receives, in ascending order, the indices i
+// with d_flags[i] != 0 (flags must be 0/1); d_count[0] receives how many.
+B2MD_EXPORT int b2md_compact_indices(const int32_t *d_flags, int64_t n, int32_t *d_out_idx,
+                                     int32_t *d_count, void *d_scratch, void *stream) {
+    if (n < 0 || !d_count || !d_scratch) { set_error("b2md_compact_indices: bad arguments"); return -1; }
+    cudaStream_t s = as_stream(stream);
+    if (n == 0) return check_cuda(cudaMemsetAsync(d_count, 0, sizeof(int32_t), s), "compact memset");
+    int32_t *offsets = (int32_t *)d_scratch;        // n + 1
+    int32_t *tiles = offsets + n + 1;
+    int rc = exclusive_scan_i32(d_flags, offsets, n, tiles, s);
+    if (rc) return rc;
+    k_compact_scatter<<<blocks_for(n, kThreads), kThreads, 0, s>>>(d_flags, offsets, n, d_out_idx);
+    B2MD_CHECK_LAUNCH("b2md_compact_indices");
+    return check_cuda(cudaMemcpyAsync(d_count, offsets + n, sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, s), "compact count");
+}
+
+// out[i] = !(a[i] | b[i])  (the "stays" flag after a migration classification)
+B2MD_EXPORT int b2md_flag_neither(const int32_t *d_a, const int32_t *d_b, int64_t n,
+                                  int32_t *d_out, void *stream) {
+    if (n < 0) { set_error("b2md_flag_neither: bad arguments"); return -1; }
+    if (n == 0) return 0;
+    k_flag_not_either<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(d_a, d_b, n,
+                                                                                   d_out);
+    B2MD_CHECK_LAUNCH("b2md_flag_neither");
+    return 0;
+}

@@ -101,13 +101,13 @@ __device__ __forceinline__ uint8_t boundary_flag(const float4 h, const ListGeom 
 template <bool PREFILTER>
 __global__ void __launch_bounds__(kBuildThreads)
 k_list_cells(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
-             ListGeom g, const int32_t *__restrict__ cell_of,
+             int64_t n_rows, ListGeom g, const int32_t *__restrict__ cell_of,
              const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_particles,
              int stride, int64_t pitch, int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
              uint8_t *__restrict__ boundary, b2md_status *status) {
     const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool active = i_raw < n;
-    const int64_t i = active ? i_raw : n - 1;
+    const bool active = i_raw < n_rows;
+    const int64_t i = active ? i_raw : n_rows - 1;
     const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
     const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
                           ds_to_double(hi_i.z, lo_i.z)};
@@ -212,7 +212,7 @@ constexpr int kBandTag = (int)0x80000000;
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
-                  const __grid_constant__ ListGeom g, int64_t n_cells,
+                  int64_t n_rows, const __grid_constant__ ListGeom g, int64_t n_cells,
                   const int32_t *__restrict__ cell_start,
                   const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
                   int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
@@ -231,6 +231,7 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
         const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
         const int i_begin = cell_start[c], i_end = cell_start[c + 1];
         const float rl2_in = g.rl2_in, rl2_out = g.rl2_out;
+        if (i_begin == i_end) return;          // empty cell (whole warp leaves together)
 
         // Visiting order of the 27 neighbour cells.  Rows must come out ascending
         // (neighbor.py:152); cells are visited by ascending first-occupant index,
@@ -247,8 +248,10 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
         warp_sort_pairs(sorted_key, sorted_slot, lane);
 
         for (int i0 = i_begin; i0 < i_end; i0 += 32) {
-            const bool active = i0 + lane < i_end;
-            const int i = active ? cell_particles[i0 + lane] : -1;
+            // rows exist for particles [0, n_rows) only (ghost rows are skipped)
+            const int i_raw = (i0 + lane < i_end) ? cell_particles[i0 + lane] : -1;
+            const bool active = i_raw >= 0 && i_raw < n_rows;
+            const int i = active ? i_raw : -1;
             // inactive lanes sit at +1e30: every distance test fails
             const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
 
@@ -371,11 +374,11 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
 // All-pairs scan for grids with fewer than three cells on some axis.
 __global__ void __launch_bounds__(kBuildThreads)
 k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
-             ListGeom g, int stride, int64_t pitch, int32_t *__restrict__ nbr,
+             int64_t n_rows, ListGeom g, int stride, int64_t pitch, int32_t *__restrict__ nbr,
              int32_t *__restrict__ counts, uint8_t *__restrict__ boundary, b2md_status *status) {
     const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool active = i_raw < n;
-    const int64_t i = active ? i_raw : n - 1;
+    const bool active = i_raw < n_rows;
+    const int64_t i = active ? i_raw : n_rows - 1;
     const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
     const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
                           ds_to_double(hi_i.z, lo_i.z)};
@@ -450,11 +453,12 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
                                  const int32_t *d_cell_of, const int32_t *d_cell_start,
                                  const int32_t *d_cell_particles, double r_list, int32_t stride,
                                  int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
-                                 uint8_t *d_boundary, double boundary_margin,
+                                 uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
                                  b2md_status *d_status, void *stream) {
     if (n <= 0 || !box || !grid || !d_status) { set_error("b2md_build_nlist: bad arguments"); return -1; }
     if (stride < 1) { set_error("b2md_build_nlist: stride must be >= 1"); return -2; }
     if (pitch < n) { set_error("b2md_build_nlist: pitch < n"); return -3; }
+    if (n_rows < 1 || n_rows > n) { set_error("b2md_build_nlist: need 1 <= n_rows <= n"); return -4; }
     cudaStream_t s = as_stream(stream);
     ListGeom g;
     g.box = make_box_d(box);
@@ -475,11 +479,11 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
     g.rl2_in = (float)(g.rl2 - band) * (1.0f - 1e-6f);
     g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
     const bool prefilter = band < 0.05 * g.rl2;
-    const unsigned blocks = blocks_for(n, kBuildThreads);
+    const unsigned blocks = blocks_for(n_rows, kBuildThreads);
     const size_t warp_smem = 32 * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, stride, pitch, d_nbr,
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, stride, pitch, d_nbr,
             d_counts, d_boundary, d_status);
     } else if (prefilter && warp_smem * 2 <= 200 * 1024) {
         // warp-per-cell kernel; fewer warps per CTA when rows are long
@@ -493,7 +497,7 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
                 attr4 = true;
             }
             k_list_cells_warp<kCellWarps><<<blocks_for(nc, kCellWarps), kCellWarps * 32, smem, s>>>(
-                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, nc, d_cell_start,
+                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
                 d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
         } else {
             const size_t smem = warp_smem * 2;
@@ -504,20 +508,20 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
                 attr2 = true;
             }
             k_list_cells_warp<2><<<blocks_for(nc, 2), 64, smem, s>>>(
-                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, nc, d_cell_start,
+                (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
                 d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
         }
     } else if (prefilter) {
         k_list_cells<true><<<blocks, kBuildThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_cell_of, d_cell_start,
-            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, d_cell_of,
+            d_cell_start, d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
     } else {
         k_list_cells<false><<<blocks, kBuildThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, g, d_cell_of, d_cell_start,
-            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, d_cell_of,
+            d_cell_start, d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
     }
     if (d_boundary)
-        k_count_boundary<<<blocks_for(n, 256), 256, 0, s>>>(d_boundary, n, d_status);
+        k_count_boundary<<<blocks_for(n_rows, 256), 256, 0, s>>>(d_boundary, n_rows, d_status);
     B2MD_CHECK_LAUNCH("b2md_build_nlist");
     return 0;
 }

@@ -121,8 +121,8 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
                        c.cell_particles, c.bin_scratch, c.stream))) return rc;
     if ((rc = b2md_build_nlist(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
                                c.cell_start, c.cell_particles, r->r_list, c.stride, c.pitch,
-                               c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.status,
-                               c.stream))) return rc;
+                               c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n,
+                               c.status, c.stream))) return rc;
     if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos,
                             c.stream))) return rc;
     r->launches += 1 + 6 + 2 + 1;

@@ -208,7 +208,7 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
               grid.c_grid(), grid.d_cell_of.data_ptr(), grid.d_cell_start.data_ptr(),
               grid.d_cell_particles.data_ptr(), float(r_list), stride, pitch,
               d_nbr.data_ptr(), d_counts.data_ptr(), d_boundary.data_ptr(),
-              float(r_list) + skin, dev.status.data_ptr(), dev.stream)
+              float(r_list) + skin, n, dev.status.data_ptr(), dev.stream)
     _lib.call("b2md_snapshot", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(),
               dev.image.data_ptr(), n, box.c_box(), d_at_build.data_ptr(), d_ref_pos.data_ptr(),
               dev.stream)
