@@ -113,7 +113,8 @@ class DeviceState:
         self.device_index = int(device)
         self.device = _require_cuda(self.device_index)
         self.n = int(n)
-        self.capacity = int(capacity if capacity is not None else n)
+        # rows are addressed up to the list pitch (n rounded up to a multiple of 32)
+        self.capacity = (int(capacity if capacity is not None else n) + 31) // 32 * 32
         cap = self.capacity
         with torch.cuda.device(self.device):
             self.pos_hi = torch.zeros((cap, 4), dtype=torch.float32, device=self.device)

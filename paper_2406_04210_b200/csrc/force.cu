@@ -132,15 +132,30 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
 // while trip t does its four position gathers and the arithmetic, the indices of
 // trips t+1 and t+2 are already in flight.  CHECK = false is used for the leading
 // trips in which every lane still has valid entries.
-template <int SUB, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
+// Where the 16-byte neighbour-position gathers go.  The LSU data pipe of L1
+// (about one 128-byte wavefront per cycle per SM) is the limiter of this kernel:
+// a gather of 32 scattered float4 costs ~11 wavefronts.  Texture fetches of the
+// same linear buffer run through the TEX pipe of the same cache, so splitting the
+// gathers between both pipes raises the gather rate.
+//   GATHER 0: all through LDG (ld.global.nc)   1: all through TEX
+//   GATHER 2: entries alternate between the two pipes
+template <int GATHER>
+__device__ __forceinline__ float4 gather_pos(const float4 *__restrict__ pos,
+                                             cudaTextureObject_t tex, int j, int u) {
+    if (GATHER == 1 || (GATHER == 2 && (u & 1))) return tex1Dfetch<float4>(tex, j);
+    return __ldg(pos + j);
+}
+
+template <int SUB, int GATHER, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
 __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, int k,
                                          const int (&j)[4], const float4 *__restrict__ pos,
-                                         const ForceArgs &a, const float4 *s_tab_a,
-                                         const float2 *s_tab_b, int ti_row) {
+                                         cudaTextureObject_t tex, const ForceArgs &a,
+                                         const float4 *s_tab_a, const float2 *s_tab_b,
+                                         int ti_row) {
     const BoxF &b = a.box;
     float4 pj[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
+    for (int u = 0; u < 4; ++u) pj[u] = gather_pos<GATHER>(pos, tex, j[u], u);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
@@ -160,12 +175,13 @@ __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, 
 // k0 = this lane's first entry (= sub); kmin / kmax = smallest / largest row
 // length among the particles of the warp.  Rows are allocated in multiples of 16
 // and zero-filled, so reads past a row's end stay inside the allocation.
-template <int SUB, bool CAREFUL, bool TABLE, bool THERMO>
+template <int SUB, int GATHER, bool CAREFUL, bool TABLE, bool THERMO>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
-                                         const ForceArgs &a, const float4 *s_tab_a,
-                                         const float2 *s_tab_b, int ti_row) {
+                                         cudaTextureObject_t tex, const ForceArgs &a,
+                                         const float4 *s_tab_a, const float2 *s_tab_b,
+                                         int ti_row) {
     constexpr int kTrip = 4 * SUB;            // entries of one particle consumed per trip
     const int64_t step = (int64_t)SUB * pitch;
     int ja[4], jb[4];
@@ -180,11 +196,11 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
 #pragma unroll
         for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (8 + u) * step) : 0;
         if (base + kTrip <= kmin)
-            row_trip<SUB, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, ja, pos, a,
-                                                         s_tab_a, s_tab_b, ti_row);
+            row_trip<SUB, GATHER, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, ja, pos,
+                                                                 tex, a, s_tab_a, s_tab_b, ti_row);
         else
-            row_trip<SUB, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, ja, pos, a,
-                                                        s_tab_a, s_tab_b, ti_row);
+            row_trip<SUB, GATHER, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, ja, pos,
+                                                                tex, a, s_tab_a, s_tab_b, ti_row);
 #pragma unroll
         for (int u = 0; u < 4; ++u) { ja[u] = jb[u]; jb[u] = jc[u]; }
         col += 4 * step;
@@ -210,9 +226,10 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
-template <int SUB, bool TABLE, bool THERMO>
+template <int SUB, int GATHER, bool TABLE, bool THERMO>
 __global__ void __launch_bounds__(kForceThreads, 8)
-k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
+k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
+           const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
            const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
            float *__restrict__ virial, b2md_status *status) {
@@ -240,11 +257,11 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ Fo
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     if (careful)
-        row_loop<SUB, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, a,
-                                           s_tab_a, s_tab_b, ti_row);
+        row_loop<SUB, GATHER, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos,
+                                                   tex, a, s_tab_a, s_tab_b, ti_row);
     else
-        row_loop<SUB, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, a,
-                                            s_tab_a, s_tab_b, ti_row);
+        row_loop<SUB, GATHER, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,
+                                                    pos, tex, a, s_tab_a, s_tab_b, ti_row);
 #pragma unroll
     for (int o = SUB >> 1; o > 0; o >>= 1) {
         acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
@@ -335,6 +352,38 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
                   ((unsigned long long)(unsigned)i << 32) | (unsigned)first_bad);
 }
 
+// Texture objects over position buffers (linear float4), created on first use
+// and reused while the same buffer comes back (the runner alternates between two).
+struct TexEntry { const void *ptr; size_t rows; cudaTextureObject_t tex; };
+static TexEntry g_tex[8];
+static int g_tex_next = 0;
+
+static int position_texture(const void *ptr, size_t rows, cudaTextureObject_t *out) {
+    for (const TexEntry &e : g_tex)
+        if (e.ptr == ptr && e.rows == rows && e.tex) { *out = e.tex; return 0; }
+    TexEntry &slot = g_tex[g_tex_next];
+    g_tex_next = (g_tex_next + 1) % 8;
+    if (slot.tex) cudaDestroyTextureObject(slot.tex);
+    cudaResourceDesc res = {};
+    res.resType = cudaResourceTypeLinear;
+    res.res.linear.devPtr = const_cast<void *>(ptr);
+    res.res.linear.desc = cudaCreateChannelDesc<float4>();
+    res.res.linear.sizeInBytes = rows * sizeof(float4);
+    cudaTextureDesc td = {};
+    td.readMode = cudaReadModeElementType;
+    td.filterMode = cudaFilterModePoint;
+    td.addressMode[0] = cudaAddressModeClamp;
+    td.normalizedCoords = 0;
+    slot.tex = 0;
+    int rc = check_cuda(cudaCreateTextureObject(&slot.tex, &res, &td, nullptr),
+                        "cudaCreateTextureObject");
+    if (rc) { slot.ptr = nullptr; slot.tex = 0; return rc; }
+    slot.ptr = ptr;
+    slot.rows = rows;
+    *out = slot.tex;
+    return 0;
+}
+
 static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int ntypes) {
     if (!box || !table) { set_error("force: null box/table"); return -1; }
     if (ntypes < 1 || ntypes > kMaxTypes) {
@@ -380,31 +429,47 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
-    static int sub = 0;     // lanes per particle; B2MD_FORCE_SUBWARP overrides (1, 2 or 4)
+    // tuning knobs (defaults chosen from profiles/)
+    static int sub = 0, gather = -1;
     if (sub == 0) {
-        const char *env = getenv("B2MD_FORCE_SUBWARP");
+        const char *env = getenv("B2MD_FORCE_SUBWARP");       // lanes per particle: 1, 2, 4
         const int v = env ? atoi(env) : 1;
         sub = (v == 1 || v == 2 || v == 4) ? v : 1;
+        env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 1 TEX, 2 alternate
+        const int w = env ? atoi(env) : 0;
+        gather = (w >= 0 && w <= 2) ? w : 0;
     }
-#define B2MD_LAUNCH_FORCE(SUB, TABLE, THERMO)                                                \
-    k_force_lj<SUB, TABLE, THERMO>                                                           \
+    cudaTextureObject_t tex = 0;
+    if (gather != 0) {
+        // rows of pos_hi are addressed up to `pitch` (owned + ghost rows)
+        rc = position_texture(d_pos_hi, (size_t)pitch, &tex);
+        if (rc) return rc;
+    }
+#define B2MD_LAUNCH_FORCE(SUB, GATHER, TABLE, THERMO)                                        \
+    k_force_lj<SUB, GATHER, TABLE, THERMO>                                                   \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
-            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary,              \
+            (const float4 *)d_pos_hi, tex, n, a, d_nbr, d_counts, pitch, d_boundary,         \
             (float4 *)d_force_f4, d_virial, d_status)
-#define B2MD_DISPATCH_FORCE(SUB)                                                             \
+#define B2MD_DISPATCH_TT(SUB, GATHER)                                                        \
     do {                                                                                     \
         if (ntypes == 1) {                                                                   \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, false, true);                                 \
-            else B2MD_LAUNCH_FORCE(SUB, false, false);                                       \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, false, true);                         \
+            else B2MD_LAUNCH_FORCE(SUB, GATHER, false, false);                               \
         } else {                                                                             \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, true, true);                                  \
-            else B2MD_LAUNCH_FORCE(SUB, true, false);                                        \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, true, true);                          \
+            else B2MD_LAUNCH_FORCE(SUB, GATHER, true, false);                                \
         }                                                                                    \
     } while (0)
-    if (sub == 1) B2MD_DISPATCH_FORCE(1);
-    else if (sub == 2) B2MD_DISPATCH_FORCE(2);
-    else B2MD_DISPATCH_FORCE(4);
-#undef B2MD_DISPATCH_FORCE
+    if (sub == 1) {
+        if (gather == 0) B2MD_DISPATCH_TT(1, 0);
+        else if (gather == 1) B2MD_DISPATCH_TT(1, 1);
+        else B2MD_DISPATCH_TT(1, 2);
+    } else if (sub == 2) {
+        B2MD_DISPATCH_TT(2, 0);
+    } else {
+        B2MD_DISPATCH_TT(4, 0);
+    }
+#undef B2MD_DISPATCH_TT
 #undef B2MD_LAUNCH_FORCE
     B2MD_CHECK_LAUNCH("b2md_force_lj");
     return 0;

@@ -260,8 +260,9 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
             // advances only when the fp32 distance is inside the outer radius (a
             // later candidate overwrites a miss).  Entries inside the guard band
             // carry a tag bit and are settled exactly afterwards.
-            int32_t *slot = s_rows;
-            int32_t *const slot_cap = s_rows + (stride + 1) * 32;
+            // 32-bit word offsets into this lane's column of s_rows (stride 32 words)
+            int slot = 0;
+            const int slot_cap = (stride + 1) * 32;
             for (int t = 0; t < 27; ++t) {
                 const int nslot = __shfl_sync(0xffffffffu, sorted_slot, t);
                 int cj; float sx, sy, sz;
@@ -285,13 +286,12 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                         const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                         const int j = __float_as_int(cnd.w);
                         const bool take = (r2f <= rl2_out) && (j != self);
-                        *slot = (r2f >= rl2_in) ? (j | kBandTag) : j;
-                        int32_t *next = slot + (take ? 32 : 0);
-                        slot = next < slot_cap ? next : slot_cap;
+                        s_rows[slot] = (r2f >= rl2_in) ? (j | kBandTag) : j;
+                        slot = min(slot + (take ? 32 : 0), slot_cap);
                     }
                 }
             }
-            int found = (int)((slot - s_rows) >> 5);
+            int found = slot >> 5;
             // settle guard-band entries exactly (rare) and compact the row
             {
                 int w = 0;

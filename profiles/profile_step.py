@@ -24,13 +24,15 @@ ap.add_argument("--steps", type=int, default=60)
 ap.add_argument("--melt", type=int, default=0, help="untimed steps before (to leave the lattice)")
 ap.add_argument("--reorder", default="hilbert")
 ap.add_argument("--density", type=float, default=0.75)
+ap.add_argument("--reorder-every", type=int, default=1)
 args = ap.parse_args()
 
 st, box = b2.init_lattice_any(args.n, args.density)
 b2.init_velocities(st, 1.2, 42)
 sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001, force_mode=b2.TRUNCATED,
                     skin=0.3, sample_interval=100,
-                    reorder=None if args.reorder == "none" else args.reorder)
+                    reorder=None if args.reorder == "none" else args.reorder,
+                    reorder_every=args.reorder_every)
 if args.melt:
     sim.run(args.melt)
 torch.cuda.synchronize()
