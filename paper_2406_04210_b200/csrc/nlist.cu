@@ -208,6 +208,7 @@ __device__ __noinline__ bool listed_exact(const float4 *__restrict__ pos_hi,
 }
 
 constexpr int kBandTag = (int)0x80000000;
+constexpr int kCandCap = 160;      // candidates staged per batch and warp
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
@@ -219,9 +220,9 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                   uint8_t *__restrict__ boundary, b2md_status *status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float4 *s_cand = reinterpret_cast<float4 *>(smem_raw) + warp * 32;
+    float4 *s_cand = reinterpret_cast<float4 *>(smem_raw) + warp * kCandCap;
     // rows: [k][lane], k = 0 .. stride+1 (two spare slots: "one too many" + scratch)
-    int32_t *s_rows = reinterpret_cast<int32_t *>(smem_raw + WARPS * 32 * sizeof(float4)) +
+    int32_t *s_rows = reinterpret_cast<int32_t *>(smem_raw + WARPS * kCandCap * sizeof(float4)) +
                       (size_t)warp * (stride + 2) * 32 + lane;
     const int64_t c = (int64_t)blockIdx.x * WARPS + warp;
     int wanted_max = 0;
@@ -256,43 +257,61 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
             const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
 
             // ---- pass 0 (fast): sorted visiting order, branch-free compaction.
-            // Every candidate is stored at the row's next free slot and the slot
-            // advances only when the fp32 distance is inside the outer radius (a
-            // later candidate overwrites a miss).  Entries inside the guard band
-            // carry a tag bit and are settled exactly afterwards.
-            // 32-bit word offsets into this lane's column of s_rows (stride 32 words)
-            int slot = 0;
+            // Candidates are staged kCandCap at a time (several neighbour cells per
+            // batch) so that the scan is one long tight loop.  Every candidate is
+            // stored at the row's next free slot and the slot advances only when
+            // the fp32 distance is inside the outer radius (a later candidate
+            // overwrites a miss).  Entries inside the guard band carry a tag bit
+            // and are settled exactly afterwards.
+            int slot = 0;                               // word offset into this lane's column
             const int slot_cap = (stride + 1) * 32;
-            for (int t = 0; t < 27; ++t) {
-                const int nslot = __shfl_sync(0xffffffffu, sorted_slot, t);
-                int cj; float sx, sy, sz;
-                neighbour_cell(g, cx, cy, cz, nslot, cj, sx, sy, sz);
-                const int p_begin = cell_start[cj], p_end = cell_start[cj + 1];
-                const int self = (cj == (int)c) ? i : -2;      // only the own cell holds j == i
-                for (int p0 = p_begin; p0 < p_end; p0 += 32) {
-                    const int m = min(32, p_end - p0);
+            {
+                int t = 0, p = 0, p_end = 0;
+                float sx = 0.f, sy = 0.f, sz = 0.f;
+                bool have = false;                      // (p, p_end) describe an open cell
+                for (;;) {
+                    int ncand = 0;
                     __syncwarp();
-                    if (lane < m) {
-                        const int j = cell_particles[p0 + lane];
-                        const float4 hj = __ldg(&pos_hi[j]);
-                        s_cand[lane] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
-                                                   __int_as_float(j));
+                    while (ncand < kCandCap) {
+                        if (!have) {
+                            if (t == 27) break;
+                            const int nslot = __shfl_sync(0xffffffffu, sorted_slot, t);
+                            int cj;
+                            neighbour_cell(g, cx, cy, cz, nslot, cj, sx, sy, sz);
+                            p = cell_start[cj];
+                            p_end = cell_start[cj + 1];
+                            have = true;
+                            ++t;
+                        }
+                        const int take = min(p_end - p, kCandCap - ncand);
+                        for (int o = lane; o < take; o += 32) {
+                            const int j = cell_particles[p + o];
+                            const float4 hj = __ldg(&pos_hi[j]);
+                            s_cand[ncand + o] = make_float4(hj.x + sx, hj.y + sy, hj.z + sz,
+                                                            __int_as_float(j));
+                        }
+                        ncand += take;
+                        p += take;
+                        if (p == p_end) have = false;
                     }
+                    if (ncand == 0) break;
                     __syncwarp();
-#pragma unroll 4
-                    for (int q = 0; q < m; ++q) {
+#pragma unroll 8
+                    for (int q = 0; q < ncand; ++q) {
                         const float4 cnd = s_cand[q];
                         const float dx = hi_i.x - cnd.x, dy = hi_i.y - cnd.y, dz = hi_i.z - cnd.z;
                         const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                         const int j = __float_as_int(cnd.w);
-                        const bool take = (r2f <= rl2_out) && (j != self);
+                        const bool take = (r2f <= rl2_out) && (j != i);
                         s_rows[slot] = (r2f >= rl2_in) ? (j | kBandTag) : j;
                         slot = min(slot + (take ? 32 : 0), slot_cap);
                     }
+                    if (t == 27 && !have) break;
                 }
             }
             int found = slot >> 5;
-            // settle guard-band entries exactly (rare) and compact the row
+            // settle guard-band entries exactly (rare), compact, and keep the row
+            // ascending (neighbor.py:152; rows are born nearly sorted)
             {
                 int w = 0;
                 for (int k = 0; k < found; ++k) {
@@ -302,7 +321,15 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                         v &= ~kBandTag;
                         keep = listed_exact(pos_hi, pos_lo, i, v, g);
                     }
-                    if (keep) { s_rows[w * 32] = v; ++w; }
+                    if (keep) {
+                        int b = w - 1;
+                        while (b >= 0 && s_rows[b * 32] > v) {
+                            s_rows[(b + 1) * 32] = s_rows[b * 32];
+                            --b;
+                        }
+                        s_rows[(b + 1) * 32] = v;
+                        ++w;
+                    }
                 }
                 // a row that filled all stride+1 slots may have lost entries: redo exactly
                 if (found <= stride) found = w;
@@ -310,7 +337,8 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
             // ---- pass 1 (only if some row may exceed the budget): reference scan
             // order with exact in-loop decisions, so that the kept prefix is the
             // reference's (first `stride` hits in its order, neighbor.py:145-149).
-            if (__any_sync(0xffffffffu, found > stride)) {
+            const bool redo = __any_sync(0xffffffffu, found > stride);
+            if (redo) {
                 found = 0;
                 for (int t = 0; t < 27; ++t) {
                     int cj; float sx, sy, sz;
@@ -344,16 +372,18 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
                     }
                 }
             }
-            // ---- ascending rows (neighbor.py:152), then publish them
+            // ---- publish (pass-1 rows still need their ascending order)
             const int kept = min(found, stride);
-            for (int a = 1; a < kept; ++a) {
-                const int v = s_rows[a * 32];
-                int b = a - 1;
-                while (b >= 0 && s_rows[b * 32] > v) {
-                    s_rows[(b + 1) * 32] = s_rows[b * 32];
-                    --b;
+            if (redo) {
+                for (int a = 1; a < kept; ++a) {
+                    const int v = s_rows[a * 32];
+                    int b = a - 1;
+                    while (b >= 0 && s_rows[b * 32] > v) {
+                        s_rows[(b + 1) * 32] = s_rows[b * 32];
+                        --b;
+                    }
+                    if (b + 1 != a) s_rows[(b + 1) * 32] = v;
                 }
-                if (b + 1 != a) s_rows[(b + 1) * 32] = v;
             }
             const int kmax = __reduce_max_sync(0xffffffffu, kept);
             for (int k = 0; k < kmax; ++k)
@@ -480,7 +510,7 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
     g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n_rows, kBuildThreads);
-    const size_t warp_smem = 32 * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
+    const size_t warp_smem = kCandCap * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, stride, pitch, d_nbr,
