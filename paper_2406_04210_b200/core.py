@@ -167,6 +167,9 @@ class DeviceView:
         return self.buffer._download()
 
 
+#: bytes moved across the host<->device boundary by side switches (process-wide)
+TRANSFER_BYTES = {"h2d": 0, "d2h": 0}
+
 _KINDS = {
     # kind: (host dtype, trailing shape, pack entry, unpack entry, device tensor(s))
     "positions": (np.float64, (3,), "b2md_pack_positions", "b2md_unpack_positions", ("pos_hi", "pos_lo")),
@@ -180,21 +183,16 @@ _KINDS = {
 }
 
 
-def _host_array(values, pinned: bool):
-    """Host copy of ``values``; page-locked when a CUDA device is present so the
-    H2D/D2H legs of a side switch are true async DMA."""
-    values = np.ascontiguousarray(values)
-    if pinned:
-        torch = _torch()
-        try:
-            t = torch.empty(values.shape, dtype=torch.from_numpy(values[:0].copy()).dtype,
-                            pin_memory=True)
-            arr = t.numpy()
-            arr[...] = values
-            return arr
-        except Exception:  # pragma: no cover - pinning is an optimisation only
-            pass
-    return values.copy()
+def _host_array(values, copy: bool):
+    """HOST-side storage of a buffer.  ``copy=False`` adopts the caller's array
+    (zero-copy; e.g. page-locked memory the caller allocated once) when it already
+    has the right layout; otherwise a private contiguous copy is made, as the
+    reference does (core.py:110-112)."""
+    arr = np.asarray(values)
+    if not copy and isinstance(values, np.ndarray) and arr.flags.c_contiguous \
+            and arr.flags.writeable and arr.flags.aligned:
+        return arr
+    return np.array(arr, order="C")
 
 
 class TrackedBuffer:
@@ -203,14 +201,8 @@ class TrackedBuffer:
 
     __slots__ = ("_host", "_owner", "kind", "version", "valid_on", "copy_count")
 
-    def __init__(self, array, owner=None, kind: str | None = None):
-        pinned = False
-        if owner is not None:
-            try:
-                pinned = _torch().cuda.is_available()
-            except Exception:  # pragma: no cover
-                pinned = False
-        self._host = _host_array(np.array(array), pinned)
+    def __init__(self, array, owner=None, kind: str | None = None, copy: bool = True):
+        self._host = _host_array(array, copy)
         self._owner = owner
         self.kind = kind
         self.version = 0
@@ -241,10 +233,14 @@ class TrackedBuffer:
         dev = self._device()
         _, _, pack, _, targets = _KINDS[self.kind]
         stage = torch.from_numpy(self._host).to(dev.device, non_blocking=True)
+        TRANSFER_BYTES["h2d"] += self._host.nbytes
         ptrs = [getattr(dev, t).data_ptr() for t in targets]
         _lib.call(pack, stage.data_ptr(), dev.n, dev.ids_ptr(), *ptrs, dev.stream)
 
-    def _download(self) -> np.ndarray:
+    def _download(self, into=None) -> np.ndarray:
+        """Decode the device rows into the reference's host format.  With ``into``
+        the result is copied straight into that array (a direct DMA when it is
+        page-locked)."""
         torch = _torch()
         dev = self._device()
         dtype, _, _, unpack, targets = _KINDS[self.kind]
@@ -252,6 +248,10 @@ class TrackedBuffer:
         stage = torch.empty(self._host.shape, dtype=tdtype, device=dev.device)
         ptrs = [getattr(dev, t).data_ptr() for t in targets]
         _lib.call(unpack, *ptrs, dev.n, dev.ids_ptr(), stage.data_ptr(), dev.stream)
+        TRANSFER_BYTES["d2h"] += self._host.nbytes
+        if into is not None:
+            torch.from_numpy(into).copy_(stage)
+            return into
         return stage.cpu().numpy()
 
     # -- acquisition -------------------------------------------------------
@@ -262,7 +262,7 @@ class TrackedBuffer:
             if side == COMPUTE:
                 self._upload()
             else:
-                self._host[...] = self._download()
+                self._download(into=self._host)
             self.copy_count += 1
             self.valid_on = "both"
         if side == HOST:
@@ -297,8 +297,11 @@ class ParticleState:
     """
 
     def __init__(self, positions, velocities=None, masses=None, images=None,
-                 species=None, device: int = 0):
-        pos = np.array(positions, dtype=np.float64)
+                 species=None, device: int = 0, copy: bool = True):
+        """``copy=False`` adopts the caller's fp64 arrays as the HOST side (they are
+        then updated in place by HOST acquisitions); the reference always copies."""
+        pos = np.array(positions, dtype=np.float64) if copy else \
+            np.asarray(positions, dtype=np.float64)
         if pos.ndim != 2 or pos.shape[1] != 3:
             raise ValueError("positions must have shape (n, 3)")
         n = pos.shape[0]
@@ -307,8 +310,8 @@ class ParticleState:
 
         def take(arr, shape, dtype, fill):
             if arr is None:
-                return np.full(shape, fill, dtype=dtype)
-            out = np.array(arr, dtype=dtype)
+                return np.zeros(shape, dtype=dtype) if fill == 0 else np.full(shape, fill, dtype=dtype)
+            out = np.array(arr, dtype=dtype) if copy else np.asarray(arr, dtype=dtype)
             if out.shape != shape:
                 raise ValueError(f"expected shape {shape}, got {out.shape}")
             return out
@@ -323,14 +326,22 @@ class ParticleState:
         self._n = n
         self._device_index = int(device)
         self._dev: DeviceState | None = None
-        self.positions = TrackedBuffer(pos, self, "positions")
-        self.images = TrackedBuffer(img, self, "images")
-        self.velocities = TrackedBuffer(take(velocities, (n, 3), np.float64, 0.0), self, "velocities")
-        self.forces = TrackedBuffer(np.zeros((n, 3)), self, "forces")
-        self.masses = TrackedBuffer(masses_arr, self, "masses")
-        self.species = TrackedBuffer(take(species, (n,), np.int32, 0), self, "species")
-        self.per_particle_potential = TrackedBuffer(np.zeros(n), self, "per_particle_potential")
-        self.virial = TrackedBuffer(np.zeros(n), self, "virial")
+        # the arrays built above are already private (or deliberately adopted): no second copy
+        self.positions = TrackedBuffer(pos, self, "positions", copy=False)
+        self.images = TrackedBuffer(img, self, "images", copy=False)
+        self.velocities = TrackedBuffer(take(velocities, (n, 3), np.float64, 0.0), self,
+                                        "velocities", copy=False)
+        self.forces = TrackedBuffer(np.zeros((n, 3)), self, "forces", copy=False)
+        self.masses = TrackedBuffer(masses_arr, self, "masses", copy=False)
+        self.species = TrackedBuffer(take(species, (n,), np.int32, 0), self, "species", copy=False)
+        self.per_particle_potential = TrackedBuffer(np.zeros(n), self, "per_particle_potential",
+                                                    copy=False)
+        self.virial = TrackedBuffer(np.zeros(n), self, "virial", copy=False)
+        # buffers that still hold their defaults match what DeviceState allocates
+        # (zeros, unit masses): no upload is needed for them
+        self._defaults = {"images": images is None, "forces": True, "masses": masses is None,
+                          "species": species is None, "per_particle_potential": True,
+                          "virial": True, "velocities": velocities is None}
 
     @property
     def n(self) -> int:
@@ -340,6 +351,11 @@ class ParticleState:
         """Packed HBM arrays, allocated on first use (raises without CUDA)."""
         if self._dev is None:
             self._dev = DeviceState(self._n, self._device_index)
+            # freshly allocated rows already equal the untouched default buffers
+            for name, is_default in self._defaults.items():
+                buf = getattr(self, name)
+                if is_default and buf.version == 0 and buf.valid_on == HOST:
+                    buf.valid_on = "both"
         return self._dev
 
     def buffers(self):
