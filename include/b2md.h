@@ -53,7 +53,11 @@ typedef struct b2md_status {
     int32_t rebuild_flag;        /* set by the fused integrate kernel when max_disp2 > (skin/2)^2 */
     uint64_t max_disp2_f64_bits; /* double bits of the exact fp64 displacement maximum */
     int32_t n_boundary;          /* particles flagged as able to interact across a periodic face */
-    int32_t reserved[7];
+    int32_t graph_steps;         /* graph mode: MD steps completed by captured step graphs */
+    int32_t graph_rebuilds;      /* graph mode: list builds done inside step graphs */
+    int32_t frozen;              /* graph mode: set when an in-graph build overflowed; every
+                                    later kernel of the batch returns at once */
+    int32_t reserved[4];
 } b2md_status;
 
 /* Orthorhombic periodic box: edge lengths in fp64 (core.py:25-57).  Inverse
@@ -165,6 +169,7 @@ int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void
  * Writes force (xyz + e_pot in w) and virial.
  * A coincident listed pair is reported in status->singular. */
 #define B2MD_FORCE_SKIP_THERMO 1
+#define B2MD_FORCE_GATED 2        /* return at once when d_status->frozen is set */
 int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                   const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
                   int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
@@ -188,6 +193,12 @@ int b2md_vv_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel, const void *d
                       void *d_image_i4, int64_t n, const b2md_box *box, double dt,
                       void *d_ref_pos_f4, double half_skin2, b2md_status *d_status,
                       void *stream);
+/* Same kernels, but they return immediately when d_status->frozen is set (used by
+ * the captured step graph; kicks = 1 or 2 half-kicks before the drift). */
+int b2md_vv_integrate_gated(void *d_pos_hi, void *d_pos_lo, void *d_vel, const void *d_force_f4,
+                            void *d_image_i4, int64_t n, const b2md_box *box, double dt,
+                            void *d_ref_pos_f4, double half_skin2, b2md_status *d_status,
+                            int32_t kicks, void *stream);
 /* vv_finalize (integrate.py:73-79). */
 int b2md_vv_finalize(void *d_vel, const void *d_force_f4, int64_t n, double dt, void *stream);
 /* finalize of step s fused with integrate of step s+1 (one pass over the state). */
@@ -261,6 +272,11 @@ int b2md_flag_neither(const int32_t *d_a, const int32_t *d_b, int64_t n, int32_t
  *   [async 64-byte status read-back]  [force(s), launched speculatively]
  *   host looks at the flag while the force kernel runs; only if it is set:
  *   bin -> (Hilbert/cell reorder) -> list build -> snapshot -> force again.
+ * With use_graph = 1 the middle steps of a call are launches of ONE captured CUDA
+ * graph per step: integrate -> gate kernel (cudaGraphSetConditional) -> IF node
+ * holding the whole rebuild sequence -> force.  No host round trip per step; an
+ * in-graph overflow freezes the remaining launches of the batch and is then
+ * handled exactly like the ungraphed case.
  *
  * All memory is caller-owned (PyTorch tensors); per-particle arrays come in
  * pairs so a reorder can gather from one set into the other.  The runner never
@@ -295,7 +311,10 @@ typedef struct b2md_runner_config {
     int32_t *perm, *perm_tmp;    /* n each (reorder only) */
     void *sort_scratch;          /* b2md_sort_scratch_bytes(n) */
     b2md_status *status;         /* device */
-    void *stream;
+    void *stream;                /* the caller's stream; the runner orders its own against it */
+    int32_t use_graph;           /* 1: middle steps run as one CUDA graph each (conditional
+                                    rebuild node), no per-step host round trip */
+    int32_t reserved0;
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };
@@ -313,6 +332,7 @@ typedef struct b2md_run_report {
     int32_t n_boundary;
     double max_disp2;            /* last displacement maximum seen (fp32 check) */
     uint64_t singular;           /* status->singular when reason == B2MD_RUN_SINGULAR */
+    int64_t graph_steps;         /* steps of this call that ran as captured graphs */
 } b2md_run_report;
 
 typedef struct b2md_runner b2md_runner;

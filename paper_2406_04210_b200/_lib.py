@@ -27,7 +27,10 @@ class Status(Structure):
         ("rebuild_flag", c_int32),
         ("max_disp2_f64_bits", c_uint64),
         ("n_boundary", c_int32),
-        ("reserved", c_int32 * 7),
+        ("graph_steps", c_int32),
+        ("graph_rebuilds", c_int32),
+        ("frozen", c_int32),
+        ("reserved", c_int32 * 4),
     ]
 
 
@@ -64,6 +67,7 @@ class RunnerConfig(Structure):
         ("keys", c_void_p), ("keys_tmp", c_void_p), ("perm", c_void_p), ("perm_tmp", c_void_p),
         ("sort_scratch", c_void_p),
         ("status", c_void_p), ("stream", c_void_p),
+        ("use_graph", c_int32), ("reserved0", c_int32),
     ]
 
 
@@ -73,7 +77,7 @@ class RunReport(Structure):
         ("reorders", c_int32), ("current", c_int32), ("max_count", c_int32),
         ("wasted_force_launches", c_int32), ("kernel_launches", c_int64),
         ("list_valid", c_int32), ("n_boundary", c_int32), ("max_disp2", c_double),
-        ("singular", c_uint64),
+        ("singular", c_uint64), ("graph_steps", c_int64),
     ]
 
 
@@ -120,6 +124,8 @@ _SIGNATURES = {
                                           _P, _P, _P, _P]),
     "b2md_vv_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,
                                     c_double, _P, _P]),
+    "b2md_vv_integrate_gated": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double,
+                                          _P, c_double, _P, c_int32, _P]),
     "b2md_vv_finalize": (c_int32, [_P, _P, c_int64, c_double, _P]),
     "b2md_vv_finalize_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double,
                                              _P, c_double, _P, _P]),

@@ -146,16 +146,19 @@ __device__ __forceinline__ float4 gather_pos(const float4 *__restrict__ pos,
     return __ldg(pos + j);
 }
 
-template <int SUB, int GATHER, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
-__device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, int k,
-                                         const int (&j)[4], const float4 *__restrict__ pos,
-                                         cudaTextureObject_t tex, const ForceArgs &a,
+template <int GATHER>
+__device__ __forceinline__ void gather4(float4 (&pj)[4], const int (&j)[4],
+                                        const float4 *__restrict__ pos, cudaTextureObject_t tex) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pj[u] = gather_pos<GATHER>(pos, tex, j[u], u);
+}
+
+template <int SUB, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
+__device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, int k,
+                                         const float4 (&pj)[4], const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
                                          int ti_row) {
     const BoxF &b = a.box;
-    float4 pj[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pj[u] = gather_pos<GATHER>(pos, tex, j[u], u);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
@@ -175,13 +178,17 @@ __device__ __forceinline__ void row_trip(RowAcc &acc, const float4 pi, int cnt, 
 // k0 = this lane's first entry (= sub); kmin / kmax = smallest / largest row
 // length among the particles of the warp.  Rows are allocated in multiples of 16
 // and zero-filled, so reads past a row's end stay inside the allocation.
-template <int SUB, int GATHER, bool CAREFUL, bool TABLE, bool THERMO>
+// PIPE = true additionally keeps the NEXT trip's four position gathers in flight
+// while the current trip is being computed (deeper memory-level parallelism at
+// the price of 16 more registers).
+template <int SUB, int GATHER, int PIPEK, bool CAREFUL, bool TABLE, bool THERMO>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
                                          cudaTextureObject_t tex, const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
                                          int ti_row) {
+    constexpr bool PIPE = (PIPEK == 1);
     constexpr int kTrip = 4 * SUB;            // entries of one particle consumed per trip
     const int64_t step = (int64_t)SUB * pitch;
     int ja[4], jb[4];
@@ -190,19 +197,27 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
         ja[u] = (0 < kmax) ? __ldcs(col + u * step) : 0;
         jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
     }
+    float4 pa[4], pb[4];
+    if (PIPE) gather4<GATHER>(pa, ja, pos, tex);
     for (int base = 0; base < kmax; base += kTrip) {
         int jc[4];
         const bool more = base + 2 * kTrip < kmax;          // warp-uniform
 #pragma unroll
         for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (8 + u) * step) : 0;
+        if (PIPE) gather4<GATHER>(pb, jb, pos, tex);         // row 0 is always a valid index
+        else gather4<GATHER>(pa, ja, pos, tex);
         if (base + kTrip <= kmin)
-            row_trip<SUB, GATHER, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, ja, pos,
-                                                                 tex, a, s_tab_a, s_tab_b, ti_row);
+            compute4<SUB, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
+                                                         s_tab_b, ti_row);
         else
-            row_trip<SUB, GATHER, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, ja, pos,
-                                                                tex, a, s_tab_a, s_tab_b, ti_row);
+            compute4<SUB, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
+                                                        s_tab_b, ti_row);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { ja[u] = jb[u]; jb[u] = jc[u]; }
+        for (int u = 0; u < 4; ++u) {
+            ja[u] = jb[u];
+            jb[u] = jc[u];
+            if (PIPE) pa[u] = pb[u];
+        }
         col += 4 * step;
     }
 }
@@ -226,15 +241,19 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
-template <int SUB, int GATHER, bool TABLE, bool THERMO>
-__global__ void __launch_bounds__(kForceThreads, 8)
+// PIPE doubles as the occupancy knob of the experiments: 0 = 8 CTAs/SM (<= 64
+// registers), 1 = gathers one trip ahead with 6 CTAs/SM, 2 = 12 CTAs/SM (<= 40).
+template <int SUB, int GATHER, int PIPE, bool TABLE, bool THERMO>
+__global__ void __launch_bounds__(kForceThreads, PIPE == 1 ? 6 : (PIPE == 2 ? 12 : 8))
 k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
            const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
            const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
-           float *__restrict__ virial, b2md_status *status) {
+           float *__restrict__ virial, b2md_status *status, int gated) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    // step-graph batches: nothing to do once an in-graph list build overflowed
+    if (gated && *(volatile int *)&status->frozen) return;
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -257,10 +276,10 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     if (careful)
-        row_loop<SUB, GATHER, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos,
+        row_loop<SUB, GATHER, PIPE, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos,
                                                    tex, a, s_tab_a, s_tab_b, ti_row);
     else
-        row_loop<SUB, GATHER, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,
+        row_loop<SUB, GATHER, PIPE, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,
                                                     pos, tex, a, s_tab_a, s_tab_b, ti_row);
 #pragma unroll
     for (int o = SUB >> 1; o > 0; o >>= 1) {
@@ -430,7 +449,7 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
     // tuning knobs (defaults chosen from profiles/)
-    static int sub = 0, gather = -1;
+    static int sub = 0, gather = -1, pipe = 0;
     if (sub == 0) {
         const char *env = getenv("B2MD_FORCE_SUBWARP");       // lanes per particle: 1, 2, 4
         const int v = env ? atoi(env) : 1;
@@ -438,6 +457,8 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 1 TEX, 2 alternate
         const int w = env ? atoi(env) : 0;
         gather = (w >= 0 && w <= 2) ? w : 0;
+        env = getenv("B2MD_FORCE_PIPE");        // 1: gathers one trip ahead, 2: 12 CTAs/SM
+        pipe = env ? atoi(env) : 0;
     }
     cudaTextureObject_t tex = 0;
     if (gather != 0) {
@@ -445,29 +466,31 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         rc = position_texture(d_pos_hi, (size_t)pitch, &tex);
         if (rc) return rc;
     }
-#define B2MD_LAUNCH_FORCE(SUB, GATHER, TABLE, THERMO)                                        \
-    k_force_lj<SUB, GATHER, TABLE, THERMO>                                                   \
+#define B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, TABLE, THERMO)                                  \
+    k_force_lj<SUB, GATHER, PIPE, TABLE, THERMO>                                             \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
             (const float4 *)d_pos_hi, tex, n, a, d_nbr, d_counts, pitch, d_boundary,         \
-            (float4 *)d_force_f4, d_virial, d_status)
-#define B2MD_DISPATCH_TT(SUB, GATHER)                                                        \
+            (float4 *)d_force_f4, d_virial, d_status, (flags & B2MD_FORCE_GATED) ? 1 : 0)
+#define B2MD_DISPATCH_TT(SUB, GATHER, PIPE)                                                  \
     do {                                                                                     \
         if (ntypes == 1) {                                                                   \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, false, true);                         \
-            else B2MD_LAUNCH_FORCE(SUB, GATHER, false, false);                               \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, false, true);                   \
+            else B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, false, false);                         \
         } else {                                                                             \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, true, true);                          \
-            else B2MD_LAUNCH_FORCE(SUB, GATHER, true, false);                                \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, true, true);                    \
+            else B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, true, false);                          \
         }                                                                                    \
     } while (0)
     if (sub == 1) {
-        if (gather == 0) B2MD_DISPATCH_TT(1, 0);
-        else if (gather == 1) B2MD_DISPATCH_TT(1, 1);
-        else B2MD_DISPATCH_TT(1, 2);
+        if (pipe == 1) B2MD_DISPATCH_TT(1, 0, 1);
+        else if (pipe == 2) B2MD_DISPATCH_TT(1, 0, 2);
+        else if (gather == 0) B2MD_DISPATCH_TT(1, 0, 0);
+        else if (gather == 1) B2MD_DISPATCH_TT(1, 1, 0);
+        else B2MD_DISPATCH_TT(1, 2, 0);
     } else if (sub == 2) {
-        B2MD_DISPATCH_TT(2, 0);
+        B2MD_DISPATCH_TT(2, 0, 0);
     } else {
-        B2MD_DISPATCH_TT(4, 0);
+        B2MD_DISPATCH_TT(4, 0, 0);
     }
 #undef B2MD_DISPATCH_TT
 #undef B2MD_LAUNCH_FORCE

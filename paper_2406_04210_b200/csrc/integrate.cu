@@ -60,12 +60,14 @@ __device__ __forceinline__ void drift(float &hi, float &lo, float v, float dt_hi
     ds_add(hi, lo, ph, pl);
 }
 
-template <int KICKS>
+template <int KICKS, bool GATED>
 __global__ void __launch_bounds__(kThreads)
 k_integrate(float4 *__restrict__ pos_hi, float4 *__restrict__ pos_lo, float4 *__restrict__ vel,
             const float4 *__restrict__ force, int4 *__restrict__ image, int64_t n,
             const StepConst c, float4 *__restrict__ ref_pos, b2md_status *status) {
     __shared__ float s_max[kThreads / 32];
+    // step-graph batches stop advancing once an in-graph list build overflowed
+    if (GATED && *(volatile int *)&status->frozen) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     float d2 = 0.0f;
     if (i < n) {
@@ -143,14 +145,15 @@ static StepConst make_step(const b2md_box *box, double dt, double half_skin2) {
     return c;
 }
 
-template <int KICKS>
+template <int KICKS, bool GATED = false>
 static int launch_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel, const void *d_force,
                             void *d_image, int64_t n, const b2md_box *box, double dt,
                             void *d_ref_pos, double half_skin2, b2md_status *d_status,
                             void *stream, const char *name) {
     if (n <= 0 || !box || !(dt > 0.0)) { set_error("%s: bad arguments", name); return -1; }
     if (d_ref_pos && !d_status) { set_error("%s: displacement check needs a status block", name); return -2; }
-    k_integrate<KICKS><<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+    if (GATED && !d_status) { set_error("%s: gated launch needs a status block", name); return -3; }
+    k_integrate<KICKS, GATED><<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
         (float4 *)d_pos_hi, (float4 *)d_pos_lo, (float4 *)d_vel, (const float4 *)d_force,
         (int4 *)d_image, n, make_step(box, dt, half_skin2), (float4 *)d_ref_pos, d_status);
     B2MD_CHECK_LAUNCH(name);
@@ -177,6 +180,20 @@ B2MD_EXPORT int b2md_vv_finalize_integrate(void *d_pos_hi, void *d_pos_lo, void 
     return launch_integrate<2>(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n, box, dt,
                                d_ref_pos_f4, half_skin2, d_status, stream,
                                "b2md_vv_finalize_integrate");
+}
+
+B2MD_EXPORT int b2md_vv_integrate_gated(void *d_pos_hi, void *d_pos_lo, void *d_vel,
+                                        const void *d_force_f4, void *d_image_i4, int64_t n,
+                                        const b2md_box *box, double dt, void *d_ref_pos_f4,
+                                        double half_skin2, b2md_status *d_status, int32_t kicks,
+                                        void *stream) {
+    if (kicks == 2)
+        return launch_integrate<2, true>(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n, box,
+                                         dt, d_ref_pos_f4, half_skin2, d_status, stream,
+                                         "b2md_vv_integrate_gated");
+    return launch_integrate<1, true>(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n, box, dt,
+                                     d_ref_pos_f4, half_skin2, d_status, stream,
+                                     "b2md_vv_integrate_gated");
 }
 
 B2MD_EXPORT int b2md_vv_finalize(void *d_vel, const void *d_force_f4, int64_t n, double dt,

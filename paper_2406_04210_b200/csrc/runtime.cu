@@ -2,15 +2,26 @@
 // core.py:262-279) with the rebuild policy of Simulation._compute_forces and
 // _rebuild (sim.py:114-149), driven from C++.
 //
-// Per MD step the stream sees
-//     k_integrate<2>   finalize(s-1) + integrate(s) + displacement check
+// Ungraphed step (first / last step of a call, and every step when use_graph = 0):
+//     k_integrate      finalize(s-1) + integrate(s) + displacement check
 //     64-byte D2H      status block -> pinned host copy, then an event
 //     k_force_lj       launched speculatively with the current list
-// and the host inspects the rebuild flag while the force kernel is running.  In
-// the common case (flag clear) nothing else happens and the GPU never idles.  If
-// the flag is set, the speculative forces are discarded: bin -> optional reorder
-// -> list build -> snapshot, the overflow word is read (one sync per rebuild),
-// and the force kernel is launched again on the fresh list.
+// The host inspects the rebuild flag while the force kernel is running.  In the
+// common case (flag clear) nothing else happens and the GPU never idles.  If the
+// flag is set, the speculative forces are discarded: (reorder) -> bin -> list
+// build -> snapshot, the overflow word is read (one sync per rebuild), and the
+// force kernel is launched again on the fresh list.
+//
+// Graphed step (use_graph = 1, middle steps of a call): one cudaGraphLaunch per MD
+// step and no host round trip at all --
+//     k_integrate<2, gated> -> k_graph_gate (cudaGraphSetConditional(flag))
+//       -> IF node { whole rebuild sequence, k_graph_after_build }
+//       -> k_force_lj (gated) -> k_graph_step_done
+// Pointers are baked into the graph, so a reorder inside the graph gathers into the
+// spare buffers and copies back.  A list build that overflows inside the graph sets
+// status->frozen: the remaining launches of the batch return immediately, the host
+// reads how many steps really completed and continues exactly like the ungraphed
+// overflow case (grow the stride, rebuild, resume the interrupted step).
 #include <new>
 #include <vector>
 
@@ -30,8 +41,15 @@ struct b2md_runner {
     bool mid_step;            // stopped after integrate, before a successful rebuild
     int rebuilds_total;
     b2md_status *h_status;    // pinned
-    cudaEvent_t ev;
+    cudaEvent_t ev;           // flag read-back
+    cudaEvent_t ev_in;        // ordering against the caller's stream
+    cudaStream_t stream;      // the runner's own (capturable) stream
     int64_t launches;
+    // step graph
+    cudaGraph_t graph;
+    cudaGraphExec_t graph_exec;
+    int64_t graph_launch_kernels;   // kernels in the always-executed part of the graph
+    int64_t graph_rebuild_kernels;  // kernels inside the conditional body
 };
 
 namespace {
@@ -41,91 +59,137 @@ struct Set {
     float *virial;
 };
 
-Set live(const b2md_runner *r) {
+Set buffer_set(const b2md_runner *r, int k) {
     const b2md_runner_config &c = r->cfg;
-    const int k = r->current;
     return Set{c.pos_hi[k], c.pos_lo[k], c.vel[k], c.force[k], c.image[k], c.virial[k]};
 }
+Set live(const b2md_runner *r) { return buffer_set(r, r->current); }
+Set spare(const b2md_runner *r) { return buffer_set(r, 1 - r->current); }
 
-Set spare(const b2md_runner *r) {
-    const b2md_runner_config &c = r->cfg;
-    const int k = 1 - r->current;
-    return Set{c.pos_hi[k], c.pos_lo[k], c.vel[k], c.force[k], c.image[k], c.virial[k]};
+int stride_rows(const b2md_runner *r) { return (r->cfg.stride + 15) / 16 * 16; }
+
+__global__ void k_graph_gate(cudaGraphConditionalHandle handle, const b2md_status *status) {
+    const bool go = !status->frozen && status->rebuild_flag != 0;
+    cudaGraphSetConditional(handle, go ? 1u : 0u);
+}
+
+__global__ void k_graph_after_build(b2md_status *status) {
+    status->graph_rebuilds += 1;
+    if (status->overflow) status->frozen = 1;
+}
+
+__global__ void k_graph_step_done(b2md_status *status) {
+    if (!status->frozen) status->graph_steps += 1;
+}
+
+__global__ void k_graph_batch_reset(b2md_status *status) {
+    status->graph_steps = 0;
+    status->graph_rebuilds = 0;
+    status->frozen = 0;
 }
 
 int read_status(b2md_runner *r) {
-    cudaStream_t s = as_stream(r->cfg.stream);
     int rc = check_cuda(cudaMemcpyAsync(r->h_status, r->cfg.status, sizeof(b2md_status),
-                                        cudaMemcpyDeviceToHost, s), "status read-back");
+                                        cudaMemcpyDeviceToHost, r->stream), "status read-back");
     if (rc) return rc;
-    return check_cuda(cudaStreamSynchronize(s), "status sync");
+    return check_cuda(cudaStreamSynchronize(r->stream), "status sync");
 }
 
 // thermo = false on steps whose per-particle energies cannot be observed
-int launch_force(b2md_runner *r, bool thermo) {
+int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     r->launches += 1;
-    return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, (c.stride + 15) / 16 * 16,
-                         c.boundary, r->table.data(), c.ntypes,
-                         thermo ? 0 : B2MD_FORCE_SKIP_THERMO, a.force, a.virial, c.status,
-                         c.stream);
+    const int flags = (thermo ? 0 : B2MD_FORCE_SKIP_THERMO) | (gated ? B2MD_FORCE_GATED : 0);
+    return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, stride_rows(r),
+                         c.boundary, r->table.data(), c.ntypes, flags, a.force, a.virial,
+                         c.status, r->stream);
 }
 
-int reorder(b2md_runner *r) {
+int reorder_key_bits(const b2md_runner *r) {
+    const b2md_runner_config &c = r->cfg;
+    if (c.reorder_mode == 1) return b2md_hilbert_key_bits(&r->grid, c.hilbert_bits);
+    int key_bits = 1;
+    while ((1ll << key_bits) < r->grid.n_cells) ++key_bits;
+    return key_bits;
+}
+
+// Enqueue key generation, sort and row gathers.  write_back = false: the spare set
+// becomes the live one (pointer swap); write_back = true: rows are copied back so
+// that the live pointers never change (needed inside a captured graph).
+int enqueue_reorder(b2md_runner *r, bool write_back, int64_t *kernels) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r), b = spare(r);
+    cudaStream_t s = r->stream;
     int rc;
-    int key_bits;
+    const int key_bits = reorder_key_bits(r);
+    if (key_bits < 0) { set_error("reorder: Hilbert key does not fit"); return -5; }
     if (c.reorder_mode == 1) {
-        rc = b2md_hilbert_keys(a.pos_hi, a.pos_lo, c.n, &r->grid, c.hilbert_bits, c.keys, c.stream);
-        key_bits = b2md_hilbert_key_bits(&r->grid, c.hilbert_bits);
-        if (key_bits < 0) { set_error("reorder: Hilbert key does not fit"); return -5; }
+        rc = b2md_hilbert_keys(a.pos_hi, a.pos_lo, c.n, &r->grid, c.hilbert_bits, c.keys, s);
     } else {
         // cell order needs the cell of every particle first
         rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,
-                      c.cell_particles, c.bin_scratch, c.stream);
-        r->launches += 6;
+                      c.cell_particles, c.bin_scratch, s);
+        *kernels += 6;
         if (rc) return rc;
-        rc = b2md_cell_keys(c.cell_of, c.n, c.keys, c.stream);
-        key_bits = 1;
-        while ((1ll << key_bits) < r->grid.n_cells) ++key_bits;
+        rc = b2md_cell_keys(c.cell_of, c.n, c.keys, s);
     }
     if (rc) return rc;
-    if ((rc = b2md_iota_i32(c.perm, c.n, c.stream))) return rc;
+    if ((rc = b2md_iota_i32(c.perm, c.n, s))) return rc;
     if ((rc = b2md_sort_pairs_u64(c.keys, c.perm, c.keys_tmp, c.perm_tmp, c.n, key_bits,
-                                  c.sort_scratch, c.stream))) return rc;
-    r->launches += 2 + 5 * ((key_bits + 7) / 8);
-    if ((rc = b2md_gather16(a.pos_hi, b.pos_hi, c.perm, c.n, c.stream))) return rc;
-    if ((rc = b2md_gather16(a.pos_lo, b.pos_lo, c.perm, c.n, c.stream))) return rc;
-    if ((rc = b2md_gather16(a.vel, b.vel, c.perm, c.n, c.stream))) return rc;
-    if ((rc = b2md_gather16(a.force, b.force, c.perm, c.n, c.stream))) return rc;
-    if ((rc = b2md_gather16(a.image, b.image, c.perm, c.n, c.stream))) return rc;
-    if ((rc = b2md_gather4(a.virial, b.virial, c.perm, c.n, c.stream))) return rc;
-    r->launches += 6;
-    r->current = 1 - r->current;
+                                  c.sort_scratch, s))) return rc;
+    *kernels += 2 + 5 * ((key_bits + 7) / 8);
+    if ((rc = b2md_gather16(a.pos_hi, b.pos_hi, c.perm, c.n, s))) return rc;
+    if ((rc = b2md_gather16(a.pos_lo, b.pos_lo, c.perm, c.n, s))) return rc;
+    if ((rc = b2md_gather16(a.vel, b.vel, c.perm, c.n, s))) return rc;
+    if ((rc = b2md_gather16(a.force, b.force, c.perm, c.n, s))) return rc;
+    if ((rc = b2md_gather16(a.image, b.image, c.perm, c.n, s))) return rc;
+    if ((rc = b2md_gather4(a.virial, b.virial, c.perm, c.n, s))) return rc;
+    *kernels += 6;
+    if (write_back) {
+        const size_t row = 16 * (size_t)c.n;
+        void *dst[5] = {a.pos_hi, a.pos_lo, a.vel, a.force, a.image};
+        void *src[5] = {b.pos_hi, b.pos_lo, b.vel, b.force, b.image};
+        for (int k = 0; k < 5; ++k)
+            if ((rc = check_cuda(cudaMemcpyAsync(dst[k], src[k], row, cudaMemcpyDeviceToDevice, s),
+                                 "reorder copy-back"))) return rc;
+        if ((rc = check_cuda(cudaMemcpyAsync(a.virial, b.virial, 4 * (size_t)c.n,
+                                             cudaMemcpyDeviceToDevice, s), "reorder copy-back")))
+            return rc;
+    } else {
+        r->current = 1 - r->current;
+    }
     return 0;
 }
 
-// bin -> (reorder) -> build -> snapshot; leaves overflow/max_count in h_status.
-int rebuild(b2md_runner *r, b2md_run_report *rep) {
+// (reorder) -> status reset -> bin -> build -> snapshot, nothing synchronous.
+int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *kernels) {
     const b2md_runner_config &c = r->cfg;
+    cudaStream_t s = r->stream;
     int rc;
-    if (c.reorder_mode != 0 && (r->rebuilds_total % c.reorder_every) == 0) {
-        if ((rc = reorder(r))) return rc;
-        rep->reorders += 1;
-    }
+    if (do_reorder && (rc = enqueue_reorder(r, write_back, kernels))) return rc;
     Set a = live(r);
-    if ((rc = b2md_status_reset_list(c.status, c.stream))) return rc;
+    if ((rc = b2md_status_reset_list(c.status, s))) return rc;
     if ((rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,
-                       c.cell_particles, c.bin_scratch, c.stream))) return rc;
+                       c.cell_particles, c.bin_scratch, s))) return rc;
     if ((rc = b2md_build_nlist(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
                                c.cell_start, c.cell_particles, r->r_list, c.stride, c.pitch,
-                               c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n,
-                               c.status, c.stream))) return rc;
-    if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos,
-                            c.stream))) return rc;
-    r->launches += 1 + 6 + 2 + 1;
+                               c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n, c.status, s)))
+        return rc;
+    if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos, s)))
+        return rc;
+    *kernels += 1 + 6 + 2 + 1;
+    return 0;
+}
+
+// Ungraphed rebuild: enqueue, then read overflow / max_count (one sync).
+int rebuild(b2md_runner *r, b2md_run_report *rep) {
+    const b2md_runner_config &c = r->cfg;
+    const bool do_reorder = c.reorder_mode != 0 && (r->rebuilds_total % c.reorder_every) == 0;
+    // graph mode keeps the live pointers fixed (they are baked into the step graph)
+    int rc = enqueue_rebuild(r, do_reorder, c.use_graph != 0, &r->launches);
+    if (rc) return rc;
+    if (do_reorder) rep->reorders += 1;
     r->rebuilds_total += 1;
     rep->rebuilds += 1;
     if ((rc = read_status(r))) return rc;
@@ -135,13 +199,192 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
     return 0;
 }
 
+void destroy_graph(b2md_runner *r) {
+    if (r->graph_exec) cudaGraphExecDestroy(r->graph_exec);
+    if (r->graph) cudaGraphDestroy(r->graph);
+    r->graph_exec = nullptr;
+    r->graph = nullptr;
+}
+
+// Capture one MD step (fused integrate, conditional rebuild, no-thermo force).
+int build_graph(b2md_runner *r) {
+    const b2md_runner_config &c = r->cfg;
+    destroy_graph(r);
+    cudaStream_t s = r->stream;
+    int rc;
+    if ((rc = check_cuda(cudaGraphCreate(&r->graph, 0), "cudaGraphCreate"))) return rc;
+    cudaGraphConditionalHandle handle;
+    if ((rc = check_cuda(cudaGraphConditionalHandleCreate(&handle, r->graph, 0,
+                                                          cudaGraphCondAssignDefault),
+                         "cudaGraphConditionalHandleCreate"))) return rc;
+    int64_t main_kernels = 0, body_kernels = 0;
+    if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, r->graph, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeRelaxed),
+                         "begin capture"))) return rc;
+    Set a = live(r);
+    rc = b2md_vv_integrate_gated(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
+                                 c.ref_pos, r->half_skin2, c.status, 2, s);
+    k_graph_gate<<<1, 1, 0, s>>>(handle, c.status);
+    main_kernels += 2;
+    // splice the conditional node in after what has been captured so far
+    cudaStreamCaptureStatus cap_status;
+    cudaGraph_t cap_graph = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t n_deps = 0;
+    cudaGraphNode_t cond_node = nullptr;
+    cudaGraphNodeParams params = {};
+    if (!rc) rc = check_cuda(cudaStreamGetCaptureInfo(s, &cap_status, nullptr, &cap_graph, &deps,
+                                                      &n_deps), "capture info");
+    if (!rc) {
+        params.type = cudaGraphNodeTypeConditional;
+        params.conditional.handle = handle;
+        params.conditional.type = cudaGraphCondTypeIf;
+        params.conditional.size = 1;
+        rc = check_cuda(cudaGraphAddNode(&cond_node, r->graph, deps, n_deps, &params),
+                        "add conditional node");
+    }
+    if (!rc) rc = check_cuda(cudaStreamUpdateCaptureDependencies(
+                                 s, &cond_node, 1, cudaStreamSetCaptureDependencies),
+                             "update capture dependencies");
+    if (!rc) {
+        rc = launch_force(r, false, true);
+        r->launches -= 1;    // only captured, not launched
+    }
+    if (!rc) { k_graph_step_done<<<1, 1, 0, s>>>(c.status); main_kernels += 2; }
+    cudaGraph_t ended = nullptr;
+    int rc_end = check_cuda(cudaStreamEndCapture(s, &ended), "end capture");
+    if (rc) return rc;
+    if (rc_end) return rc_end;
+
+    // body of the IF node: the whole rebuild, captured on the same stream
+    cudaGraph_t body = params.conditional.phGraph_out[0];
+    if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeRelaxed),
+                         "begin body capture"))) return rc;
+    rc = enqueue_rebuild(r, c.reorder_mode != 0, true, &body_kernels);
+    if (!rc) { k_graph_after_build<<<1, 1, 0, s>>>(c.status); body_kernels += 1; }
+    rc_end = check_cuda(cudaStreamEndCapture(s, &ended), "end body capture");
+    if (rc) return rc;
+    if (rc_end) return rc_end;
+    if ((rc = check_cuda(cudaGraphInstantiate(&r->graph_exec, r->graph, 0), "graph instantiate")))
+        return rc;
+    r->graph_launch_kernels = main_kernels;
+    r->graph_rebuild_kernels = body_kernels;
+    return 0;
+}
+
 void finish_report(b2md_runner *r, b2md_run_report *rep, int64_t launches_before) {
     rep->current = r->current;
     rep->kernel_launches = r->launches - launches_before;
     rep->list_valid = r->list_valid ? 1 : 0;
 }
 
+// Make the runner's stream wait for everything the caller enqueued so far.
+int order_after_caller(b2md_runner *r) {
+    cudaStream_t caller = as_stream(r->cfg.stream);
+    int rc = check_cuda(cudaEventRecord(r->ev_in, caller), "order event record");
+    if (rc) return rc;
+    return check_cuda(cudaStreamWaitEvent(r->stream, r->ev_in, 0), "order stream wait");
+}
+
+// One ungraphed step.  *stop = 1 when the call must return (overflow / singular).
+int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before, int *stop) {
+    const b2md_runner_config &c = r->cfg;
+    cudaStream_t s = r->stream;
+    Set a = live(r);
+    int rc;
+    *stop = 0;
+    if (r->pending_kick)
+        rc = b2md_vv_finalize_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box,
+                                        c.dt, c.ref_pos, r->half_skin2, c.status, s);
+    else
+        rc = b2md_vv_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
+                               c.ref_pos, r->half_skin2, c.status, s);
+    if (rc) return rc;
+    r->launches += 1;
+    r->pending_kick = false;
+    if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
+                                         cudaMemcpyDeviceToHost, s), "flag read-back"))) return rc;
+    if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
+    if ((rc = launch_force(r, thermo))) return rc;           // speculative
+    if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
+    rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
+    if (r->h_status->singular != ~0ull) {
+        // a force evaluation of an earlier step met a coincident pair
+        // (forces.py:113-116); stop after draining the stream
+        if ((rc = read_status(r))) return rc;
+        rep->singular = r->h_status->singular;
+        rep->reason = B2MD_RUN_SINGULAR;
+        r->pending_kick = true;
+        rep->steps_done += 1;
+        finish_report(r, rep, before);
+        *stop = 1;
+        return 0;
+    }
+    if (r->h_status->rebuild_flag) {
+        rep->wasted_force_launches += 1;
+        if ((rc = rebuild(r, rep))) return rc;
+        if (!r->list_valid) {
+            r->mid_step = true;
+            rep->reason = B2MD_RUN_OVERFLOW;
+            finish_report(r, rep, before);
+            *stop = 1;
+            return 0;
+        }
+        if ((rc = launch_force(r, thermo))) return rc;
+    }
+    r->pending_kick = true;
+    rep->steps_done += 1;
+    return 0;
+}
+
+// A batch of graphed steps.  *stop = 1 on overflow / singular.
+int graph_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_batch, int64_t before, int *stop) {
+    const b2md_runner_config &c = r->cfg;
+    cudaStream_t s = r->stream;
+    int rc;
+    *stop = 0;
+    if (!r->graph_exec && (rc = build_graph(r))) return rc;
+    k_graph_batch_reset<<<1, 1, 0, s>>>(c.status);
+    for (int64_t k = 0; k < n_batch; ++k)
+        if ((rc = check_cuda(cudaGraphLaunch(r->graph_exec, s), "cudaGraphLaunch"))) return rc;
+    if ((rc = read_status(r))) return rc;
+    const b2md_status &st = *r->h_status;
+    rep->steps_done += st.graph_steps;
+    rep->graph_steps += st.graph_steps;
+    rep->rebuilds += st.graph_rebuilds;
+    r->rebuilds_total += st.graph_rebuilds;
+    if (c.reorder_mode != 0) rep->reorders += st.graph_rebuilds;
+    r->launches += 1 + st.graph_steps * r->graph_launch_kernels +
+                   st.graph_rebuilds * r->graph_rebuild_kernels;
+    rep->max_disp2 = (double)__builtin_bit_cast(float, st.max_disp2_bits);
+    if (st.graph_rebuilds) {
+        rep->max_count = st.max_count;
+        rep->n_boundary = st.n_boundary;
+    }
+    if (st.frozen) {
+        // the step after the last completed one integrated, then its build overflowed
+        r->list_valid = false;
+        r->mid_step = true;
+        r->pending_kick = false;
+        rep->reason = B2MD_RUN_OVERFLOW;
+        finish_report(r, rep, before);
+        *stop = 1;
+        return 0;
+    }
+    r->pending_kick = true;
+    if (st.singular != ~0ull) {
+        rep->singular = st.singular;
+        rep->reason = B2MD_RUN_SINGULAR;
+        finish_report(r, rep, before);
+        *stop = 1;
+    }
+    return 0;
+}
+
 }  // namespace
+
+B2MD_EXPORT void b2md_runner_destroy(b2md_runner *r);
 
 B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     if (!cfg || cfg->n <= 0 || cfg->capacity < cfg->n || !cfg->status || !cfg->nbr ||
@@ -169,10 +412,21 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->mid_step = false;
     r->rebuilds_total = 0;
     r->launches = 0;
+    r->graph = nullptr;
+    r->graph_exec = nullptr;
+    r->h_status = nullptr;
+    r->ev = r->ev_in = nullptr;
+    r->stream = nullptr;
+    // in-graph rebuilds always reorder (the decision cannot depend on a host counter)
+    if (r->cfg.use_graph && r->cfg.reorder_mode != 0 && r->cfg.reorder_every != 1)
+        r->cfg.use_graph = 0;
     if (b2md_grid_shape(&cfg->box, r->r_list, &r->grid)) { delete r; return nullptr; }
     if (check_cuda(cudaMallocHost((void **)&r->h_status, sizeof(b2md_status)), "cudaMallocHost") ||
-        check_cuda(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming), "cudaEventCreate")) {
-        delete r;
+        check_cuda(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming), "cudaEventCreate") ||
+        check_cuda(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming), "cudaEventCreate") ||
+        check_cuda(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking),
+                   "cudaStreamCreate")) {
+        b2md_runner_destroy(r);
         return nullptr;
     }
     return r;
@@ -180,8 +434,11 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
 
 B2MD_EXPORT void b2md_runner_destroy(b2md_runner *r) {
     if (!r) return;
-    cudaFreeHost(r->h_status);
-    cudaEventDestroy(r->ev);
+    destroy_graph(r);
+    if (r->h_status) cudaFreeHost(r->h_status);
+    if (r->ev) cudaEventDestroy(r->ev);
+    if (r->ev_in) cudaEventDestroy(r->ev_in);
+    if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
 }
 
@@ -190,6 +447,7 @@ B2MD_EXPORT int b2md_runner_set_list(b2md_runner *r, int32_t *nbr, int32_t strid
     r->cfg.nbr = nbr;
     r->cfg.stride = stride;
     r->list_valid = false;
+    destroy_graph(r);          // the list pointer and stride are baked into the graph
     return 0;
 }
 
@@ -197,8 +455,9 @@ B2MD_EXPORT int b2md_runner_prepare(b2md_runner *r, b2md_run_report *rep) {
     if (!r || !rep) { set_error("b2md_runner_prepare: null argument"); return -1; }
     *rep = b2md_run_report();
     const int64_t before = r->launches;
-    int rc = rebuild(r, rep);
+    int rc = order_after_caller(r);
     if (rc) return rc;
+    if ((rc = rebuild(r, rep))) return rc;
     if (!r->list_valid) {
         rep->reason = B2MD_RUN_OVERFLOW;
         finish_report(r, rep, before);
@@ -219,12 +478,12 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
     *rep = b2md_run_report();
     const int64_t before = r->launches;
     const b2md_runner_config &c = r->cfg;
-    cudaStream_t s = as_stream(c.stream);
-    int rc;
+    int rc, stop = 0;
     if (!r->list_valid && !r->mid_step) {
         set_error("b2md_runner_run: no valid neighbour list; call b2md_runner_prepare first");
         return -2;
     }
+    if ((rc = order_after_caller(r))) return rc;
     if (r->mid_step) {
         // previous call stopped on overflow after integrating: finish that step
         if ((rc = rebuild(r, rep))) return rc;
@@ -239,53 +498,19 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
         rep->steps_done += 1;
     }
     while (rep->steps_done < n_steps) {
-        Set a = live(r);
-        if (r->pending_kick)
-            rc = b2md_vv_finalize_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n,
-                                            &c.box, c.dt, c.ref_pos, r->half_skin2, c.status, s);
-        else
-            rc = b2md_vv_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
-                                   c.ref_pos, r->half_skin2, c.status, s);
-        if (rc) return rc;
-        r->launches += 1;
-        r->pending_kick = false;
-        if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
-                                             cudaMemcpyDeviceToHost, s), "flag read-back")))
-            return rc;
-        if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
-        // energies / virial only on the step the caller can observe (the last one)
-        const bool thermo = rep->steps_done + 1 >= n_steps;
-        if ((rc = launch_force(r, thermo))) return rc;     // speculative
-        if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
-        rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
-        if (r->h_status->singular != ~0ull) {
-            // a force evaluation of an earlier step met a coincident pair
-            // (forces.py:113-116); stop after draining the stream
-            if ((rc = read_status(r))) return rc;
-            rep->singular = r->h_status->singular;
-            rep->reason = B2MD_RUN_SINGULAR;
-            r->pending_kick = true;
-            rep->steps_done += 1;
-            finish_report(r, rep, before);
-            return 0;
+        const int64_t left = n_steps - rep->steps_done;
+        // graphed steps need the fused kick and must not be the observable last step
+        if (c.use_graph && r->pending_kick && left > 1) {
+            if ((rc = graph_batch(r, rep, left - 1, before, &stop))) return rc;
+        } else {
+            // energies / virial only on the step the caller can observe (the last one)
+            if ((rc = plain_step(r, rep, left == 1, before, &stop))) return rc;
         }
-        if (r->h_status->rebuild_flag) {
-            rep->wasted_force_launches += 1;
-            if ((rc = rebuild(r, rep))) return rc;
-            if (!r->list_valid) {
-                r->mid_step = true;
-                rep->reason = B2MD_RUN_OVERFLOW;
-                finish_report(r, rep, before);
-                return 0;
-            }
-            if ((rc = launch_force(r, thermo))) return rc;
-        }
-        r->pending_kick = true;
-        rep->steps_done += 1;
+        if (stop) return 0;
     }
     if (finalize_at_end && r->pending_kick) {
         Set a = live(r);
-        if ((rc = b2md_vv_finalize(a.vel, a.force, c.n, c.dt, s))) return rc;
+        if ((rc = b2md_vv_finalize(a.vel, a.force, c.n, c.dt, r->stream))) return rc;
         r->launches += 1;
         r->pending_kick = false;
     }

@@ -29,7 +29,9 @@ __global__ void k_status_reset(b2md_status *st, bool keep_singular) {
     st->rebuild_flag = 0;
     st->max_disp2_f64_bits = 0ull;
     st->n_boundary = 0;
-    for (int k = 0; k < 7; ++k) st->reserved[k] = 0;
+    // graph_steps / graph_rebuilds / frozen belong to the step-graph batch and are
+    // reset by the runner, not here
+    for (int k = 0; k < 4; ++k) st->reserved[k] = 0;
 }
 
 __global__ void k_pack_positions(const double *__restrict__ src, int64_t n,

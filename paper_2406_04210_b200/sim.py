@@ -60,7 +60,7 @@ class Simulation:
                  sample_interval: int = 100, deterministic: bool = True,
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
-                 stride_policy: str = "fit"):
+                 stride_policy: str = "fit", graph: bool = True):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -72,8 +72,8 @@ class Simulation:
                               "(SURVEY.md section 8 row f3); run NVE")
         if reorder not in _REORDER_MODES:
             raise ConfigError(f"unknown reorder mode {reorder!r}")
-        if stride_policy not in ("fit", "double"):
-            raise ConfigError("stride_policy must be 'fit' or 'double'")
+        if stride_policy not in ("fit", "double", "tight"):
+            raise ConfigError("stride_policy must be 'fit', 'double' or 'tight'")
 
         self.state = state
         self.box = box
@@ -87,6 +87,8 @@ class Simulation:
         self.reorder = reorder if force_mode == TRUNCATED else None
         self.reorder_every = max(int(reorder_every), 1)
         self.stride_policy = stride_policy
+        self.graph = bool(graph)
+        self.graph_steps = 0
         self.native = (force_mode == TRUNCATED) if native is None else bool(native)
         if self.native and force_mode != TRUNCATED:
             raise ConfigError("the native step loop drives truncated forces only")
@@ -152,6 +154,8 @@ class Simulation:
     def _grow_stride(self, max_count: int):
         if self.stride_policy == "double":
             self._stride *= 2                       # sim.py:149
+        elif self.stride_policy == "tight":         # exactly what the fullest row wanted
+            self._stride = max(self._stride + 1, int(max_count))
         else:
             self._stride = max(self._stride + 1, _round_up(int(max_count * 1.125) + 1, 8))
 
@@ -246,6 +250,7 @@ class Simulation:
             setattr(cfg, name, k[name].data_ptr())
         cfg.status = dev.status.data_ptr()
         cfg.stream = dev.stream
+        cfg.use_graph = 1 if self.graph else 0
         k["cfg"] = cfg
         dev.reset_status()
         handle = lib.b2md_runner_create(ctypes.byref(cfg))
@@ -297,6 +302,7 @@ class Simulation:
         self.reorders += rep.reorders
         self.kernel_launches += rep.kernel_launches
         self.wasted_force_launches += rep.wasted_force_launches
+        self.graph_steps += rep.graph_steps
         if rep.reorders:
             dev.identity_order = False
         if rep.current != k["current"]:

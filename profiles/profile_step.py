@@ -25,6 +25,7 @@ ap.add_argument("--melt", type=int, default=0, help="untimed steps before (to le
 ap.add_argument("--reorder", default="hilbert")
 ap.add_argument("--density", type=float, default=0.75)
 ap.add_argument("--reorder-every", type=int, default=1)
+ap.add_argument("--graph", type=int, default=1)
 args = ap.parse_args()
 
 st, box = b2.init_lattice_any(args.n, args.density)
@@ -32,7 +33,7 @@ b2.init_velocities(st, 1.2, 42)
 sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001, force_mode=b2.TRUNCATED,
                     skin=0.3, sample_interval=100,
                     reorder=None if args.reorder == "none" else args.reorder,
-                    reorder_every=args.reorder_every)
+                    reorder_every=args.reorder_every, graph=bool(args.graph))
 if args.melt:
     sim.run(args.melt)
 torch.cuda.synchronize()
@@ -45,5 +46,5 @@ ms = start.elapsed_time(stop)
 print(f"n={args.n} steps={args.steps} ms/step={ms / args.steps:.4f} "
       f"particle-steps/s={args.n * args.steps / ms * 1e3:.3e} rebuilds={sim.rebuild_count} "
       f"launches={sim.kernel_launches} wasted={sim.wasted_force_launches} stride={sim.stride} "
-      f"boundary={getattr(sim, '_n_boundary', None)}")
+      f"boundary={getattr(sim, '_n_boundary', None)} graph_steps={sim.graph_steps}")
 sim.close()
