@@ -312,8 +312,9 @@ typedef struct b2md_runner_config {
     void *sort_scratch;          /* b2md_sort_scratch_bytes(n) */
     b2md_status *status;         /* device */
     void *stream;                /* the caller's stream; the runner orders its own against it */
-    int32_t use_graph;           /* 1: middle steps run as one CUDA graph each (conditional
-                                    rebuild node), no per-step host round trip */
+    int32_t use_graph;           /* k >= 1: middle steps run as captured CUDA graphs of k MD
+                                    steps each (conditional rebuild node per step), no
+                                    per-step host round trip; 0: host-driven steps */
     int32_t reserved0;
 } b2md_runner_config;
 

@@ -45,11 +45,12 @@ struct b2md_runner {
     cudaEvent_t ev_in;        // ordering against the caller's stream
     cudaStream_t stream;      // the runner's own (capturable) stream
     int64_t launches;
-    // step graph
-    cudaGraph_t graph;
-    cudaGraphExec_t graph_exec;
-    int64_t graph_launch_kernels;   // kernels in the always-executed part of the graph
-    int64_t graph_rebuild_kernels;  // kernels inside the conditional body
+    // step graphs: [0] = one MD step, [1] = steps_per_graph MD steps
+    cudaGraph_t graph[2];
+    cudaGraphExec_t graph_exec[2];
+    int steps_per_graph;
+    int64_t graph_launch_kernels;   // kernels per step in the always-executed part
+    int64_t graph_rebuild_kernels;  // kernels inside one conditional body
 };
 
 namespace {
@@ -200,74 +201,86 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
 }
 
 void destroy_graph(b2md_runner *r) {
-    if (r->graph_exec) cudaGraphExecDestroy(r->graph_exec);
-    if (r->graph) cudaGraphDestroy(r->graph);
-    r->graph_exec = nullptr;
-    r->graph = nullptr;
+    for (int g = 0; g < 2; ++g) {
+        if (r->graph_exec[g]) cudaGraphExecDestroy(r->graph_exec[g]);
+        if (r->graph[g]) cudaGraphDestroy(r->graph[g]);
+        r->graph_exec[g] = nullptr;
+        r->graph[g] = nullptr;
+    }
 }
 
-// Capture one MD step (fused integrate, conditional rebuild, no-thermo force).
-int build_graph(b2md_runner *r) {
+// Capture `n_steps` MD steps (fused integrate, conditional rebuild, no-thermo
+// force) into graph slot `slot`.  Every step gets its own conditional handle and
+// its own copy of the rebuild body.
+int build_graph(b2md_runner *r, int slot, int n_steps) {
     const b2md_runner_config &c = r->cfg;
-    destroy_graph(r);
     cudaStream_t s = r->stream;
     int rc;
-    if ((rc = check_cuda(cudaGraphCreate(&r->graph, 0), "cudaGraphCreate"))) return rc;
-    cudaGraphConditionalHandle handle;
-    if ((rc = check_cuda(cudaGraphConditionalHandleCreate(&handle, r->graph, 0,
-                                                          cudaGraphCondAssignDefault),
-                         "cudaGraphConditionalHandleCreate"))) return rc;
+    if ((rc = check_cuda(cudaGraphCreate(&r->graph[slot], 0), "cudaGraphCreate"))) return rc;
+    cudaGraph_t graph = r->graph[slot];
+    std::vector<cudaGraphNodeParams> params(n_steps);
     int64_t main_kernels = 0, body_kernels = 0;
-    if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, r->graph, nullptr, nullptr, 0,
+    if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0,
                                                        cudaStreamCaptureModeRelaxed),
                          "begin capture"))) return rc;
     Set a = live(r);
-    rc = b2md_vv_integrate_gated(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
-                                 c.ref_pos, r->half_skin2, c.status, 2, s);
-    k_graph_gate<<<1, 1, 0, s>>>(handle, c.status);
-    main_kernels += 2;
-    // splice the conditional node in after what has been captured so far
-    cudaStreamCaptureStatus cap_status;
-    cudaGraph_t cap_graph = nullptr;
-    const cudaGraphNode_t *deps = nullptr;
-    size_t n_deps = 0;
-    cudaGraphNode_t cond_node = nullptr;
-    cudaGraphNodeParams params = {};
-    if (!rc) rc = check_cuda(cudaStreamGetCaptureInfo(s, &cap_status, nullptr, &cap_graph, &deps,
-                                                      &n_deps), "capture info");
-    if (!rc) {
-        params.type = cudaGraphNodeTypeConditional;
-        params.conditional.handle = handle;
-        params.conditional.type = cudaGraphCondTypeIf;
-        params.conditional.size = 1;
-        rc = check_cuda(cudaGraphAddNode(&cond_node, r->graph, deps, n_deps, &params),
+    for (int k = 0; k < n_steps && !rc; ++k) {
+        cudaGraphConditionalHandle handle;
+        rc = check_cuda(cudaGraphConditionalHandleCreate(&handle, graph, 0,
+                                                         cudaGraphCondAssignDefault),
+                        "cudaGraphConditionalHandleCreate");
+        if (rc) break;
+        rc = b2md_vv_integrate_gated(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box,
+                                     c.dt, c.ref_pos, r->half_skin2, c.status, 2, s);
+        if (rc) break;
+        k_graph_gate<<<1, 1, 0, s>>>(handle, c.status);
+        // splice the conditional node in after what has been captured so far
+        cudaStreamCaptureStatus cap_status;
+        cudaGraph_t cap_graph = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t n_deps = 0;
+        cudaGraphNode_t cond_node = nullptr;
+        rc = check_cuda(cudaStreamGetCaptureInfo(s, &cap_status, nullptr, &cap_graph, &deps,
+                                                 &n_deps), "capture info");
+        if (rc) break;
+        params[k] = cudaGraphNodeParams();
+        params[k].type = cudaGraphNodeTypeConditional;
+        params[k].conditional.handle = handle;
+        params[k].conditional.type = cudaGraphCondTypeIf;
+        params[k].conditional.size = 1;
+        rc = check_cuda(cudaGraphAddNode(&cond_node, graph, deps, n_deps, &params[k]),
                         "add conditional node");
-    }
-    if (!rc) rc = check_cuda(cudaStreamUpdateCaptureDependencies(
-                                 s, &cond_node, 1, cudaStreamSetCaptureDependencies),
-                             "update capture dependencies");
-    if (!rc) {
+        if (rc) break;
+        rc = check_cuda(cudaStreamUpdateCaptureDependencies(s, &cond_node, 1,
+                                                            cudaStreamSetCaptureDependencies),
+                        "update capture dependencies");
+        if (rc) break;
         rc = launch_force(r, false, true);
         r->launches -= 1;    // only captured, not launched
+        if (rc) break;
+        k_graph_step_done<<<1, 1, 0, s>>>(c.status);
     }
-    if (!rc) { k_graph_step_done<<<1, 1, 0, s>>>(c.status); main_kernels += 2; }
+    main_kernels = 4;
     cudaGraph_t ended = nullptr;
     int rc_end = check_cuda(cudaStreamEndCapture(s, &ended), "end capture");
     if (rc) return rc;
     if (rc_end) return rc_end;
 
-    // body of the IF node: the whole rebuild, captured on the same stream
-    cudaGraph_t body = params.conditional.phGraph_out[0];
-    if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
-                                                       cudaStreamCaptureModeRelaxed),
-                         "begin body capture"))) return rc;
-    rc = enqueue_rebuild(r, c.reorder_mode != 0, true, &body_kernels);
-    if (!rc) { k_graph_after_build<<<1, 1, 0, s>>>(c.status); body_kernels += 1; }
-    rc_end = check_cuda(cudaStreamEndCapture(s, &ended), "end body capture");
-    if (rc) return rc;
-    if (rc_end) return rc_end;
-    if ((rc = check_cuda(cudaGraphInstantiate(&r->graph_exec, r->graph, 0), "graph instantiate")))
-        return rc;
+    // bodies of the IF nodes: the whole rebuild, captured on the same stream
+    for (int k = 0; k < n_steps; ++k) {
+        cudaGraph_t body = params[k].conditional.phGraph_out[0];
+        body_kernels = 0;
+        if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                                           cudaStreamCaptureModeRelaxed),
+                             "begin body capture"))) return rc;
+        rc = enqueue_rebuild(r, c.reorder_mode != 0, true, &body_kernels);
+        if (!rc) { k_graph_after_build<<<1, 1, 0, s>>>(c.status); body_kernels += 1; }
+        rc_end = check_cuda(cudaStreamEndCapture(s, &ended), "end body capture");
+        if (rc) return rc;
+        if (rc_end) return rc_end;
+    }
+    if ((rc = check_cuda(cudaGraphInstantiate(&r->graph_exec[slot], graph, 0),
+                         "graph instantiate"))) return rc;
     r->graph_launch_kernels = main_kernels;
     r->graph_rebuild_kernels = body_kernels;
     return 0;
@@ -344,10 +357,17 @@ int graph_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_batch, int64_t b
     cudaStream_t s = r->stream;
     int rc;
     *stop = 0;
-    if (!r->graph_exec && (rc = build_graph(r))) return rc;
+    if (!r->graph_exec[0] && (rc = build_graph(r, 0, 1))) return rc;
+    if (r->steps_per_graph > 1 && !r->graph_exec[1] &&
+        (rc = build_graph(r, 1, r->steps_per_graph))) return rc;
     k_graph_batch_reset<<<1, 1, 0, s>>>(c.status);
-    for (int64_t k = 0; k < n_batch; ++k)
-        if ((rc = check_cuda(cudaGraphLaunch(r->graph_exec, s), "cudaGraphLaunch"))) return rc;
+    int64_t left = n_batch;
+    while (left > 0) {
+        const bool big = r->steps_per_graph > 1 && left >= r->steps_per_graph;
+        if ((rc = check_cuda(cudaGraphLaunch(r->graph_exec[big ? 1 : 0], s), "cudaGraphLaunch")))
+            return rc;
+        left -= big ? r->steps_per_graph : 1;
+    }
     if ((rc = read_status(r))) return rc;
     const b2md_status &st = *r->h_status;
     rep->steps_done += st.graph_steps;
@@ -412,8 +432,9 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->mid_step = false;
     r->rebuilds_total = 0;
     r->launches = 0;
-    r->graph = nullptr;
-    r->graph_exec = nullptr;
+    r->graph[0] = r->graph[1] = nullptr;
+    r->graph_exec[0] = r->graph_exec[1] = nullptr;
+    r->steps_per_graph = cfg->use_graph > 1 ? cfg->use_graph : 1;
     r->h_status = nullptr;
     r->ev = r->ev_in = nullptr;
     r->stream = nullptr;

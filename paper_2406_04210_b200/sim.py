@@ -60,7 +60,7 @@ class Simulation:
                  sample_interval: int = 100, deterministic: bool = True,
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
-                 stride_policy: str = "fit", graph: bool = True):
+                 stride_policy: str = "fit", graph: int | bool = True):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -87,7 +87,7 @@ class Simulation:
         self.reorder = reorder if force_mode == TRUNCATED else None
         self.reorder_every = max(int(reorder_every), 1)
         self.stride_policy = stride_policy
-        self.graph = bool(graph)
+        self.graph = int(graph)          # MD steps per captured CUDA graph (0 = host-driven)
         self.graph_steps = 0
         self.native = (force_mode == TRUNCATED) if native is None else bool(native)
         if self.native and force_mode != TRUNCATED:
@@ -250,7 +250,7 @@ class Simulation:
             setattr(cfg, name, k[name].data_ptr())
         cfg.status = dev.status.data_ptr()
         cfg.stream = dev.stream
-        cfg.use_graph = 1 if self.graph else 0
+        cfg.use_graph = self.graph
         k["cfg"] = cfg
         dev.reset_status()
         handle = lib.b2md_runner_create(ctypes.byref(cfg))

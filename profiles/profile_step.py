@@ -33,7 +33,7 @@ b2.init_velocities(st, 1.2, 42)
 sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001, force_mode=b2.TRUNCATED,
                     skin=0.3, sample_interval=100,
                     reorder=None if args.reorder == "none" else args.reorder,
-                    reorder_every=args.reorder_every, graph=bool(args.graph))
+                    reorder_every=args.reorder_every, graph=args.graph)
 if args.melt:
     sim.run(args.melt)
 torch.cuda.synchronize()
