@@ -218,7 +218,7 @@ int build_graph(b2md_runner *r, int slot, int n_steps) {
     int rc;
     if ((rc = check_cuda(cudaGraphCreate(&r->graph[slot], 0), "cudaGraphCreate"))) return rc;
     cudaGraph_t graph = r->graph[slot];
-    std::vector<cudaGraphNodeParams> params(n_steps);
+    std::vector<cudaGraph_t> bodies(n_steps, nullptr);
     int64_t main_kernels = 0, body_kernels = 0;
     if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0,
                                                        cudaStreamCaptureModeRelaxed),
@@ -243,14 +243,15 @@ int build_graph(b2md_runner *r, int slot, int n_steps) {
         rc = check_cuda(cudaStreamGetCaptureInfo(s, &cap_status, nullptr, &cap_graph, &deps,
                                                  &n_deps), "capture info");
         if (rc) break;
-        params[k] = cudaGraphNodeParams();
-        params[k].type = cudaGraphNodeTypeConditional;
-        params[k].conditional.handle = handle;
-        params[k].conditional.type = cudaGraphCondTypeIf;
-        params[k].conditional.size = 1;
-        rc = check_cuda(cudaGraphAddNode(&cond_node, graph, deps, n_deps, &params[k]),
+        cudaGraphNodeParams params = {};
+        params.type = cudaGraphNodeTypeConditional;
+        params.conditional.handle = handle;
+        params.conditional.type = cudaGraphCondTypeIf;
+        params.conditional.size = 1;
+        rc = check_cuda(cudaGraphAddNode(&cond_node, graph, deps, n_deps, &params),
                         "add conditional node");
         if (rc) break;
+        bodies[k] = params.conditional.phGraph_out[0];
         rc = check_cuda(cudaStreamUpdateCaptureDependencies(s, &cond_node, 1,
                                                             cudaStreamSetCaptureDependencies),
                         "update capture dependencies");
@@ -268,7 +269,7 @@ int build_graph(b2md_runner *r, int slot, int n_steps) {
 
     // bodies of the IF nodes: the whole rebuild, captured on the same stream
     for (int k = 0; k < n_steps; ++k) {
-        cudaGraph_t body = params[k].conditional.phGraph_out[0];
+        cudaGraph_t body = bodies[k];
         body_kernels = 0;
         if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                                            cudaStreamCaptureModeRelaxed),
