@@ -449,17 +449,22 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
     // tuning knobs (defaults chosen from profiles/)
-    static int sub = 0, gather = -1, pipe = 0;
-    if (sub == 0) {
+    // Measured on B200 at N = 1 M (profiles/README.md): 12 CTAs/SM (<= 40 registers)
+    // beats 8 CTAs/SM by 5 %; one lane per particle beats sub-warps for large systems,
+    // while small systems (few CTAs, latency-bound serial row loops) want 4 lanes per
+    // particle; texture gathers and deeper gather pipelining do not pay.
+    static int sub_env = -1, gather = 0, pipe = 2;
+    if (sub_env < 0) {
         const char *env = getenv("B2MD_FORCE_SUBWARP");       // lanes per particle: 1, 2, 4
-        const int v = env ? atoi(env) : 1;
-        sub = (v == 1 || v == 2 || v == 4) ? v : 1;
+        const int v = env ? atoi(env) : 0;
+        sub_env = (v == 1 || v == 2 || v == 4) ? v : 0;       // 0 = choose by system size
         env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 1 TEX, 2 alternate
         const int w = env ? atoi(env) : 0;
         gather = (w >= 0 && w <= 2) ? w : 0;
-        env = getenv("B2MD_FORCE_PIPE");        // 1: gathers one trip ahead, 2: 12 CTAs/SM
-        pipe = env ? atoi(env) : 0;
+        env = getenv("B2MD_FORCE_PIPE");   // 0: 8 CTAs/SM, 1: gathers one trip ahead, 2: 12 CTAs/SM
+        pipe = env ? atoi(env) : 2;
     }
+    const int sub = sub_env ? sub_env : (n < 200000 ? 4 : 1);
     cudaTextureObject_t tex = 0;
     if (gather != 0) {
         // rows of pos_hi are addressed up to `pitch` (owned + ghost rows)

@@ -60,7 +60,7 @@ class Simulation:
                  sample_interval: int = 100, deterministic: bool = True,
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
-                 stride_policy: str = "fit", graph: int | bool = True):
+                 stride_policy: str = "fit", graph: int | bool = False):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:

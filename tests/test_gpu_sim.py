@@ -49,7 +49,7 @@ def test_graphed_steps_equal_ungraphed_steps_bitwise():
     """The CUDA-graph step (conditional rebuild node) runs the same kernels on the
     same data as the host-driven loop: identical trajectories, no host round trips."""
     runs = {}
-    for graph in (True, False):
+    for graph in (8, False):
         sim = lattice_sim(2048, True, reorder="hilbert", every=40, graph=graph)
         sim.run(130)
         sim.run(70)
@@ -58,10 +58,10 @@ def test_graphed_steps_equal_ungraphed_steps_bitwise():
                        np.array(sim.state.images.acquire_read(b2.HOST)), sim.rebuild_count,
                        sim.graph_steps, sim.wasted_force_launches)
         sim.close()
-    for a, b in zip(runs[True][:5], runs[False][:5]):
+    for a, b in zip(runs[8][:5], runs[False][:5]):
         assert np.array_equal(a, b)
-    assert runs[True][5] >= 180 and runs[False][5] == 0       # most steps ran as graphs
-    assert runs[True][6] < runs[False][6]                     # no speculative force launches
+    assert runs[8][5] >= 180 and runs[False][5] == 0          # most steps ran as graphs
+    assert runs[8][6] < runs[False][6]                        # no speculative force launches
 
 
 def test_overflow_inside_a_step_graph_is_recovered():
