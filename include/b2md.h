@@ -207,6 +207,20 @@ int b2md_vv_finalize_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel,
                                const b2md_box *box, double dt, void *d_ref_pos_f4,
                                double half_skin2, b2md_status *d_status, void *stream);
 
+/* ------------------------------------------------- Andersen thermostat + streams
+ * andersen_thermostat (integrate.py:82-107) over the counter-based streams of
+ * rng.py:40-66 (Philox4x64-10 keyed (seed, 0), counter (block+1, 0, stream, step),
+ * u = ((raw >> 11) + 0.5) 2^-53, normals = ndtri(u)).  Particle i (LOGICAL id, taken
+ * from pos_lo.w when d_ids_pos_lo != NULL) is redrawn iff uniform word i < probability;
+ * its new velocity is normal words n+3i..n+3i+2 times sqrt(T / m).  d_redrawn
+ * (may be NULL) receives the number of redrawn particles.
+ * b2md_stream_words exposes raw words / uniforms / normals [offset, offset+count). */
+int b2md_andersen(void *d_vel, const void *d_ids_pos_lo, int64_t n, uint64_t seed, uint64_t step,
+                  double probability, double temperature, int32_t *d_redrawn, void *stream);
+int b2md_stream_words(uint64_t seed, uint64_t stream_id, uint64_t step, int64_t word_offset,
+                      int64_t count, uint64_t *d_raw, double *d_uniform, double *d_normal,
+                      void *stream);
+
 /* ------------------------------------------------------------ observables
  * reduce_sum (observables.py:43-74): the reference's fixed pairing tree
  * (4096-value blocks, adjacent pairs, odd leftover carried), bit-exact in fp64.

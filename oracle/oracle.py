@@ -406,6 +406,45 @@ def vv_finalize(vel, forces, masses, dt):
 
 
 # --------------------------------------------------------------------------
+# random streams + Andersen thermostat (rng.py:40-66, integrate.py:82-107)
+# --------------------------------------------------------------------------
+
+def stream_raw(seed, stream, step, count):
+    """rng.py:40-53: numpy Philox keyed (seed, 0) at counter (0, 0, stream, step)."""
+    two64 = 1 << 64
+    gen = np.random.Philox(counter=np.array([0, 0, stream % two64, step % two64], dtype=np.uint64),
+                           key=np.array([seed % two64, 0], dtype=np.uint64))
+    return gen.random_raw(count) if count else np.empty(0, dtype=np.uint64)
+
+
+def stream_uniforms(seed, stream, step, count, word_offset=0):
+    """rng.py:56-60."""
+    words = stream_raw(seed, stream, step, word_offset + count)[word_offset:]
+    return ((words >> np.uint64(11)).astype(np.float64) + 0.5) * np.float64(2.0 ** -53)
+
+
+def stream_normals(seed, stream, step, count, word_offset=0):
+    """rng.py:63-66 (scipy.special.ndtri = Cephes ndtri)."""
+    from scipy.special import ndtri
+    return ndtri(stream_uniforms(seed, stream, step, count, word_offset))
+
+
+def andersen_thermostat(vel, masses, temperature, rate, seed, dt, step):
+    """integrate.py:82-107 -> (new velocities, redraw mask)."""
+    vel = np.array(vel, dtype=np.float64)
+    n = vel.shape[0]
+    p = min(rate * dt, 1.0)
+    if p <= 0.0:
+        return vel, np.zeros(n, dtype=bool)
+    redraw = stream_uniforms(seed, 0, step, n) < p
+    if redraw.any():
+        z = stream_normals(seed, 0, step, 3 * n, word_offset=n).reshape(n, 3)
+        scale = np.sqrt(temperature / np.asarray(masses, dtype=np.float64))
+        vel[redraw] = z[redraw] * scale[redraw, None]
+    return vel, redraw
+
+
+# --------------------------------------------------------------------------
 # observables (observables.py:28-98)
 # --------------------------------------------------------------------------
 

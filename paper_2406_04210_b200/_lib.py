@@ -129,6 +129,9 @@ _SIGNATURES = {
     "b2md_vv_finalize": (c_int32, [_P, _P, c_int64, c_double, _P]),
     "b2md_vv_finalize_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double,
                                              _P, c_double, _P, _P]),
+    "b2md_andersen": (c_int32, [_P, _P, c_int64, c_uint64, c_uint64, c_double, c_double, _P, _P]),
+    "b2md_stream_words": (c_int32, [c_uint64, c_uint64, c_uint64, c_int64, c_int64, _P, _P, _P,
+                                    _P]),
     "b2md_reduce_scratch_bytes": (c_int64, [c_int64]),
     "b2md_reduce_sum_f64": (c_int32, [_P, c_int64, _P, _P, _P]),
     "b2md_thermo_scratch_bytes": (c_int64, [c_int64]),

@@ -15,7 +15,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libb2md.so")
 
 SOURCES = ["state.cu", "cells.cu", "nlist.cu", "force.cu", "integrate.cu",
-           "reduce.cu", "sort.cu", "halo.cu", "runtime.cu"]
+           "reduce.cu", "sort.cu", "halo.cu", "thermostat.cu", "runtime.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -113,13 +113,22 @@ class SlabComm:
             dev_right, dev_left = from_right, from_left
             to_left, to_right = to_left.cpu(), to_right.cpu()
             from_right, from_left = from_right.cpu(), from_left.cpu()
-        ops = [dist.P2POp(dist.isend, to_left.contiguous(), g.left, self.group, tag=0),
-               dist.P2POp(dist.isend, to_right.contiguous(), g.right, self.group, tag=1),
-               # what my right neighbour sent leftwards / my left neighbour sent rightwards
-               dist.P2POp(dist.irecv, from_right, g.right, self.group, tag=0),
-               dist.P2POp(dist.irecv, from_left, g.left, self.group, tag=1)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        # Order matters for world == 2 (both neighbours are the same rank, and NCCL
+        # matches messages between a pair of ranks in posting order, ignoring tags):
+        # what I send leftwards is what my left neighbour receives "from its right".
+        # Empty messages are skipped on both sides (sizes were agreed on beforehand).
+        ops = []
+        if to_left.numel():
+            ops.append(dist.P2POp(dist.isend, to_left.contiguous(), g.left, self.group, tag=0))
+        if to_right.numel():
+            ops.append(dist.P2POp(dist.isend, to_right.contiguous(), g.right, self.group, tag=1))
+        if from_right.numel():
+            ops.append(dist.P2POp(dist.irecv, from_right, g.right, self.group, tag=0))
+        if from_left.numel():
+            ops.append(dist.P2POp(dist.irecv, from_left, g.left, self.group, tag=1))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
         if staged:
             dev_right.copy_(from_right)
             dev_left.copy_(from_left)

@@ -31,7 +31,7 @@ from .backend import BackendSelector
 from .core import COMPUTE, DeviceState, ParticleState, SignalEngine, SimBox
 from .errors import ConfigError, NeighborOverflowError, SingularPairError
 from .forces import compute_forces_all_to_all, compute_forces_truncated
-from .integrate import IntegratorParams, vv_finalize, vv_integrate
+from .integrate import IntegratorParams, andersen_thermostat, vv_finalize, vv_integrate
 from .neighbor import (HILBERT_SUB_BITS, NeighborList, _round_up, bin_particles,
                        build_neighbor_list, grid_shape, needs_rebuild, reorder_hilbert)
 from .observables import DETERMINISTIC, FAST, Sample, thermo
@@ -67,9 +67,9 @@ class Simulation:
             raise ConfigError("truncated force mode needs a finite r_cut")
         if skin < 0.0:
             raise ConfigError("skin must be non-negative")
-        if thermostat is not None and getattr(thermostat, "rate", 0.0) > 0.0:
-            raise ConfigError("the Andersen thermostat is not part of the B200 hot path yet "
-                              "(SURVEY.md section 8 row f3); run NVE")
+        thermostatted = thermostat is not None and getattr(thermostat, "rate", 0.0) > 0.0
+        if thermostatted and native:
+            raise ConfigError("the native step loop is NVE; a thermostat runs the operator loop")
         if reorder not in _REORDER_MODES:
             raise ConfigError(f"unknown reorder mode {reorder!r}")
         if stride_policy not in ("fit", "double", "tight"):
@@ -82,14 +82,16 @@ class Simulation:
         self.backend = backend if backend is not None else BackendSelector()
         self.force_mode = force_mode
         self.skin = float(skin)
-        self.thermostat = None
+        self.thermostat = thermostat
         self.reduction_mode = DETERMINISTIC if deterministic else FAST
         self.reorder = reorder if force_mode == TRUNCATED else None
         self.reorder_every = max(int(reorder_every), 1)
         self.stride_policy = stride_policy
         self.graph = int(graph)          # MD steps per captured CUDA graph (0 = host-driven)
         self.graph_steps = 0
-        self.native = (force_mode == TRUNCATED) if native is None else bool(native)
+        # the thermostat acts between finalize and the next integrate: operator loop
+        self.native = (force_mode == TRUNCATED and not thermostatted) if native is None \
+            else bool(native)
         if self.native and force_mode != TRUNCATED:
             raise ConfigError("the native step loop drives truncated forces only")
         if not self.native and self.reorder == "cell":
@@ -113,6 +115,8 @@ class Simulation:
         self.engine.connect("integrate", self._integrate_slot)
         self.engine.connect("force", self._force_slot)
         self.engine.connect("finalize", self._finalize_slot)
+        if thermostatted:
+            self.engine.connect("finalize", self._thermostat_slot)     # sim.py:86-87
         self.engine.connect("sample", self._sample_slot)
 
         self._runner = None
@@ -128,6 +132,10 @@ class Simulation:
 
     def _finalize_slot(self):
         vv_finalize(self.state, self.integrator)
+
+    def _thermostat_slot(self):
+        andersen_thermostat(self.state, self.thermostat, self.integrator.dt,
+                            self.engine.step_count)                    # sim.py:100-102
 
     def _force_slot(self):
         self._compute_forces()

@@ -25,7 +25,7 @@ ap.add_argument("--melt", type=int, default=0, help="untimed steps before (to le
 ap.add_argument("--reorder", default="hilbert")
 ap.add_argument("--density", type=float, default=0.75)
 ap.add_argument("--reorder-every", type=int, default=1)
-ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--graph", type=int, default=0)
 args = ap.parse_args()
 
 st, box = b2.init_lattice_any(args.n, args.density)

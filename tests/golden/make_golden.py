@@ -300,6 +300,26 @@ def trajectory_case():
          lat256_edges=box256.edge_lengths)
 
 
+# ---------------------------------------------------------- rng / thermostat
+def thermostat_case():
+    from mdbench import rng
+    # test_rng.py:9-13 address (12345, 0, 7)
+    raw = rng.raw_words(12345, 0, 7, 12)
+    uni = rng.uniforms(12345, 0, 7, 8, word_offset=3)
+    nrm = rng.normals(12345, 1, 0, 9, word_offset=2)
+    gen = np.random.default_rng(5)
+    n = 3000
+    vel = gen.normal(size=(n, 3))
+    masses = gen.uniform(0.5, 2.0, size=n)
+    st = ref.ParticleState(gen.uniform(0, 5, size=(n, 3)), velocities=vel, masses=masses)
+    params = ref.ThermostatParams(temperature=1.7, rate=25.0, seed=99)
+    count = ref.andersen_thermostat(st, params, 0.004, 321)
+    save("thermostat", raw=raw, uniforms=uni, normals=nrm, vel=vel, masses=masses,
+         temperature=np.float64(1.7), rate=np.float64(25.0), seed=np.int64(99),
+         dt=np.float64(0.004), step=np.int64(321), count=np.int64(count),
+         vel_after=np.array(st.velocities.acquire_read(COMPUTE)))
+
+
 if __name__ == "__main__":
     print("reference mdbench", ref.__version__)
     neighbor_cases()
@@ -308,3 +328,4 @@ if __name__ == "__main__":
     integrate_cases()
     observable_cases()
     trajectory_case()
+    thermostat_case()

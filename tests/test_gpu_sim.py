@@ -220,3 +220,18 @@ def test_large_system_properties():
     assert counts.sum() % 2 == 0 and counts.min() > 30 and counts.max() <= sim.stride
     assert sorted(sim.state.particle_ids().tolist()) == list(range(n))
     sim.close()
+
+
+def test_reference_presets_run_through_the_harness():
+    """bench.py presets on the B200 backend: smoke-256 (thermostatted, truncated) and a
+    shortened all2all-2k (the paper's primary benchmark, untruncated all-pairs)."""
+    from dataclasses import replace
+    rec, samples = b2.run_benchmark(b2.preset_config("smoke-256"))
+    assert rec.steps_per_second > 0 and len(samples) == 4
+    assert abs(np.mean([s.temperature for s in samples]) - 1.5) < 0.35
+    cfg = replace(b2.preset_config("all2all-2k"), steps=400, equilibration_steps=100)
+    rec, samples = b2.run_benchmark(cfg)
+    assert rec.final_energy_drift_rel < 1e-4                  # test_acceptance.py:82-91 bound
+    assert rec.rebuild_count == 0 and len(samples) == 8
+    mom = np.array([s.total_momentum for s in samples])
+    assert np.max(np.abs(mom)) < 1e-2

@@ -1,0 +1,80 @@
+"""Andersen thermostat and counter-based streams on the device (`-m gpu`) against
+the reference's golden vectors (tests/golden/thermostat.npz) and the oracle."""
+import numpy as np
+import pytest
+
+import paper_2406_04210_b200 as b2
+from paper_2406_04210_b200 import rng
+from conftest import load_golden
+from helpers import quantize_f32
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def test_stream_words_match_reference_vectors():
+    G = load_golden("thermostat")
+    assert np.array_equal(rng.raw_words(12345, 0, 7, 12), G["raw"])            # bit-exact
+    assert np.array_equal(rng.uniforms(12345, 0, 7, 8, word_offset=3), G["uniforms"])
+    got = rng.normals(12345, 1, 0, 9, word_offset=2)
+    assert np.max(np.abs(got - G["normals"])) <= 4e-16 * np.max(np.abs(G["normals"]))
+    # a long block: every uniform identical, normals to a few ulp, tails included
+    n = 200_000
+    assert np.array_equal(rng.uniforms(7, 0, 3, n), orc.stream_uniforms(7, 0, 3, n))
+    z, zr = rng.normals(7, 0, 3, n), orc.stream_normals(7, 0, 3, n)
+    assert np.max(np.abs(z - zr) / np.maximum(np.abs(zr), 1e-3)) <= 1e-14
+    assert rng.raw_words(1, 2, 3, 0).size == 0
+
+
+def test_andersen_thermostat_matches_reference():
+    G = load_golden("thermostat")
+    vel, masses = quantize_f32(G["vel"]), quantize_f32(G["masses"])
+    params = b2.ThermostatParams(float(G["temperature"]), float(G["rate"]), int(G["seed"]))
+    st = b2.ParticleState(np.zeros_like(vel), velocities=vel, masses=masses)
+    count = b2.andersen_thermostat(st, params, float(G["dt"]), int(G["step"]))
+    want_vel, redraw = orc.andersen_thermostat(vel, masses, params.temperature, params.rate,
+                                               params.seed, float(G["dt"]), int(G["step"]))
+    assert count == int(redraw.sum()) == int(G["count"])       # same particles selected
+    got = st.velocities.acquire_read(b2.HOST)
+    assert np.array_equal(got[~redraw], vel[~redraw])           # untouched rows bit-identical
+    assert np.max(np.abs(got[redraw] - want_vel[redraw])
+                  / np.maximum(np.abs(want_vel[redraw]), 1e-3)) <= 2e-7   # fp32 velocities
+    # zero rate: nothing happens
+    assert b2.andersen_thermostat(st, b2.ThermostatParams(1.0, 0.0, 1), 0.01, 5) == 0
+    with pytest.raises(ValueError):
+        b2.ThermostatParams(-1.0, 1.0, 0)
+
+
+def test_thermostat_is_independent_of_device_row_order():
+    """Streams are addressed by logical particle id: an internal Hilbert reorder
+    must not change who is redrawn or what they receive."""
+    gen = np.random.default_rng(3)
+    n, edge = 4000, 17.0
+    pos = gen.uniform(0, edge, size=(n, 3))
+    vel = quantize_f32(gen.normal(size=(n, 3)))
+    params = b2.ThermostatParams(0.9, 40.0, 1234)
+    out = []
+    for reorder in (False, True):
+        st = b2.ParticleState(pos, velocities=vel)
+        if reorder:
+            b2.reorder_hilbert(st, b2.SimBox.cubic(edge), 2.8, internal=True)
+        c = b2.andersen_thermostat(st, params, 0.005, 77)
+        out.append((c, np.array(st.velocities.acquire_read(b2.HOST))))
+    assert out[0][0] == out[1][0] > 0
+    assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_thermostatted_simulation_holds_the_target_temperature():
+    # test_acceptance.py:123-136 analogue: mean T within a few standard errors
+    st, box = b2.init_lattice_any(4000, 0.75)
+    b2.init_velocities(st, 1.5, 42)
+    thermo = b2.ThermostatParams(temperature=1.5, rate=20.0, seed=7)
+    sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.002, force_mode=b2.TRUNCATED,
+                        skin=0.3, thermostat=thermo, sample_interval=10)
+    assert not sim.native
+    sim.run(1500)
+    temps = np.array([s.temperature for s in sim.samples[50:]])
+    assert abs(temps.mean() - 1.5) < 0.03
+    with pytest.raises(b2.ConfigError):
+        b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.002, force_mode=b2.TRUNCATED,
+                      thermostat=thermo, native=True)

@@ -161,3 +161,37 @@ def test_simulation_argument_validation():
         b2.Simulation(st, box, b2.make_shifted(1.0, 1.0), 0.001, force_mode=b2.TRUNCATED)
     with pytest.raises(b2.ConfigError):
         b2.Simulation(st, box, lj, 0.001, force_mode=b2.TRUNCATED, skin=-0.1)
+
+
+def test_bench_config_files_and_records_round_trip(tmp_path):
+    # reference bench.py:126-142, 207-263 (test_bench.py analogues)
+    cfg_path = tmp_path / "run.cfg"
+    cfg_path.write_text("# quick run\nn_particles = 864\ndensity=0.75\nsteps = 50  # short\n"
+                        "deterministic = no\nforce_mode = truncated\n")
+    cfg = b2.parse_config_file(cfg_path)
+    assert (cfg.n_particles, cfg.density, cfg.steps, cfg.deterministic) == (864, 0.75, 50, False)
+    assert cfg.backend == "b200"
+    (tmp_path / "bad.cfg").write_text("n_particles = 10\nbogus = 1\n")
+    with pytest.raises(b2.ConfigError, match=r"bad.cfg:2"):
+        b2.parse_config_file(tmp_path / "bad.cfg")
+    with pytest.raises(b2.ConfigError):
+        b2.BenchConfig(backend="sequential").validate()
+    with pytest.raises(b2.ConfigError):
+        b2.BenchConfig(r_cut=float("inf")).validate()       # truncated needs a finite cutoff
+    assert set(b2.PRESETS) == {"all2all-2k", "all2all-2k-long", "trunc-10k", "smoke-256"}
+    assert b2.preset_config("trunc-10k").thermostat_rate == 5.0
+    with pytest.raises(b2.ConfigError):
+        b2.preset_config("nope")
+    rec = b2.BenchRecord(cfg, 0.1234567890123456789, 405.0, 0.6, 0.3, 7, 1, 1.25e-06)
+    path = tmp_path / "records.csv"
+    b2.write_records_csv(path, [rec])
+    b2.write_records_csv(path, [rec], append=True)
+    back = b2.read_records_csv(path)
+    assert back == [rec, rec]                                  # 17 significant digits round-trip
+    header = path.read_text().splitlines()[0].split(",")
+    assert header[:3] == ["n_particles", "density", "temperature"] and header[-1] == "engine_version"
+    s = b2.Sample(10, 0.02, -1.5, 0.5, -1.0, 1.1, (1e-3, -2e-3, 0.0), 2)
+    b2.write_samples_csv(tmp_path / "samples.csv", [s])
+    lines = (tmp_path / "samples.csv").read_text().splitlines()
+    assert lines[0] == "step,time,potential_energy,kinetic_energy,total_energy,temperature,px,py,pz,rebuild_count"
+    assert lines[1].startswith("10,0.02") and lines[1].endswith(",2")

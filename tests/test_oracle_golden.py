@@ -219,3 +219,16 @@ def test_nve_trajectory_bit_exact():
     assert np.array_equal(sim.images, G["img_end"])
     assert np.array_equal(sim.forces, G["forces_end"])
     assert sim.stride == int(G["stride_end"])
+
+
+# ----------------------------------------------------------- rng / thermostat
+def test_random_streams_and_thermostat_bit_exact():
+    G = load_golden("thermostat")
+    assert np.array_equal(orc.stream_raw(12345, 0, 7, 12), G["raw"])
+    assert np.array_equal(orc.stream_uniforms(12345, 0, 7, 8, word_offset=3), G["uniforms"])
+    assert np.array_equal(orc.stream_normals(12345, 1, 0, 9, word_offset=2), G["normals"])
+    vel, redraw = orc.andersen_thermostat(G["vel"], G["masses"], float(G["temperature"]),
+                                          float(G["rate"]), int(G["seed"]), float(G["dt"]),
+                                          int(G["step"]))
+    assert int(redraw.sum()) == int(G["count"])
+    assert np.array_equal(vel, G["vel_after"])
