@@ -235,3 +235,21 @@ def test_reference_presets_run_through_the_harness():
     assert rec.rebuild_count == 0 and len(samples) == 8
     mom = np.array([s.total_momentum for s in samples])
     assert np.max(np.abs(mom)) < 1e-2
+
+
+def test_config2_energy_drift_matches_the_reference_bound():
+    """BASELINE config 2: N=65 536, rho=0.75, T0=1.2, rc=2.5, skin 0.3, dt=0.001,
+    10^4 NVE steps with Hilbert reordering.  The fp64 reference drifts 1.29e-6 end
+    to end (second-half max deviation 2.1e-7, 267 rebuilds).
+    Stated bound for the fp32 / double-single engine: 1e-5 end to end, 5e-6 over the
+    second half."""
+    sim = lattice_sim(65_536, True, every=100)
+    sim.run(10_000)
+    e = np.array([s.total_energy for s in sim.samples])
+    assert abs(e[-1] - e[0]) / abs(e[0]) <= 1e-5
+    half = len(e) // 2
+    assert np.max(np.abs(e[half:] - e[half])) / abs(e[0]) <= 5e-6
+    assert 230 <= sim.rebuild_count <= 310
+    assert 0.60 < sim.samples[-1].temperature < 0.68
+    assert np.max(np.abs(np.array([s.total_momentum for s in sim.samples]))) < 0.05
+    sim.close()
