@@ -153,7 +153,8 @@ __device__ __forceinline__ void gather4(float4 (&pj)[4], const int (&j)[4],
     for (int u = 0; u < 4; ++u) pj[u] = gather_pos<GATHER>(pos, tex, j[u], u);
 }
 
-template <int SUB, bool CAREFUL, bool TABLE, bool THERMO, bool CHECK>
+// AXES: bit a set = pairs of this warp may need an image shift along axis a.
+template <int SUB, int AXES, bool TABLE, bool THERMO, bool CHECK>
 __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, int k,
                                          const float4 (&pj)[4], const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
@@ -161,9 +162,9 @@ __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, 
     const BoxF &b = a.box;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const float dx = delta<CAREFUL>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-        const float dy = delta<CAREFUL>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-        const float dz = delta<CAREFUL>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        const float dx = delta<(AXES & 1) != 0>(pi.x, pj[u].x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<(AXES & 2) != 0>(pi.y, pj[u].y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<(AXES & 4) != 0>(pi.z, pj[u].z, b.L_hi[2], b.L_lo[2], b.invL[2]);
         const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
         const bool valid = CHECK ? (k + u * SUB) < cnt : true;
         if (TABLE) {
@@ -181,7 +182,7 @@ __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, 
 // PIPE = true additionally keeps the NEXT trip's four position gathers in flight
 // while the current trip is being computed (deeper memory-level parallelism at
 // the price of 16 more registers).
-template <int SUB, int GATHER, int PIPEK, bool CAREFUL, bool TABLE, bool THERMO>
+template <int SUB, int GATHER, int PIPEK, int AXES, bool TABLE, bool THERMO>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
@@ -207,10 +208,10 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
         if (PIPE) gather4<GATHER>(pb, jb, pos, tex);         // row 0 is always a valid index
         else gather4<GATHER>(pa, ja, pos, tex);
         if (base + kTrip <= kmin)
-            compute4<SUB, CAREFUL, TABLE, THERMO, false>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
+            compute4<SUB, AXES, TABLE, THERMO, false>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
                                                          s_tab_b, ti_row);
         else
-            compute4<SUB, CAREFUL, TABLE, THERMO, true>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
+            compute4<SUB, AXES, TABLE, THERMO, true>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
                                                         s_tab_b, ti_row);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -270,17 +271,23 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
     const int cnt = active ? counts[i] : 0;
     const int kmax = __reduce_max_sync(0xffffffffu, cnt);
     const int kmin = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff);
-    const bool careful = boundary ? (__any_sync(0xffffffffu, active && boundary[i] != 0)) : true;
+    // which axes can need an image shift for some pair of this warp (0 = interior warp)
+    const int axes = boundary ? __reduce_or_sync(0xffffffffu, active ? (int)boundary[i] : 0) : 7;
     const int32_t *col = nbr + (int64_t)sub * pitch + i;
     const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
-    if (careful)
-        row_loop<SUB, GATHER, PIPE, true, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos,
-                                                   tex, a, s_tab_a, s_tab_b, ti_row);
-    else
-        row_loop<SUB, GATHER, PIPE, false, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,
-                                                    pos, tex, a, s_tab_a, s_tab_b, ti_row);
+#define B2MD_ROW_LOOP(AXES)                                                                  \
+    row_loop<SUB, GATHER, PIPE, AXES, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,  \
+                                                     pos, tex, a, s_tab_a, s_tab_b, ti_row)
+    switch (axes) {                 // warp-uniform
+        case 0: B2MD_ROW_LOOP(0); break;      // interior: plain differences
+        case 1: B2MD_ROW_LOOP(1); break;      // one face family only
+        case 2: B2MD_ROW_LOOP(2); break;
+        case 4: B2MD_ROW_LOOP(4); break;
+        default: B2MD_ROW_LOOP(7); break;     // edges / corners / tiny boxes
+    }
+#undef B2MD_ROW_LOOP
 #pragma unroll
     for (int o = SUB >> 1; o > 0; o >>= 1) {
         acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
@@ -458,11 +465,10 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         const char *env = getenv("B2MD_FORCE_SUBWARP");       // lanes per particle: 1, 2, 4
         const int v = env ? atoi(env) : 0;
         sub_env = (v == 1 || v == 2 || v == 4) ? v : 0;       // 0 = choose by system size
-        env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 1 TEX, 2 alternate
-        const int w = env ? atoi(env) : 0;
-        gather = (w >= 0 && w <= 2) ? w : 0;
-        env = getenv("B2MD_FORCE_PIPE");   // 0: 8 CTAs/SM, 1: gathers one trip ahead, 2: 12 CTAs/SM
-        pipe = env ? atoi(env) : 2;
+        env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 2 alternate LDG / TEX
+        gather = (env && atoi(env) == 2) ? 2 : 0;
+        env = getenv("B2MD_FORCE_PIPE");                      // 0: 8 CTAs/SM, 2: 12 CTAs/SM
+        pipe = (env && atoi(env) == 0) ? 0 : 2;
     }
     const int sub = sub_env ? sub_env : (n < 200000 ? 4 : 1);
     cudaTextureObject_t tex = 0;
@@ -487,11 +493,9 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         }                                                                                    \
     } while (0)
     if (sub == 1) {
-        if (pipe == 1) B2MD_DISPATCH_TT(1, 0, 1);
-        else if (pipe == 2) B2MD_DISPATCH_TT(1, 0, 2);
-        else if (gather == 0) B2MD_DISPATCH_TT(1, 0, 0);
-        else if (gather == 1) B2MD_DISPATCH_TT(1, 1, 0);
-        else B2MD_DISPATCH_TT(1, 2, 0);
+        if (gather == 2) B2MD_DISPATCH_TT(1, 2, 2);
+        else if (pipe == 0) B2MD_DISPATCH_TT(1, 0, 0);
+        else B2MD_DISPATCH_TT(1, 0, 2);
     } else if (sub == 2) {
         B2MD_DISPATCH_TT(2, 0, 0);
     } else {

@@ -89,13 +89,16 @@ __device__ __forceinline__ void finish_row(int32_t *__restrict__ nbr, int64_t pi
     }
 }
 
+// Bit a is set when the particle is within `margin` of a periodic face on axis a:
+// only then can one of its listed pairs need an image shift along that axis
+// during the list's lifetime.
 __device__ __forceinline__ uint8_t boundary_flag(const float4 h, const ListGeom &g) {
-    bool near_face = false;
     const float p[3] = {h.x, h.y, h.z};
+    int bits = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-        near_face |= (p[a] < g.margin[a]) | (p[a] > g.Lhi[a] - g.margin[a]);
-    return near_face ? 1 : 0;
+        if ((p[a] < g.margin[a]) | (p[a] > g.Lhi[a] - g.margin[a])) bits |= 1 << a;
+    return (uint8_t)bits;
 }
 
 template <bool PREFILTER>
@@ -421,14 +424,14 @@ k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_l
             ++found;
         }
     }
-    if (boundary && active) boundary[i] = 1;  // tiny boxes: every pair may cross a face
+    if (boundary && active) boundary[i] = 7;  // tiny boxes: every pair may cross any face
     finish_row(nbr, pitch, i, active, found, stride, counts, status);
 }
 
 __global__ void k_count_boundary(const uint8_t *__restrict__ boundary, int64_t n,
                                  b2md_status *status) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int v = (i < n) ? boundary[i] : 0;
+    int v = (i < n) ? (boundary[i] != 0) : 0;
     v = warp_sum_i(v);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&status->n_boundary, v);
 }

@@ -45,6 +45,7 @@ struct b2md_runner {
     cudaEvent_t ev_in;        // ordering against the caller's stream
     cudaStream_t stream;      // the runner's own (capturable) stream
     int64_t launches;
+    double last_disp2;        // max squared displacement seen one step ago (fp32 check)
     // step graphs: [0] = one MD step, [1] = steps_per_graph MD steps
     cudaGraph_t graph[2];
     cudaGraphExec_t graph_exec[2];
@@ -320,9 +321,14 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
                                          cudaMemcpyDeviceToHost, s), "flag read-back"))) return rc;
     if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
-    if ((rc = launch_force(r, thermo))) return rc;           // speculative
+    // Launch the force kernel before the flag is known -- unless the displacement
+    // was already close to the threshold one step ago, in which case a rebuild is
+    // likely and waiting a few microseconds beats discarding a force evaluation.
+    const bool speculate = r->last_disp2 < 0.85 * r->half_skin2;
+    if (speculate && (rc = launch_force(r, thermo))) return rc;
     if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
     rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
+    r->last_disp2 = rep->max_disp2;
     if (r->h_status->singular != ~0ull) {
         // a force evaluation of an earlier step met a coincident pair
         // (forces.py:113-116); stop after draining the stream
@@ -336,8 +342,9 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
         return 0;
     }
     if (r->h_status->rebuild_flag) {
-        rep->wasted_force_launches += 1;
+        if (speculate) rep->wasted_force_launches += 1;
         if ((rc = rebuild(r, rep))) return rc;
+        r->last_disp2 = 0.0;
         if (!r->list_valid) {
             r->mid_step = true;
             rep->reason = B2MD_RUN_OVERFLOW;
@@ -345,6 +352,8 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
             *stop = 1;
             return 0;
         }
+        if ((rc = launch_force(r, thermo))) return rc;
+    } else if (!speculate) {
         if ((rc = launch_force(r, thermo))) return rc;
     }
     r->pending_kick = true;
@@ -433,6 +442,7 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->mid_step = false;
     r->rebuilds_total = 0;
     r->launches = 0;
+    r->last_disp2 = 0.0;
     r->graph[0] = r->graph[1] = nullptr;
     r->graph_exec[0] = r->graph_exec[1] = nullptr;
     r->steps_per_graph = cfg->use_graph > 1 ? cfg->use_graph : 1;
