@@ -245,12 +245,39 @@ def run_gpu_arm(args):
     tab_ptr = tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     rows = k["nbr"].shape[0]
 
-    def launch_force():
+    def launch_force_rows():
         _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), n, box.c_box(), k["nbr"].data_ptr(),
                   k["counts"].data_ptr(), k["pitch"], rows, k["boundary"].data_ptr(), tab_ptr, 1,
                   _lib.FORCE_SKIP_THERMO, dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
 
-    force_ms = time_kernel(launch_force, 50, torch, stream)
+    def launch_force_pairs():
+        cfg = k["cfg"]
+        _lib.call("b2md_force_lj_pairs", dev.pos_hi.data_ptr(), n, box.c_box(),
+                  k["pair_nbr"].data_ptr(), k["pair_counts"].data_ptr(), cfg.pair_pitch,
+                  k["nbr"].data_ptr(), k["counts"].data_ptr(), k["pitch"],
+                  k["boundary"].data_ptr(), tab_ptr, 1, _lib.FORCE_SKIP_THERMO,
+                  dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
+
+    # the kernel the step loop launches (pair rows for systems this large)
+    force_kernel = "k_force_lj_pair" if sim.pair_rows else "k_force_lj"
+    force_ms = time_kernel(launch_force_pairs if sim.pair_rows else launch_force_rows, 50, torch,
+                           stream)
+    pair_entries = float(k["pair_counts"].float().sum().item()) / n if sim.pair_rows else None
+    extra_kernels = {}
+    if sim.pair_rows:
+        # for comparison: the thread-per-particle kernel on the same list, and the merge
+        rows_ms = time_kernel(launch_force_rows, 20, torch, stream)
+        extra_kernels["k_force_lj (thread per particle, same list)"] = {
+            "launch_ms": rows_ms,
+            "achieved": n * (32.0 + 4.0 * cbar) / (rows_ms * 1e-3) / 1e9}
+        cfg = k["cfg"]
+
+        def launch_merge():
+            _lib.call("b2md_pair_rows", k["nbr"].data_ptr(), k["counts"].data_ptr(), k["pitch"],
+                      rows, n, k["pair_nbr"].data_ptr(), k["pair_counts"].data_ptr(),
+                      cfg.pair_pitch, cfg.pair_rows, dev.stream)
+        extra_kernels["k_pair_rows (once per rebuild)"] = {
+            "launch_ms": time_kernel(launch_merge, 10, torch, stream)}
     force_bytes = n * (32.0 + 4.0 * cbar)          # pos 16 + idx 4*c + force 16 (no-thermo variant)
     peak, peak_src = measured_peak()
     achieved = force_bytes / (force_ms * 1e-3) / 1e9
@@ -321,7 +348,8 @@ def run_gpu_arm(args):
         "config": {"workload": WORKLOAD, "particles": n, "l2": "inputs larger than L2: the "
                    f"neighbour list streamed every step is {rows * k['pitch'] * 4 / 1e6:.0f} MB "
                    "(L2 126 MB), state 80 MB",
-                   "mean_listed_neighbours": cbar, "rebuilds_in_timed_region": rebuilds,
+                   "mean_listed_neighbours": cbar, "pair_row_entries_per_particle": pair_entries,
+                   "rebuilds_in_timed_region": rebuilds,
                    "reorder": "hilbert", "sample_interval": 100,
                    "step_algorithmic_bytes": step_bytes,
                    "step_hbm_fraction": step_bytes * value / n / 1e9 / peak,
@@ -329,11 +357,11 @@ def run_gpu_arm(args):
                    "final_temperature": last.temperature},
         "clocks": clock_info,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_force_lj", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": force_kernel, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": force_bytes,
                      "launch_ms": force_ms,
-                     "other_kernels": {"k_integrate<2>": {
+                     "other_kernels": {**extra_kernels, "k_integrate<2>": {
                          "achieved": integ_bytes / (integ_ms * 1e-3) / 1e9, "launch_ms": integ_ms,
                          "algorithmic_bytes_per_launch": integ_bytes,
                          "frac": integ_bytes / (integ_ms * 1e-3) / 1e9 / peak}}},

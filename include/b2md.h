@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 100
+#define B2MD_VERSION 101
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -175,6 +175,33 @@ int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                   int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
                   int32_t flags, void *d_force_f4, float *d_virial, b2md_status *d_status,
                   void *stream);
+
+/* Pair rows -- the layout the production force kernel reads.  Thread t of
+ * b2md_force_lj_pairs owns particles 2t and 2t+1 (neighbours in memory and, after
+ * the Hilbert / cell reorder, in space) and walks the ascending merge of their two
+ * rows of the list above: every distinct j once, entry = j << 2 | (row of 2t lists
+ * j) | (row of 2t+1 lists j) << 1.  Entries 4q..4q+3 of pair t form the int4 at
+ * d_pair_nbr[(q * pair_pitch + t) * 4]; rows are padded with flag-less entries to
+ * the longest row of their warp.  pair_pitch: multiple of 32 >= ceil(n_rows/2);
+ * pair_rows (entries per pair row): multiple of 4, >= 2 * stride, so a merge can
+ * never overflow.  Derived data: the per-particle list stays the source of truth
+ * (and what build_neighbor_list returns, neighbor.py:185-240). */
+int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, int32_t stride,
+                   int64_t n_rows, int32_t *d_pair_nbr, int32_t *d_pair_counts,
+                   int64_t pair_pitch, int32_t pair_rows, void *stream);
+
+/* compute_forces_truncated over pair rows (forces.py:141-159; kernel 72-110): r_j
+ * is gathered once per pair-row entry and evaluated against both particles of the
+ * pair; an entry only one of them lists contributes exact zeros to the other, so
+ * every per-particle result is bit-identical to b2md_force_lj's.  d_nbr / d_counts
+ * / pitch (the per-particle list) are only read to name a coincident pair.  Other
+ * arguments as b2md_force_lj. */
+int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                        const int32_t *d_pair_nbr, const int32_t *d_pair_counts,
+                        int64_t pair_pitch, const int32_t *d_nbr, const int32_t *d_counts,
+                        int64_t pitch, const uint8_t *d_boundary, const double *table,
+                        int32_t ntypes, int32_t flags, void *d_force_f4, float *d_virial,
+                        b2md_status *d_status, void *stream);
 
 /* compute_forces_all_to_all (forces.py:129-138; kernel 29-69): shared-memory
  * tiled all-pairs scan, same outputs. */
@@ -329,7 +356,11 @@ typedef struct b2md_runner_config {
     int32_t use_graph;           /* k >= 1: middle steps run as captured CUDA graphs of k MD
                                     steps each (conditional rebuild node per step), no
                                     per-step host round trip; 0: host-driven steps */
-    int32_t reserved0;
+    int32_t pair_rows;           /* entries per pair row (multiple of 4, >= 2*round_up(stride,16));
+                                    0 = one thread per particle (b2md_force_lj) */
+    int32_t *pair_nbr;           /* pair_rows * pair_pitch (b2md_pair_rows layout) */
+    int32_t *pair_counts;        /* pair_pitch */
+    int64_t pair_pitch;          /* multiple of 32 >= ceil(n/2) */
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };
@@ -356,6 +387,8 @@ b2md_runner *b2md_runner_create(const b2md_runner_config *cfg);
 void b2md_runner_destroy(b2md_runner *r);
 /* Swap in bigger list buffers after B2MD_RUN_OVERFLOW (nbr: round_up(stride,16)*pitch, zero-filled). */
 int b2md_runner_set_list(b2md_runner *r, int32_t *nbr, int32_t stride);
+/* ... and the matching pair-row buffer (pair_rows >= 2 * round_up(stride,16)). */
+int b2md_runner_set_pair_list(b2md_runner *r, int32_t *pair_nbr, int32_t pair_rows);
 /* (Re)build the list for the current positions and evaluate forces
  * (Simulation.__init__'s initial _compute_forces, sim.py:90).  Synchronous. */
 int b2md_runner_prepare(b2md_runner *r, b2md_run_report *report);

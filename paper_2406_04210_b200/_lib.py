@@ -67,7 +67,8 @@ class RunnerConfig(Structure):
         ("keys", c_void_p), ("keys_tmp", c_void_p), ("perm", c_void_p), ("perm_tmp", c_void_p),
         ("sort_scratch", c_void_p),
         ("status", c_void_p), ("stream", c_void_p),
-        ("use_graph", c_int32), ("reserved0", c_int32),
+        ("use_graph", c_int32), ("pair_rows", c_int32),
+        ("pair_nbr", c_void_p), ("pair_counts", c_void_p), ("pair_pitch", c_int64),
     ]
 
 
@@ -120,6 +121,9 @@ _SIGNATURES = {
     "b2md_max_displacement": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),
     "b2md_force_lj": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, c_int32, _P,
                                 POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
+    "b2md_pair_rows": (c_int32, [_P, _P, c_int64, c_int32, c_int64, _P, _P, c_int64, c_int32, _P]),
+    "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
+                                      _P, POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_force_lj_all_pairs": (c_int32, [_P, c_int64, POINTER(Box), POINTER(c_double), c_int32,
                                           _P, _P, _P, _P]),
     "b2md_vv_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,
@@ -147,6 +151,7 @@ _SIGNATURES = {
     "b2md_runner_create": (c_void_p, [POINTER(RunnerConfig)]),
     "b2md_runner_destroy": (None, [c_void_p]),
     "b2md_runner_set_list": (c_int32, [c_void_p, _P, c_int32]),
+    "b2md_runner_set_pair_list": (c_int32, [c_void_p, _P, c_int32]),
     "b2md_runner_prepare": (c_int32, [c_void_p, POINTER(RunReport)]),
     "b2md_runner_run": (c_int32, [c_void_p, c_int64, c_int32, POINTER(RunReport)]),
 }

@@ -100,6 +100,38 @@ __device__ __forceinline__ void lj_pair_single(RowAcc &acc, float dx, float dy, 
     }
 }
 
+// Pair-row variant: `flag` is the entry's ownership bit for this particle; the
+// masked reciprocal is one LOP3 (bit -> predicate), one FSETP.LT.AND and one FSEL.
+__device__ __forceinline__ float masked_rcp(float r2, float rc2, int e, int bit) {
+    float out;
+    const float rc = rcp_fast(r2);
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %3, %4;\n\t"
+        "setp.ne.u32 q, t, 0;\n\t"
+        "setp.lt.and.f32 p, %1, %2, q;\n\t"
+        "selp.f32 %0, %5, 0f00000000, p;\n\t}"
+        : "=f"(out) : "f"(r2), "f"(rc2), "r"(e), "r"(bit), "f"(rc));
+    return out;
+}
+
+// Same arithmetic as lj_pair_single / lj_pair_table from the masked reciprocal on.
+template <bool THERMO>
+__device__ __forceinline__ void lj_apply_single(RowAcc &acc, float dx, float dy, float dz,
+                                                float ir2, const PairParams &p) {
+    const float s2 = p.sig2 * ir2;
+    const float s6 = s2 * s2 * s2;
+    const float t = s6 * fmaf(2.0f, s6, -1.0f);
+    const float g = t * ir2;
+    acc.fx = fmaf(g, dx, acc.fx);
+    acc.fy = fmaf(g, dy, acc.fy);
+    acc.fz = fmaf(g, dz, acc.fz);
+    if (THERMO) {
+        acc.u = fmaf(s6, s6 - 1.0f, acc.u);
+        acc.w += t;
+        acc.cnt += ir2 != 0.0f ? 1 : 0;
+    }
+}
+
 template <bool THERMO>
 __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, float dz, float r2,
                                               bool valid, const float4 pa, const float2 pb) {
@@ -315,6 +347,251 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
         report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
 }
 
+// ---- pair rows: two particles per thread -------------------------------------
+// Thread t owns particles 2t and 2t+1 and walks their merged row (k_pair_rows in
+// nlist.cu: ascending j, entry = j << 2 | listed-for-2t | listed-for-2t+1 << 1,
+// int4 tiles).  r_j is gathered once and evaluated against both particles; an
+// entry that only one of them lists contributes exact zeros to the other, so each
+// particle's sums are bit-identical to the one-row kernel's (same ascending-j
+// order, same fp32 sequence).  Compared with one thread per particle this needs
+// about a third fewer 16-byte gathers and index bytes per particle -- the L1 data
+// pipe, not HBM or issue, limits the one-row kernel -- and one 16-byte index load
+// per four entries instead of four 4-byte ones.
+template <int AXES, bool TABLE, bool THERMO>
+__device__ __forceinline__ void pair_entry(RowAcc &A, RowAcc &B, const float4 pa, const float4 pb,
+                                           int e, const float4 pj, const ForceArgs &a,
+                                           const float4 *s_tab_a, const float2 *s_tab_b,
+                                           int ta_row, int tb_row) {
+    const BoxF &b = a.box;
+    const int tj = TABLE ? __float_as_int(pj.w) : 0;
+    {
+        const float dx = delta<(AXES & 1) != 0>(pa.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<(AXES & 2) != 0>(pa.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<(AXES & 4) != 0>(pa.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (TABLE)
+            lj_pair_table<THERMO>(A, dx, dy, dz, r2, (e & 1) != 0, s_tab_a[ta_row + tj],
+                                  s_tab_b[ta_row + tj]);
+        else
+            lj_apply_single<THERMO>(A, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 1), a.single);
+    }
+    {
+        const float dx = delta<(AXES & 1) != 0>(pb.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<(AXES & 2) != 0>(pb.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<(AXES & 4) != 0>(pb.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (TABLE)
+            lj_pair_table<THERMO>(B, dx, dy, dz, r2, (e & 2) != 0, s_tab_a[tb_row + tj],
+                                  s_tab_b[tb_row + tj]);
+        else
+            lj_apply_single<THERMO>(B, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 2), a.single);
+    }
+}
+
+// ---- packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2) -------------------------
+// One-species pairs: the two particles of a thread go through identical
+// instruction sequences against the same r_j, so they ride in the two halves of
+// sm_100's packed fp32 instructions -- half the issue slots for the same
+// per-lane IEEE operations (round-to-nearest, no contraction beyond the fmas the
+// scalar code has), hence the same bits as the scalar kernels.  A scalar operand
+// packed with itself is encoded by ptxas as a broadcast, not a move.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f32x2 pk1(float v) { return pk(v, v); }
+__device__ __forceinline__ void upk(f32x2 v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// delta<CAREFUL> for both particles of a pair against one x_j
+template <bool CAREFUL>
+__device__ __forceinline__ f32x2 delta2(f32x2 xi, float xj, float L_hi, float L_lo, float invL) {
+    const f32x2 d0 = sub2(xi, pk1(xj));
+    if (!CAREFUL) return d0;
+    const float magic = 12582912.0f;  // 1.5 * 2^23 (rint_small)
+    const f32x2 ns = sub2(add2(mul2(d0, pk1(invL)), pk1(magic)), pk1(magic));
+    float n0, n1;
+    upk(ns, n0, n1);
+    // fmaf(-m, L, x) == fmaf(m, -L, x): the negation moves onto the constant
+    const f32x2 sa = fma2(pk(fmaxf(n0, 0.0f), fmaxf(n1, 0.0f)), pk1(-L_hi), xi);
+    const f32x2 sb = fma2(pk(fmaxf(-n0, 0.0f), fmaxf(-n1, 0.0f)), pk1(-L_hi), pk1(xj));
+    return fma2(ns, pk1(-L_lo), sub2(sa, sb));
+}
+
+struct PackAcc {
+    f32x2 fx, fy, fz, u, w;   // halves: particle 2t, particle 2t+1
+    int cnt_a, cnt_b;
+};
+
+template <int AXES, bool THERMO>
+__device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 ay, f32x2 az,
+                                                  int e, const float4 pj, const ForceArgs &a) {
+    const BoxF &b = a.box;
+    const PairParams &p = a.single;
+    const f32x2 dx = delta2<(AXES & 1) != 0>(ax, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+    const f32x2 dy = delta2<(AXES & 2) != 0>(ay, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+    const f32x2 dz = delta2<(AXES & 4) != 0>(az, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+    float r2a, r2b;
+    upk(r2, r2a, r2b);
+    const float ia = masked_rcp(r2a, p.rc2, e, 1), ib = masked_rcp(r2b, p.rc2, e, 2);
+    const f32x2 ir2 = pk(ia, ib);
+    const f32x2 s2 = mul2(pk1(p.sig2), ir2);
+    const f32x2 s6 = mul2(mul2(s2, s2), s2);
+    const f32x2 t = mul2(s6, fma2(pk1(2.0f), s6, pk1(-1.0f)));
+    const f32x2 g = mul2(t, ir2);
+    acc.fx = fma2(g, dx, acc.fx);
+    acc.fy = fma2(g, dy, acc.fy);
+    acc.fz = fma2(g, dz, acc.fz);
+    if (THERMO) {
+        acc.u = fma2(s6, add2(s6, pk1(-1.0f)), acc.u);
+        acc.w = add2(acc.w, t);
+        acc.cnt_a += ia != 0.0f ? 1 : 0;
+        acc.cnt_b += ib != 0.0f ? 1 : 0;
+    }
+}
+
+// `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
+// flag-less entries); the index tiles of the next two trips are kept in flight.
+template <int AXES, bool TABLE, bool THERMO>
+__device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4 pa,
+                                              const float4 pb, int tiles,
+                                              const int4 *__restrict__ col, int64_t pair_pitch,
+                                              const float4 *__restrict__ pos, const ForceArgs &a,
+                                              const float4 *s_tab_a, const float2 *s_tab_b,
+                                              int ta_row, int tb_row) {
+    // The loop body is kept to one trip: unrolling it further (to rotate the tile
+    // registers without moves) made instruction fetch the limiter -- 30 % of the
+    // stall samples were "no instruction".
+    const int4 zero = make_int4(0, 0, 0, 0);
+    int4 e0 = tiles > 0 ? __ldcs(col) : zero;
+    int4 e1 = tiles > 1 ? __ldcs(col + pair_pitch) : zero;
+    col += 2 * pair_pitch;
+    PackAcc acc = {0ull, 0ull, 0ull, 0ull, 0ull, 0, 0};     // +0.0f in both halves
+    const f32x2 ax = pk(pa.x, pb.x), ay = pk(pa.y, pb.y), az = pk(pa.z, pb.z);
+#pragma unroll 1
+    for (int q = 0; q < tiles; ++q) {
+        const int ev[4] = {e0.x, e0.y, e0.z, e0.w};
+        e0 = e1;
+        e1 = (q + 2 < tiles) ? __ldcs(col) : zero;      // warp-uniform
+        col += pair_pitch;
+        float4 pj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + ((unsigned)ev[u] >> 2));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (TABLE)
+                pair_entry<AXES, TABLE, THERMO>(A, B, pa, pb, ev[u], pj[u], a, s_tab_a, s_tab_b,
+                                                ta_row, tb_row);
+            else
+                pair_entry_packed<AXES, THERMO>(acc, ax, ay, az, ev[u], pj[u], a);
+        }
+    }
+    if (!TABLE) {
+        upk(acc.fx, A.fx, B.fx);
+        upk(acc.fy, A.fy, B.fy);
+        upk(acc.fz, A.fz, B.fz);
+        upk(acc.u, A.u, B.u);
+        upk(acc.w, A.w, B.w);
+        A.cnt = acc.cnt_a;
+        B.cnt = acc.cnt_b;
+    }
+}
+
+template <bool TABLE, bool THERMO>
+__global__ void __launch_bounds__(kForceThreads, 8)
+k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
+                const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
+                int64_t pair_pitch, const int32_t *__restrict__ nbr,
+                const int32_t *__restrict__ counts, int64_t pitch,
+                const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
+                float *__restrict__ virial, b2md_status *status, int gated) {
+    __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    if (gated && *(volatile int *)&status->frozen) return;
+    if (TABLE) {
+        for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
+            s_tab_a[t] = a.tab_a[t];
+            s_tab_b[t] = a.tab_b[t];
+        }
+        __syncthreads();
+    }
+    const int64_t n_pairs = (n + 1) >> 1;
+    const int64_t t_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = t_raw < n_pairs;
+    const int64_t t = active ? t_raw : n_pairs - 1;
+    const int64_t ia = 2 * t;
+    const bool has_b = ia + 1 < n;
+    const int64_t ib = has_b ? ia + 1 : ia;
+    const float4 pa = pos[ia], pb = pos[ib];
+    const int cnt = active ? pair_counts[t] : 0;
+    const int tiles = __reduce_max_sync(0xffffffffu, (cnt + 3) >> 2);
+    const int axes = boundary ? __reduce_or_sync(0xffffffffu,
+                                                 active ? (int)(boundary[ia] | boundary[ib]) : 0)
+                              : 7;
+    const int4 *col = pair_nbr + t;
+    const int ta_row = TABLE ? __float_as_int(pa.w) * a.ntypes : 0;
+    const int tb_row = TABLE ? __float_as_int(pb.w) * a.ntypes : 0;
+
+    RowAcc A = {0.f, 0.f, 0.f, 0.f, 0.f, 0}, B = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+#define B2MD_PAIR_LOOP(AXES)                                                                  \
+    pair_row_loop<AXES, TABLE, THERMO>(A, B, pa, pb, tiles, col, pair_pitch, pos, a, s_tab_a,  \
+                                       s_tab_b, ta_row, tb_row)
+    switch (axes) {                 // warp-uniform
+        case 0: B2MD_PAIR_LOOP(0); break;
+        case 1: B2MD_PAIR_LOOP(1); break;
+        case 2: B2MD_PAIR_LOOP(2); break;
+        case 4: B2MD_PAIR_LOOP(4); break;
+        default: B2MD_PAIR_LOOP(7); break;
+    }
+#undef B2MD_PAIR_LOOP
+    if (!active) return;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+        if (which == 1 && !has_b) break;
+        const RowAcc &acc = which ? B : A;
+        const int64_t i = which ? ib : ia;
+        float fx, fy, fz, u, w;
+        if (TABLE) {
+            fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
+        } else {
+            const PairParams &p = a.single;
+            fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+            u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
+            w = p.c_w * acc.w;
+        }
+        force[i] = make_float4(fx, fy, fz, u);
+        if (THERMO && virial) virial[i] = w;
+        if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
+            report_singular((int)i, which ? pb : pa, counts[i], nbr + i, pitch, pos, a.box,
+                            status);
+    }
+}
+
 // ---- all pairs, shared-memory tiles of 128 positions ------------------------
 template <bool TABLE>
 __global__ void __launch_bounds__(kForceThreads)
@@ -523,5 +800,43 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
         k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(
             (const float4 *)d_pos_hi, n, a, (float4 *)d_force_f4, d_virial, d_status);
     B2MD_CHECK_LAUNCH("b2md_force_lj_all_pairs");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                                    const int32_t *d_pair_nbr, const int32_t *d_pair_counts,
+                                    int64_t pair_pitch, const int32_t *d_nbr,
+                                    const int32_t *d_counts, int64_t pitch,
+                                    const uint8_t *d_boundary, const double *table,
+                                    int32_t ntypes, int32_t flags, void *d_force_f4,
+                                    float *d_virial, b2md_status *d_status, void *stream) {
+    if (n <= 0 || !d_pair_nbr || !d_pair_counts || !d_nbr || !d_counts || !d_status ||
+        pair_pitch < (n + 1) / 2) {
+        set_error("b2md_force_lj_pairs: bad arguments");
+        return -1;
+    }
+    ForceArgs a;
+    int rc = fill_args(a, box, table, ntypes);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
+#define B2MD_LAUNCH_PAIR(TABLE, THERMO)                                                       \
+    k_force_lj_pair<TABLE, THERMO><<<blocks, kForceThreads, 0, s>>>(                          \
+        (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
+        d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
+        (flags & B2MD_FORCE_GATED) ? 1 : 0)
+    // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 10 or
+    // 12 CTAs/SM (register-starved), 32/64-thread CTAs, position gathers one trip ahead
+    // and L2 prefetch of the index stream were all neutral or slower.
+    const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
+    if (ntypes == 1) {
+        if (thermo) B2MD_LAUNCH_PAIR(false, true);
+        else B2MD_LAUNCH_PAIR(false, false);
+    } else {
+        if (thermo) B2MD_LAUNCH_PAIR(true, true);
+        else B2MD_LAUNCH_PAIR(true, false);
+    }
+#undef B2MD_LAUNCH_PAIR
+    B2MD_CHECK_LAUNCH("b2md_force_lj_pairs");
     return 0;
 }

@@ -477,6 +477,66 @@ __global__ void k_max_disp(const float4 *__restrict__ pos_hi, const float4 *__re
                   (unsigned long long)__double_as_longlong(s));
 }
 
+
+// ---------------------------------------------------------------------------
+// Pair rows: the force kernel's own view of the list (b2md_pair_rows).
+//
+// Particles 2t and 2t+1 are neighbours in memory and -- after the Hilbert / cell
+// reorder -- in space, so their rows overlap heavily.  Thread t merges the two
+// ascending rows into one ascending "pair row": every distinct j once, with two
+// flag bits saying whose row it came from,
+//     entry = j << 2 | (listed for 2t) | (listed for 2t+1) << 1 .
+// The pair force kernel gathers r_j once and evaluates it against both particles,
+// which cuts the 16-byte position gathers per particle (the L1 data-pipe limiter
+// of the one-row kernel) by about a third and the index stream with them.
+//
+// Layout: int4 tiles, column-major in tile units -- entries 4q .. 4q+3 of pair t
+// are the int4 at d_pair_nbr[q * pair_pitch + t], so one 16-byte load per thread
+// and trip fetches four entries and a warp reads 512 contiguous bytes.  Rows are
+// padded with flag-less entries (j = 0) up to the longest row of the warp, so the
+// force kernel needs no per-entry bound check.
+__global__ void __launch_bounds__(128)
+k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
+            int64_t n_rows, int4 *__restrict__ pair_nbr, int32_t *__restrict__ pair_counts,
+            int64_t pair_pitch, int pair_tiles) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n_pairs = (n_rows + 1) >> 1;
+    const bool active = t < n_pairs;
+    const int64_t a = 2 * t, b = 2 * t + 1;
+    const int ca = active ? counts[a] : 0;
+    const int cb = (active && b < n_rows) ? counts[b] : 0;
+    const int32_t *ra = nbr + a, *rb = nbr + b;
+    constexpr int kEnd = 0x7fffffff;
+    int ia = 0, ib = 0;
+    int va = ca > 0 ? ra[0] : kEnd;
+    int vb = cb > 0 ? rb[0] : kEnd;
+    int e0 = 0, e1 = 0, e2 = 0, e3 = 0, k = 0;
+    int4 *out = pair_nbr + t;
+    const int cap = pair_tiles * 4;
+    while (va != kEnd || vb != kEnd) {
+        const int m = min(va, vb);
+        const bool from_a = va == m, from_b = vb == m;
+        const int e = (m << 2) | (from_a ? 1 : 0) | (from_b ? 2 : 0);
+        if (from_a) { ++ia; va = ia < ca ? ra[(int64_t)ia * pitch] : kEnd; }
+        if (from_b) { ++ib; vb = ib < cb ? rb[(int64_t)ib * pitch] : kEnd; }
+        e0 = e1; e1 = e2; e2 = e3; e3 = e;
+        ++k;
+        if ((k & 3) == 0 && k <= cap)
+            out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
+    }
+    const int total = k;                       // <= ca + cb <= capacity by construction
+    // flush the partial tile, then pad to the warp's longest row (flag-less entries)
+    while (k & 3) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; ++k; }
+    if (k > total && k <= cap)
+        out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
+    const int tiles = k >> 2;
+    const int warp_tiles = __reduce_max_sync(0xffffffffu, tiles);
+    if (t < pair_pitch)
+        for (int q = tiles; q < warp_tiles; ++q)
+            out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
+    if (t < pair_pitch) pair_counts[t] = active ? total : 0;
+}
+
 }  // namespace b2md
 
 using namespace b2md;
@@ -579,5 +639,28 @@ B2MD_EXPORT int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo
         (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, (const int4 *)d_image, n,
         make_box_d(box), d_at_build_f64, d_status);
     B2MD_CHECK_LAUNCH("b2md_max_displacement");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
+                               int32_t stride, int64_t n_rows, int32_t *d_pair_nbr, int32_t *d_pair_counts,
+                               int64_t pair_pitch, int32_t pair_rows, void *stream) {
+    if (!d_nbr || !d_counts || !d_pair_nbr || !d_pair_counts || n_rows < 1 || pitch < n_rows) {
+        set_error("b2md_pair_rows: bad arguments");
+        return -1;
+    }
+    const int64_t n_pairs = (n_rows + 1) / 2;
+    if (pair_pitch < n_pairs || pair_pitch % 32 != 0 || pair_rows % 4 != 0 ||
+        pair_rows < 2 * stride) {
+        set_error("b2md_pair_rows: pair_pitch must be a multiple of 32 >= ceil(n_rows/2), "
+                  "pair_rows a multiple of 4 >= 2 * stride");
+        return -2;
+    }
+    // whole warps only: the padding loop uses a warp reduction
+    const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
+    k_pair_rows<<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+                                                       (int4 *)d_pair_nbr, d_pair_counts,
+                                                       pair_pitch, pair_rows / 4);
+    B2MD_CHECK_LAUNCH("b2md_pair_rows");
     return 0;
 }

@@ -103,6 +103,11 @@ int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
     Set a = live(r);
     r->launches += 1;
     const int flags = (thermo ? 0 : B2MD_FORCE_SKIP_THERMO) | (gated ? B2MD_FORCE_GATED : 0);
+    if (c.pair_rows > 0)
+        return b2md_force_lj_pairs(a.pos_hi, c.n, &c.box, c.pair_nbr, c.pair_counts,
+                                   c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
+                                   r->table.data(), c.ntypes, flags, a.force, a.virial, c.status,
+                                   r->stream);
     return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, stride_rows(r),
                          c.boundary, r->table.data(), c.ntypes, flags, a.force, a.virial,
                          c.status, r->stream);
@@ -181,6 +186,11 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
     if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos, s)))
         return rc;
     *kernels += 1 + 6 + 2 + 1;
+    if (c.pair_rows > 0) {
+        if ((rc = b2md_pair_rows(c.nbr, c.counts, c.pitch, stride_rows(r), c.n, c.pair_nbr,
+                                 c.pair_counts, c.pair_pitch, c.pair_rows, s))) return rc;
+        *kernels += 1;
+    }
     return 0;
 }
 
@@ -423,6 +433,13 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
         set_error("b2md_runner_create: bad configuration");
         return nullptr;
     }
+    if (cfg->pair_rows != 0 &&
+        (!cfg->pair_nbr || !cfg->pair_counts || cfg->pair_rows % 4 != 0 ||
+         cfg->pair_rows < 2 * ((cfg->stride + 15) / 16 * 16) || cfg->pair_pitch % 32 != 0 ||
+         cfg->pair_pitch < (cfg->n + 1) / 2)) {
+        set_error("b2md_runner_create: bad pair-row buffers");
+        return nullptr;
+    }
     if (cfg->reorder_mode != 0 && (!cfg->keys || !cfg->keys_tmp || !cfg->perm || !cfg->perm_tmp ||
                                    !cfg->sort_scratch || cfg->reorder_every < 1 ||
                                    !cfg->pos_hi[1])) {
@@ -480,6 +497,18 @@ B2MD_EXPORT int b2md_runner_set_list(b2md_runner *r, int32_t *nbr, int32_t strid
     r->cfg.stride = stride;
     r->list_valid = false;
     destroy_graph(r);          // the list pointer and stride are baked into the graph
+    return 0;
+}
+
+B2MD_EXPORT int b2md_runner_set_pair_list(b2md_runner *r, int32_t *pair_nbr, int32_t pair_rows) {
+    if (!r || !pair_nbr || pair_rows % 4 != 0 || pair_rows < 2 * stride_rows(r)) {
+        set_error("b2md_runner_set_pair_list: bad arguments");
+        return -1;
+    }
+    r->cfg.pair_nbr = pair_nbr;
+    r->cfg.pair_rows = pair_rows;
+    r->list_valid = false;
+    destroy_graph(r);
     return 0;
 }
 

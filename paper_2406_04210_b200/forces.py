@@ -15,6 +15,7 @@ raises :class:`SingularPairError` naming the lowest i and its first partner j
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -49,12 +50,30 @@ def raise_if_singular(state: ParticleState, status: _lib.Status):
         raise SingularPairError(i, j)
 
 
+#: systems at least this large use the two-particles-per-thread kernel over pair
+#: rows; smaller ones are latency-bound and want more threads (sub-warp per particle)
+PAIR_ROWS_MIN_PARTICLES = 200_000
+
+
+def use_pair_rows(n: int, pair_rows: bool | None = None) -> bool:
+    """Kernel choice: explicit argument, else B2MD_PAIR_ROWS=0/1, else by size."""
+    if pair_rows is not None:
+        return bool(pair_rows)
+    env = os.environ.get("B2MD_PAIR_ROWS")
+    if env in ("0", "1"):
+        return env == "1"
+    return n >= PAIR_ROWS_MIN_PARTICLES
+
+
 def compute_forces_truncated(state: ParticleState, params, box: SimBox, nlist: NeighborList,
-                             backend: BackendSelector | None = None, check: bool = True):
+                             backend: BackendSelector | None = None, check: bool = True,
+                             pair_rows: bool | None = None):
     """Fill forces / per-particle potential / virial scanning listed neighbours.
 
     ``check=False`` skips the synchronising status read (the step loop polls the
-    status block itself at sample time)."""
+    status block itself at sample time).  ``pair_rows`` selects the kernel (None =
+    by system size): one thread per particle over the list itself, or one thread
+    per particle pair over the merged rows; per-particle results are bit-identical."""
     if nlist.overflow:
         raise NeighborOverflowError(
             "neighbor list overflowed its stride; rebuild with a larger one")
@@ -65,10 +84,18 @@ def compute_forces_truncated(state: ParticleState, params, box: SimBox, nlist: N
     dev = state.device_state()
     if check:
         dev.reset_status()
-    _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), dev.n, box.c_box(),
-              nlist.d_nbr.data_ptr(), nlist.d_counts.data_ptr(), nlist.pitch,
-              nlist.d_nbr.shape[0], nlist.d_boundary.data_ptr(), tab_ptr, nt, 0,
-              dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
+    if use_pair_rows(dev.n, pair_rows):
+        d_pair_nbr, d_pair_counts, pair_pitch = nlist.pair_rows()
+        _lib.call("b2md_force_lj_pairs", dev.pos_hi.data_ptr(), dev.n, box.c_box(),
+                  d_pair_nbr.data_ptr(), d_pair_counts.data_ptr(), pair_pitch,
+                  nlist.d_nbr.data_ptr(), nlist.d_counts.data_ptr(), nlist.pitch,
+                  nlist.d_boundary.data_ptr(), tab_ptr, nt, 0, dev.force.data_ptr(),
+                  dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
+    else:
+        _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), dev.n, box.c_box(),
+                  nlist.d_nbr.data_ptr(), nlist.d_counts.data_ptr(), nlist.pitch,
+                  nlist.d_nbr.shape[0], nlist.d_boundary.data_ptr(), tab_ptr, nt, 0,
+                  dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
     state.mark_compute_written("forces", "per_particle_potential", "virial")
     if check:
         raise_if_singular(state, dev.read_status())

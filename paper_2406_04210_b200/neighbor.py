@@ -132,6 +132,32 @@ class NeighborList:
         self.r_list = float(r_list)
         self.r_cut = float(r_cut)
         self.rebuild_count = int(rebuild_count)
+        self._pair = None          # (d_pair_nbr, d_pair_counts, pair_pitch), built on demand
+
+    def pair_rows(self):
+        """Merged rows of particles (2t, 2t+1) for the two-particles-per-thread force
+        kernel (``b2md_pair_rows``): returns ``(d_pair_nbr, d_pair_counts, pair_pitch)``
+        with ``d_pair_nbr`` of shape (tiles, pair_pitch, 4) int32, entry
+        ``j << 2 | listed_for_2t | listed_for_2t+1 << 1``.  Derived from this list
+        on first use and cached (the list is immutable once built)."""
+        if self._pair is None:
+            torch = _torch()
+            dev = self._dev
+            n = dev.n
+            rows = int(self.d_nbr.shape[0])
+            pair_pitch = _round_up((n + 1) // 2, 32)
+            buf = self._pair_buf
+            if buf is None or buf[0].shape != (2 * rows // 4, pair_pitch, 4):
+                buf = (torch.zeros((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
+                                   device=dev.device),
+                       torch.zeros(pair_pitch, dtype=torch.int32, device=dev.device))
+            _lib.call("b2md_pair_rows", self.d_nbr.data_ptr(), self.d_counts.data_ptr(),
+                      self.pitch, rows, n, buf[0].data_ptr(), buf[1].data_ptr(), pair_pitch,
+                      2 * rows, dev.stream)
+            self._pair = (buf[0], buf[1], pair_pitch)
+        return self._pair
+
+    _pair_buf = None               # buffers handed over by the list this one replaced
 
     @property
     def skin(self) -> float:
@@ -213,10 +239,14 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
               dev.image.data_ptr(), n, box.c_box(), d_at_build.data_ptr(), d_ref_pos.data_ptr(),
               dev.stream)
     st = dev.read_status()
-    return NeighborList(dev, d_nbr, d_counts, d_boundary, d_at_build, d_ref_pos, stride, pitch,
-                        overflow=st.overflow != 0, max_count=st.max_count, r_list=r_list,
-                        r_cut=r_cut,
-                        rebuild_count=(prev.rebuild_count if prev is not None else 0) + 1)
+    out = NeighborList(dev, d_nbr, d_counts, d_boundary, d_at_build, d_ref_pos, stride, pitch,
+                       overflow=st.overflow != 0, max_count=st.max_count, r_list=r_list,
+                       r_cut=r_cut,
+                       rebuild_count=(prev.rebuild_count if prev is not None else 0) + 1)
+    if reuse and prev._pair is not None:
+        out._pair_buf = prev._pair[:2]     # same shapes: merge into the old buffers
+        prev._pair = None
+    return out
 
 
 def max_displacement_sq(state: ParticleState, box: SimBox, nlist: NeighborList) -> float:

@@ -30,7 +30,7 @@ from . import _lib
 from .backend import BackendSelector
 from .core import COMPUTE, DeviceState, ParticleState, SignalEngine, SimBox
 from .errors import ConfigError, NeighborOverflowError, SingularPairError
-from .forces import compute_forces_all_to_all, compute_forces_truncated
+from .forces import compute_forces_all_to_all, compute_forces_truncated, use_pair_rows
 from .integrate import IntegratorParams, andersen_thermostat, vv_finalize, vv_integrate
 from .neighbor import (HILBERT_SUB_BITS, NeighborList, _round_up, bin_particles,
                        build_neighbor_list, grid_shape, needs_rebuild, reorder_hilbert)
@@ -60,7 +60,8 @@ class Simulation:
                  sample_interval: int = 100, deterministic: bool = True,
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
-                 stride_policy: str = "fit", graph: int | bool = False):
+                 stride_policy: str = "fit", graph: int | bool = False,
+                 pair_rows: bool | None = None):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -88,6 +89,8 @@ class Simulation:
         self.reorder_every = max(int(reorder_every), 1)
         self.stride_policy = stride_policy
         self.graph = int(graph)          # MD steps per captured CUDA graph (0 = host-driven)
+        # force kernel: one thread per particle pair over merged rows (None = by size)
+        self.pair_rows = use_pair_rows(state.n, pair_rows)
         self.graph_steps = 0
         # the thermostat acts between finalize and the next integrate: operator loop
         self.native = (force_mode == TRUNCATED and not thermostatted) if native is None \
@@ -156,7 +159,8 @@ class Simulation:
             self._rebuild()
         self.nlist_seconds += time.perf_counter() - t0
         t0 = time.perf_counter()
-        compute_forces_truncated(self.state, self.lj, self.box, self._nlist, self.backend)
+        compute_forces_truncated(self.state, self.lj, self.box, self._nlist, self.backend,
+                                 pair_rows=self.pair_rows)
         self.force_seconds += time.perf_counter() - t0
 
     def _grow_stride(self, max_count: int):
@@ -198,6 +202,14 @@ class Simulation:
         rows = _round_up(self._stride, 16)
         # zero-filled: padding entries must stay valid row indices
         return torch.zeros((rows, pitch), dtype=torch.int32, device=dev.device), pitch
+
+    def _alloc_pair_list(self, dev: DeviceState):
+        """Pair-row buffer: 2 * rows entries per pair, so a merge never overflows."""
+        torch = _torch()
+        rows = _round_up(self._stride, 16)
+        pair_pitch = _round_up((dev.n + 1) // 2, 32)
+        return (torch.zeros((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
+                            device=dev.device), pair_pitch, 2 * rows)
 
     def _native_setup(self):
         torch = _torch()
@@ -259,6 +271,11 @@ class Simulation:
         cfg.status = dev.status.data_ptr()
         cfg.stream = dev.stream
         cfg.use_graph = self.graph
+        if self.pair_rows:
+            k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
+            k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
+            cfg.pair_nbr = k["pair_nbr"].data_ptr()
+            cfg.pair_counts = k["pair_counts"].data_ptr()
         k["cfg"] = cfg
         dev.reset_status()
         handle = lib.b2md_runner_create(ctypes.byref(cfg))
@@ -300,6 +317,11 @@ class Simulation:
                 self._keep["nbr"], _ = self._alloc_list(dev)
                 _lib.call("b2md_runner_set_list", self._runner, self._keep["nbr"].data_ptr(),
                           self._stride)
+                if self.pair_rows:
+                    self._keep["pair_nbr"], _, rows2 = self._alloc_pair_list(dev)
+                    _lib.call("b2md_runner_set_pair_list", self._runner,
+                              self._keep["pair_nbr"].data_ptr(), rows2)
+                    self._keep["cfg"].pair_rows = rows2
                 continue
             return
 

@@ -308,32 +308,35 @@ def check_forces(pos, edges, params, r_list, species=None, stride=256):
     grid = b2.bin_particles(st, box, r_list)
     nl = b2.build_neighbor_list(st, grid, r_list, stride, r_cut=params.max_r_cut)
     assert not nl.overflow
-    b2.compute_forces_truncated(st, params, box, nl)
     og = orc.bin_particles(pos, edges, r_list)
     onl = orc.build_neighbor_list(pos, np.zeros_like(pos, dtype=np.int64), og, r_list, stride,
                                   r_cut=params.max_r_cut, threads=orc.host_threads())
     table = params.table()
     rf, rpe, rw = orc.forces_truncated(pos, edges, table, onl, species=species,
                                        threads=orc.host_threads())
-    f = st.forces.acquire_read(b2.HOST)
-    pe = st.per_particle_potential.acquire_read(b2.HOST)
-    w = st.virial.acquire_read(b2.HOST)
     # Stated metric: absolute error of each per-particle
     # quantity relative to the sum of the magnitudes of its pair terms (backward-
     # error scale), plus the rms-force scale for the force vector.
     fs, us, ws = orc.pair_scales(pos, edges, table, onl, species=species,
                                  threads=orc.host_threads())
-    m = force_error_metrics(f, rf, fs)
-    assert m["M2"] <= FORCE_TOL, m      # error / sum_j |f_ij|  (the stated per-particle metric)
-    assert np.linalg.norm(f - rf) <= FORCE_TOL * np.linalg.norm(rf)   # relative L2 error
-    # per-particle error against the NET force (cancellation-sensitive: the net force
-    # can be 100x smaller than the pair terms it is the sum of) -- looser bound
-    assert m["M1"] <= 1e-4, m
-    assert backward_error(pe, rpe, us) <= FORCE_TOL
-    assert backward_error(w, rw, ws) <= FORCE_TOL
-    # totals (what measure() reports) are far tighter
-    assert abs(pe.sum() - rpe.sum()) <= 1e-6 * np.abs(rpe).sum()
-    assert abs(w.sum() - rw.sum()) <= 1e-6 * np.abs(rw).sum()
+    # both force kernels: thread (or sub-warp) per particle over the list itself,
+    # and thread per particle pair over the merged rows
+    for pair_rows in (True, False):
+        b2.compute_forces_truncated(st, params, box, nl, pair_rows=pair_rows)
+        f = st.forces.acquire_read(b2.HOST)
+        pe = st.per_particle_potential.acquire_read(b2.HOST)
+        w = st.virial.acquire_read(b2.HOST)
+        m = force_error_metrics(f, rf, fs)
+        assert m["M2"] <= FORCE_TOL, m      # error / sum_j |f_ij|  (the stated per-particle metric)
+        assert np.linalg.norm(f - rf) <= FORCE_TOL * np.linalg.norm(rf)   # relative L2 error
+        # per-particle error against the NET force (cancellation-sensitive: the net force
+        # can be 100x smaller than the pair terms it is the sum of) -- looser bound
+        assert m["M1"] <= 1e-4, m
+        assert backward_error(pe, rpe, us) <= FORCE_TOL
+        assert backward_error(w, rw, ws) <= FORCE_TOL
+        # totals (what measure() reports) are far tighter
+        assert abs(pe.sum() - rpe.sum()) <= 1e-6 * np.abs(rpe).sum()
+        assert abs(w.sum() - rw.sum()) <= 1e-6 * np.abs(rw).sum()
     return st, box, nl, m
 
 
