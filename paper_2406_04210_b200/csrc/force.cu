@@ -132,6 +132,25 @@ __device__ __forceinline__ void lj_apply_single(RowAcc &acc, float dx, float dy,
     }
 }
 
+// lj_pair_table with the entry's ownership bit folded into the masked reciprocal
+template <bool THERMO>
+__device__ __forceinline__ void lj_apply_table(RowAcc &acc, float dx, float dy, float dz, float r2,
+                                               int e, int bit, const float4 pa, const float2 pb) {
+    const float ir2 = masked_rcp(r2, pa.y, e, bit);
+    const float s2 = pa.x * ir2;
+    const float s6 = s2 * s2 * s2;
+    const float t = s6 * fmaf(2.0f, s6, -1.0f);
+    const float g = pa.z * t * ir2;
+    acc.fx = fmaf(g, dx, acc.fx);
+    acc.fy = fmaf(g, dy, acc.fy);
+    acc.fz = fmaf(g, dz, acc.fz);
+    if (THERMO) {
+        acc.u = fmaf(pa.w * s6, s6 - 1.0f, acc.u);
+        acc.u += ir2 != 0.0f ? pb.x : 0.0f;
+        acc.w = fmaf(pb.y, t, acc.w);
+    }
+}
+
 template <bool THERMO>
 __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, float dz, float r2,
                                               bool valid, const float4 pa, const float2 pb) {
@@ -370,8 +389,8 @@ __device__ __forceinline__ void pair_entry(RowAcc &A, RowAcc &B, const float4 pa
         const float dz = delta<(AXES & 4) != 0>(pa.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
         const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
         if (TABLE)
-            lj_pair_table<THERMO>(A, dx, dy, dz, r2, (e & 1) != 0, s_tab_a[ta_row + tj],
-                                  s_tab_b[ta_row + tj]);
+            lj_apply_table<THERMO>(A, dx, dy, dz, r2, e, 1, s_tab_a[ta_row + tj],
+                                   s_tab_b[ta_row + tj]);
         else
             lj_apply_single<THERMO>(A, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 1), a.single);
     }
@@ -381,8 +400,8 @@ __device__ __forceinline__ void pair_entry(RowAcc &A, RowAcc &B, const float4 pa
         const float dz = delta<(AXES & 4) != 0>(pb.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
         const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
         if (TABLE)
-            lj_pair_table<THERMO>(B, dx, dy, dz, r2, (e & 2) != 0, s_tab_a[tb_row + tj],
-                                  s_tab_b[tb_row + tj]);
+            lj_apply_table<THERMO>(B, dx, dy, dz, r2, e, 2, s_tab_a[tb_row + tj],
+                                   s_tab_b[tb_row + tj]);
         else
             lj_apply_single<THERMO>(B, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 2), a.single);
     }
@@ -825,9 +844,9 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
         (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
         (flags & B2MD_FORCE_GATED) ? 1 : 0)
-    // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 10 or
-    // 12 CTAs/SM (register-starved), 32/64-thread CTAs, position gathers one trip ahead
-    // and L2 prefetch of the index stream were all neutral or slower.
+    // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 7, 9,
+    // 10 or 12 CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead and L2
+    // prefetch of the index stream were all neutral or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
     if (ntypes == 1) {
         if (thermo) B2MD_LAUNCH_PAIR(false, true);

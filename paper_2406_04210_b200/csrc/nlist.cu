@@ -12,6 +12,7 @@
 // Output layout is column-major and padded: entry k of particle i lives at
 // nbr[k * pitch + i], so the force kernel's per-k loads coalesce across a warp.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -404,6 +405,305 @@ k_list_cells_warp(const float4 *__restrict__ pos_hi, const float4 *__restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Production build kernel, second generation: one warp per cell, LANE = CANDIDATE.
+//
+// k_list_cells_warp keeps one particle of the cell per lane (19 of 32 lanes busy
+// at rho = 0.75) and walks all 513 candidates per lane; its per-lane compaction
+// and the settle / sort pass behind it made it issue-bound at ~30 instructions per
+// candidate.  Here the roles are swapped: the candidates of the 27 neighbour cells
+// form one stream in ascending visiting order, every lane holds one candidate of a
+// 32-wide chunk (all lanes busy), and the cell's particles are walked one after the
+// other by shared-memory broadcast.  The listing decision of a chunk is a ballot,
+// the slot of an accepted candidate is the population count of the lower lanes, so
+// rows are compacted in stream order without any per-lane state: they are born
+// ascending whenever the particle order is cell-contiguous (always, after the
+// Hilbert / cell reorder) -- checked while staging, else a sort pass runs.
+// The fp32 distance pre-sorts as before; the rare candidate inside the guard band
+// is settled on the spot with the reference's exact fp64 sequence (warp-uniform
+// branch), so rows are final -- and bit-identical to the reference -- as written.
+// Rows wanting more than `stride` entries send the cell through the reference-order
+// rescan of k_list_cells_warp (the kept prefix must be the reference's).
+constexpr int kStreamCap = 640;    // candidate indices staged per batch and warp
+
+constexpr int kPassRows = 24;      // particles of the cell handled per pass
+constexpr int kMaskPitch = kStreamCap / 32 + 1;   // ballot words per row and batch (odd)
+
+__host__ __device__ inline size_t ballot_warp_bytes() {
+    return (kPassRows / 2) * 2 * sizeof(float4) + kPassRows * kMaskPitch * sizeof(uint32_t) +
+           kStreamCap * sizeof(int32_t);
+}
+
+// One particle's row straight into the column-major list in the reference's scan
+// order (27 cells, x offset outermost; neighbor.py:126-149) with exact decisions,
+// then sorted ascending in place (neighbor.py:152).  Slow path of the ballot kernel:
+// rows that overflow `stride` (the kept prefix must be the reference's) and particle
+// orders that are not cell-contiguous.  Returns the unclamped count.
+__device__ __noinline__ int scan_row_reference_order(
+    const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, const ListGeom &g,
+    int cx, int cy, int cz, const int32_t *__restrict__ cell_start,
+    const int32_t *__restrict__ cell_particles, int i, const float4 hi_i, int stride,
+    int64_t pitch, int32_t *__restrict__ nbr) {
+    int found = 0;
+    for (int t = 0; t < 27; ++t) {
+        int cj; float sx, sy, sz;
+        neighbour_cell(g, cx, cy, cz, t, cj, sx, sy, sz);
+        const int p_end = cell_start[cj + 1];
+        for (int p = cell_start[cj]; p < p_end; ++p) {
+            const int j = cell_particles[p];
+            if (j == i) continue;
+            const float4 hj = __ldg(&pos_hi[j]);
+            const float dx = hi_i.x - (hj.x + sx), dy = hi_i.y - (hj.y + sy),
+                        dz = hi_i.z - (hj.z + sz);
+            const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            if (r2f > g.rl2_out) continue;
+            if (r2f < g.rl2_in || listed_exact(pos_hi, pos_lo, i, j, g)) {
+                if (found < stride) nbr[(int64_t)found * pitch + i] = j;
+                ++found;
+            }
+        }
+    }
+    const int kept = min(found, stride);
+    for (int a = 1; a < kept; ++a) {
+        const int v = nbr[(int64_t)a * pitch + i];
+        int b = a - 1;
+        while (b >= 0) {
+            const int w = nbr[(int64_t)b * pitch + i];
+            if (w <= v) break;
+            nbr[(int64_t)(b + 1) * pitch + i] = w;
+            --b;
+        }
+        if (b + 1 != a) nbr[(int64_t)(b + 1) * pitch + i] = v;
+    }
+    return found;
+}
+
+// fp32x2 helpers (FADD2 / FMUL2 / FFMA2): two particles of the cell per instruction
+__device__ __forceinline__ unsigned long long nl_pk(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long nl_sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long nl_mul2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long nl_fma2(unsigned long long a, unsigned long long b,
+                                                      unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
+                    int64_t n, int64_t n_rows, const __grid_constant__ ListGeom g,
+                    int64_t n_cells, const int32_t *__restrict__ cell_start,
+                    const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
+                    int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
+                    uint8_t *__restrict__ boundary, b2md_status *status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char *base = smem_raw + warp * ballot_warp_bytes();
+    // particles of the pass, two per slot: A = (x0, x1, y0, y1), B = (z0, z1, i0, i1)
+    float4 *s_pa = reinterpret_cast<float4 *>(base);
+    float4 *s_pb = s_pa + kPassRows / 2;
+    uint32_t *s_mask = reinterpret_cast<uint32_t *>(s_pb + kPassRows / 2);   // [row][chunk]
+    int32_t *s_stream = reinterpret_cast<int32_t *>(s_mask + kPassRows * kMaskPitch);
+    const int64_t c = (int64_t)blockIdx.x * WARPS + warp;
+    if (c >= n_cells) return;
+    const int cz = (int)(c % g.nc[2]);
+    const int cy = (int)((c / g.nc[2]) % g.nc[1]);
+    const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
+    const int i_begin = cell_start[c], i_end = cell_start[c + 1];
+    if (i_begin == i_end) return;
+    const float rl2_in = g.rl2_in, rl2_out = g.rl2_out;
+
+    // visiting order: neighbour cells by ascending first-occupant index (lane s = slot s)
+    int my_key = 0x7fffffff, my_begin = 0, my_size = 0, my_wrap = 0;
+    if (lane < 27) {
+        int cj; float sx, sy, sz;
+        neighbour_cell(g, cx, cy, cz, lane, cj, sx, sy, sz);
+        my_begin = cell_start[cj];
+        my_size = cell_start[cj + 1] - my_begin;
+        if (my_size > 0) my_key = cell_particles[my_begin];
+        // periodic image of the whole neighbour cell: 2 bits per axis (0: -L, 1: 0, 2: +L)
+        my_wrap = ((sx < 0.f) ? 0 : (sx > 0.f) ? 2 : 1) | (((sy < 0.f) ? 0 : (sy > 0.f) ? 2 : 1) << 2) |
+                  (((sz < 0.f) ? 0 : (sz > 0.f) ? 2 : 1) << 4);
+    }
+    int sorted_key = my_key, sorted_slot = lane;
+    warp_sort_pairs(sorted_key, sorted_slot, lane);
+    // lane t now describes the t-th cell to visit; v_end = candidates up to and including it
+    const int v_begin = __shfl_sync(0xffffffffu, my_begin, sorted_slot);
+    const int v_size = __shfl_sync(0xffffffffu, my_size, sorted_slot);
+    const int v_wrap = __shfl_sync(0xffffffffu, my_wrap, sorted_slot);
+    int v_end = v_size;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, v_end, o);
+        if (lane >= o) v_end += up;
+    }
+    const int n_cand = __shfl_sync(0xffffffffu, v_end, 31);
+    // Is the candidate stream ascending?  (Every visited cell a contiguous index range,
+    // ranges in ascending order: true after every Hilbert / cell reorder.)  Rows are
+    // then born sorted; otherwise the cell takes the slow path.
+    bool ascending;
+    {
+        const int first = sorted_key;                 // first occupant of visited cell `lane`
+        const int last = v_size > 0 ? cell_particles[v_begin + v_size - 1] : first;
+        const int prev_last = __shfl_up_sync(0xffffffffu, last, 1);
+        const bool ok = v_size == 0 ||
+                        (last - first == v_size - 1 && (lane == 0 || prev_last < first));
+        ascending = __all_sync(0xffffffffu, ok);
+    }
+
+    int wanted_max = 0;
+    for (int i0 = i_begin; i0 < i_end; i0 += kPassRows) {
+        const int ni = min(kPassRows, i_end - i0);
+        const int i_raw = (lane < ni) ? cell_particles[i0 + lane] : -1;
+        const bool active = i_raw >= 0 && i_raw < n_rows;    // ghost rows get no list
+        const int i = active ? i_raw : -1;
+        const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+        int found = 0;
+        if (ascending) {
+            __syncwarp();
+            if (lane < kPassRows) {
+                float *fa = reinterpret_cast<float *>(s_pa + (lane >> 1));
+                float *fb = reinterpret_cast<float *>(s_pb + (lane >> 1));
+                const int h = lane & 1;
+                fa[h] = hi_i.x;
+                fa[2 + h] = hi_i.y;
+                fb[h] = hi_i.z;
+                fb[2 + h] = __int_as_float(i);
+            }
+            int32_t *out = nbr + (active ? i : 0);       // entry k of this row: out[k * pitch]
+            for (int batch0 = 0; batch0 < n_cand; batch0 += kStreamCap) {
+                const int total = min(kStreamCap, n_cand - batch0);
+                const int n_chunks = (total + 31) >> 5;
+                __syncwarp();
+                // stage candidate indices (+ wrap code) of stream positions [batch0, +total)
+                for (int m0 = 0; m0 < total; m0 += 32) {         // warp-uniform trip count
+                    const int m = m0 + lane;
+                    const int pos = batch0 + min(m, total - 1);
+                    // visited cell holding stream position `pos`: first t with v_end[t] > pos
+                    int t = 0;
+#pragma unroll
+                    for (int bit = 16; bit > 0; bit >>= 1) {
+                        const int probe = __shfl_sync(0xffffffffu, v_end, min(t + bit - 1, 31));
+                        if (probe <= pos) t += bit;
+                    }
+                    const int ce = __shfl_sync(0xffffffffu, v_end, t);
+                    const int cs = __shfl_sync(0xffffffffu, v_size, t);
+                    const int cb = __shfl_sync(0xffffffffu, v_begin, t);
+                    const int cw = __shfl_sync(0xffffffffu, v_wrap, t);
+                    if (m < total)
+                        s_stream[m] = cell_particles[cb + (pos - (ce - cs))] | (cw << 26);
+                }
+                __syncwarp();
+                // ---- phase 1: all particles of the pass against 32 candidates per chunk;
+                // the decisions of row r on chunk w are one ballot, parked in s_mask[r][w]
+                for (int w = 0; w < n_chunks; ++w) {
+                    float qx = -1e30f, qy = -1e30f, qz = -1e30f;
+                    int j = -2;
+                    if (w * 32 + lane < total) {
+                        const int code = s_stream[w * 32 + lane];
+                        j = code & 0x03ffffff;
+                        const float4 hj = __ldg(&pos_hi[j]);
+                        qx = hj.x + (float)(((code >> 26) & 3) - 1) * g.Lf[0];
+                        qy = hj.y + (float)(((code >> 28) & 3) - 1) * g.Lf[1];
+                        qz = hj.z + (float)(((code >> 30) & 3) - 1) * g.Lf[2];
+                    }
+                    const unsigned long long qx2 = nl_pk(qx, qx), qy2 = nl_pk(qy, qy),
+                                             qz2 = nl_pk(qz, qz);
+                    bool in_band = false;
+                    uint32_t *mask_w = s_mask + w;
+#pragma unroll 2
+                    for (int p = 0; p < (ni + 1) >> 1; ++p) {
+                        const float4 A = s_pa[p], B = s_pb[p];               // broadcasts
+                        const unsigned long long dx = nl_sub2(nl_pk(A.x, A.y), qx2);
+                        const unsigned long long dy = nl_sub2(nl_pk(A.z, A.w), qy2);
+                        const unsigned long long dz = nl_sub2(nl_pk(B.x, B.y), qz2);
+                        const unsigned long long r2 =
+                            nl_fma2(dz, dz, nl_fma2(dy, dy, nl_mul2(dx, dx)));
+                        float r2a, r2b;
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(r2a), "=f"(r2b) : "l"(r2));
+                        const bool take_a = (r2a <= rl2_out) && (j != __float_as_int(B.z));
+                        const bool take_b = (r2b <= rl2_out) && (j != __float_as_int(B.w));
+                        in_band |= (take_a && r2a >= rl2_in) || (take_b && r2b >= rl2_in);
+                        const unsigned ha = __ballot_sync(0xffffffffu, take_a);
+                        const unsigned hb = __ballot_sync(0xffffffffu, take_b);
+                        if (lane == 0) {
+                            mask_w[(2 * p) * kMaskPitch] = ha;
+                            mask_w[(2 * p + 1) * kMaskPitch] = hb;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, in_band)) {
+                        // guard band (a shell ~1e-5 sigma thick): settle with the reference's
+                        // exact fp64 sequence and clear the bits that fail
+                        __syncwarp();
+                        for (int r = 0; r < ni; ++r) {
+                            const float *fa = reinterpret_cast<const float *>(s_pa + (r >> 1));
+                            const float *fb = reinterpret_cast<const float *>(s_pb + (r >> 1));
+                            const float dx = fa[r & 1] - qx, dy = fa[2 + (r & 1)] - qy,
+                                        dz = fb[r & 1] - qz;
+                            const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                            const int ir = __float_as_int(fb[2 + (r & 1)]);
+                            if ((r2f <= rl2_out) && (j != ir) && (r2f >= rl2_in) &&
+                                !listed_exact(pos_hi, pos_lo, ir, j, g))
+                                atomicAnd(&mask_w[r * kMaskPitch], ~(1u << lane));
+                        }
+                    }
+                }
+                __syncwarp();
+                // ---- phase 2: lane r walks the set bits of row r in stream order
+                // (= ascending j) and stores entry k of its row; all rows are at the
+                // same k, so the column-major stores coalesce across the cell's particles
+                {
+                    const uint32_t *my_mask = s_mask + lane * kMaskPitch;
+                    int w = 0;
+                    unsigned m = active ? my_mask[0] : 0u;
+                    const int my_chunks = active ? n_chunks : 0;
+                    for (;;) {
+                        while (m == 0u && w + 1 < my_chunks) m = my_mask[++w];
+                        if (!__any_sync(0xffffffffu, m != 0u)) break;
+                        if (m != 0u) {
+                            const int bit = __ffs(m) - 1;
+                            m &= m - 1u;
+                            const int j = s_stream[w * 32 + bit] & 0x03ffffff;
+                            if (found < stride) out[(int64_t)found * pitch] = j;
+                            ++found;
+                        }
+                    }
+                }
+            }
+        }
+        // slow path: non-contiguous particle order, or some row wants more than `stride`
+        // entries (the reference's scan order then decides which ones are kept)
+        if (!ascending || __any_sync(0xffffffffu, found > stride)) {
+            found = 0;
+            if (active)
+                found = scan_row_reference_order(pos_hi, pos_lo, g, cx, cy, cz, cell_start,
+                                                 cell_particles, i, hi_i, stride, pitch, nbr);
+        }
+        if (active) {
+            counts[i] = min(found, stride);
+            if (boundary) boundary[i] = boundary_flag(hi_i, g);
+        }
+        wanted_max = max(wanted_max, __reduce_max_sync(0xffffffffu, found));
+    }
+    if (lane == 0 && wanted_max > 0) {
+        if (wanted_max > stride) atomicExch(&status->overflow, 1);
+        atomicMax(&status->max_count, wanted_max);
+    }
+}
+
 // All-pairs scan for grids with fewer than three cells on some axis.
 __global__ void __launch_bounds__(kBuildThreads)
 k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, int64_t n,
@@ -574,10 +874,29 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n_rows, kBuildThreads);
     const size_t warp_smem = kCandCap * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
+    static int list_kernel = -1;           // 0: lane = candidate (default), 1: lane = particle
+    if (list_kernel < 0) {
+        const char *env = getenv("B2MD_LIST_KERNEL");
+        list_kernel = (env && atoi(env) == 1) ? 1 : 0;
+    }
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, stride, pitch, d_nbr,
             d_counts, d_boundary, d_status);
+    } else if (prefilter && list_kernel == 0 && n < (1ll << 26)) {
+        // lane = candidate; the wrap code shares the staged word with the index (26 bits)
+        constexpr int kBallotWarps = 8;
+        const int64_t nc = grid->n_cells;
+        const size_t smem = ballot_warp_bytes() * kBallotWarps;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_list_cells_ballot<kBallotWarps><<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
+            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
+            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
     } else if (prefilter && warp_smem * 2 <= 200 * 1024) {
         // warp-per-cell kernel; fewer warps per CTA when rows are long
         const int64_t nc = grid->n_cells;
