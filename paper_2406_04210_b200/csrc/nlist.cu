@@ -667,17 +667,22 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                 // same k, so the column-major stores coalesce across the cell's particles
                 {
                     const uint32_t *my_mask = s_mask + lane * kMaskPitch;
-                    int w = 0;
-                    unsigned m = active ? my_mask[0] : 0u;
                     const int my_chunks = active ? n_chunks : 0;
+                    const int32_t *my_stream = s_stream;         // advanced with the mask word
+                    int left = my_chunks - 1;                    // mask words not yet fetched
+                    unsigned m = active ? my_mask[0] : 0u;
                     for (;;) {
-                        while (m == 0u && w + 1 < my_chunks) m = my_mask[++w];
-                        if (!__any_sync(0xffffffffu, m != 0u)) break;
+                        if (m == 0u && left > 0) {               // next word (1 % are empty)
+                            m = *++my_mask;
+                            my_stream += 32;
+                            --left;
+                        }
+                        if (!__any_sync(0xffffffffu, (m != 0u) | (left > 0))) break;
                         if (m != 0u) {
-                            const int bit = __ffs(m) - 1;
+                            const int j = my_stream[__ffs(m) - 1] & 0x03ffffff;
                             m &= m - 1u;
-                            const int j = s_stream[w * 32 + bit] & 0x03ffffff;
-                            if (found < stride) out[(int64_t)found * pitch] = j;
+                            if (found < stride) *out = j;
+                            out += pitch;
                             ++found;
                         }
                     }
