@@ -145,6 +145,19 @@ int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                      uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
                      b2md_status *d_status, void *stream);
 
+/* Same, with flags.  B2MD_LIST_ANY_PREFIX: when a row overflows `stride` the kept
+ * entries need not be the reference's first `stride` hits in its scan order
+ * (neighbor.py:145-149) -- for callers that react to status->overflow by growing the
+ * stride and rebuilding (sim.py:141-149), as the native step loop does. */
+#define B2MD_LIST_ANY_PREFIX 1
+int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                        const b2md_box *box, const b2md_grid *grid,
+                        const int32_t *d_cell_of, const int32_t *d_cell_start,
+                        const int32_t *d_cell_particles, double r_list,
+                        int32_t stride, int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
+                        uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
+                        int32_t flags, b2md_status *d_status, void *stream);
+
 /* Snapshot of the unwrapped positions a list was built from
  * (neighbor.py:238, core.py:216-219): exact fp64 rows (n,3) and the fp32
  * reference copy used by the in-loop displacement check. */

@@ -508,7 +508,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                     int64_t n_cells, const int32_t *__restrict__ cell_start,
                     const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
                     int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
-                    uint8_t *__restrict__ boundary, b2md_status *status) {
+                    uint8_t *__restrict__ boundary, b2md_status *status, int exact_prefix) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char *base = smem_raw + warp * ballot_warp_bytes();
@@ -678,20 +678,24 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                             --left;
                         }
                         if (!__any_sync(0xffffffffu, (m != 0u) | (left > 0))) break;
-                        if (m != 0u) {
-                            const int j = my_stream[__ffs(m) - 1] & 0x03ffffff;
-                            m &= m - 1u;
-                            if (found < stride) *out = j;
-                            out += pitch;
-                            ++found;
+#pragma unroll
+                        for (int rep = 0; rep < 3; ++rep) {      // amortise the vote
+                            if (m != 0u) {
+                                const int j = my_stream[__ffs(m) - 1] & 0x03ffffff;
+                                m &= m - 1u;
+                                if (found < stride) *out = j;
+                                out += pitch;
+                                ++found;
+                            }
                         }
                     }
                 }
             }
         }
         // slow path: non-contiguous particle order, or some row wants more than `stride`
-        // entries (the reference's scan order then decides which ones are kept)
-        if (!ascending || __any_sync(0xffffffffu, found > stride)) {
+        // entries (the reference's scan order then decides which ones are kept; skipped
+        // when the caller is going to grow the stride and rebuild anyway)
+        if (!ascending || (exact_prefix && __any_sync(0xffffffffu, found > stride))) {
             found = 0;
             if (active)
                 found = scan_row_reference_order(pos_hi, pos_lo, g, cx, cy, cz, cell_start,
@@ -846,13 +850,14 @@ k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
 
 using namespace b2md;
 
-B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
-                                 const b2md_box *box, const b2md_grid *grid,
-                                 const int32_t *d_cell_of, const int32_t *d_cell_start,
-                                 const int32_t *d_cell_particles, double r_list, int32_t stride,
-                                 int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
-                                 uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
-                                 b2md_status *d_status, void *stream) {
+B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                    const b2md_box *box, const b2md_grid *grid,
+                                    const int32_t *d_cell_of, const int32_t *d_cell_start,
+                                    const int32_t *d_cell_particles, double r_list,
+                                    int32_t stride, int64_t pitch, int32_t *d_nbr,
+                                    int32_t *d_counts, uint8_t *d_boundary,
+                                    double boundary_margin, int64_t n_rows, int32_t flags,
+                                    b2md_status *d_status, void *stream) {
     if (n <= 0 || !box || !grid || !d_status) { set_error("b2md_build_nlist: bad arguments"); return -1; }
     if (stride < 1) { set_error("b2md_build_nlist: stride must be >= 1"); return -2; }
     if (pitch < n) { set_error("b2md_build_nlist: pitch < n"); return -3; }
@@ -901,7 +906,8 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
         }
         k_list_cells_ballot<kBallotWarps><<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
-            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
+            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status,
+            (flags & B2MD_LIST_ANY_PREFIX) ? 0 : 1);
     } else if (prefilter && warp_smem * 2 <= 200 * 1024) {
         // warp-per-cell kernel; fewer warps per CTA when rows are long
         const int64_t nc = grid->n_cells;
@@ -941,6 +947,18 @@ B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int
         k_count_boundary<<<blocks_for(n_rows, 256), 256, 0, s>>>(d_boundary, n_rows, d_status);
     B2MD_CHECK_LAUNCH("b2md_build_nlist");
     return 0;
+}
+
+B2MD_EXPORT int b2md_build_nlist(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                 const b2md_box *box, const b2md_grid *grid,
+                                 const int32_t *d_cell_of, const int32_t *d_cell_start,
+                                 const int32_t *d_cell_particles, double r_list, int32_t stride,
+                                 int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
+                                 uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
+                                 b2md_status *d_status, void *stream) {
+    return b2md_build_nlist_ex(d_pos_hi, d_pos_lo, n, box, grid, d_cell_of, d_cell_start,
+                               d_cell_particles, r_list, stride, pitch, d_nbr, d_counts,
+                               d_boundary, boundary_margin, n_rows, 0, d_status, stream);
 }
 
 B2MD_EXPORT int b2md_snapshot(const void *d_pos_hi, const void *d_pos_lo, const void *d_image,

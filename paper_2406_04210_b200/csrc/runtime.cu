@@ -179,9 +179,11 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
     if ((rc = b2md_status_reset_list(c.status, s))) return rc;
     if ((rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,
                        c.cell_particles, c.bin_scratch, s))) return rc;
-    if ((rc = b2md_build_nlist(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
-                               c.cell_start, c.cell_particles, r->r_list, c.stride, c.pitch,
-                               c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n, c.status, s)))
+    // an overflowed list is never used here: the caller grows the stride and rebuilds
+    if ((rc = b2md_build_nlist_ex(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
+                                  c.cell_start, c.cell_particles, r->r_list, c.stride, c.pitch,
+                                  c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n,
+                                  B2MD_LIST_ANY_PREFIX, c.status, s)))
         return rc;
     if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos, s)))
         return rc;
