@@ -494,6 +494,7 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
     }
 }
 
+
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
 template <int AXES, bool TABLE, bool THERMO>
@@ -845,8 +846,9 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
         (flags & B2MD_FORCE_GATED) ? 1 : 0)
     // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 7, 9,
-    // 10 or 12 CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead and L2
-    // prefetch of the index stream were all neutral or slower.
+    // 10 or 12 CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch
+    // of the index stream, L1::no_allocate indices / L1::evict_last positions were all
+    // neutral or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
     if (ntypes == 1) {
         if (thermo) B2MD_LAUNCH_PAIR(false, true);

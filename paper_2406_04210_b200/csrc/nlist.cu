@@ -434,11 +434,28 @@ __host__ __device__ inline size_t ballot_warp_bytes() {
            kStreamCap * sizeof(int32_t);
 }
 
+// Ascending order of one row of the column-major list, in place (neighbor.py:152);
+// insertion sort: the callers' rows are nearly sorted.
+__device__ __forceinline__ void sort_row_in_list(int32_t *__restrict__ nbr, int64_t pitch, int i,
+                                                 int kept) {
+    for (int a = 1; a < kept; ++a) {
+        const int v = nbr[(int64_t)a * pitch + i];
+        int b = a - 1;
+        while (b >= 0) {
+            const int w = nbr[(int64_t)b * pitch + i];
+            if (w <= v) break;
+            nbr[(int64_t)(b + 1) * pitch + i] = w;
+            --b;
+        }
+        if (b + 1 != a) nbr[(int64_t)(b + 1) * pitch + i] = v;
+    }
+}
+
 // One particle's row straight into the column-major list in the reference's scan
 // order (27 cells, x offset outermost; neighbor.py:126-149) with exact decisions,
-// then sorted ascending in place (neighbor.py:152).  Slow path of the ballot kernel:
-// rows that overflow `stride` (the kept prefix must be the reference's) and particle
-// orders that are not cell-contiguous.  Returns the unclamped count.
+// then sorted ascending in place.  Slow path of the ballot kernel for rows that
+// overflow `stride` (the kept prefix must be the reference's).  Returns the unclamped
+// count.
 __device__ __noinline__ int scan_row_reference_order(
     const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo, const ListGeom &g,
     int cx, int cy, int cz, const int32_t *__restrict__ cell_start,
@@ -463,18 +480,7 @@ __device__ __noinline__ int scan_row_reference_order(
             }
         }
     }
-    const int kept = min(found, stride);
-    for (int a = 1; a < kept; ++a) {
-        const int v = nbr[(int64_t)a * pitch + i];
-        int b = a - 1;
-        while (b >= 0) {
-            const int w = nbr[(int64_t)b * pitch + i];
-            if (w <= v) break;
-            nbr[(int64_t)(b + 1) * pitch + i] = w;
-            --b;
-        }
-        if (b + 1 != a) nbr[(int64_t)(b + 1) * pitch + i] = v;
-    }
+    sort_row_in_list(nbr, pitch, i, min(found, stride));
     return found;
 }
 
@@ -553,7 +559,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
     const int n_cand = __shfl_sync(0xffffffffu, v_end, 31);
     // Is the candidate stream ascending?  (Every visited cell a contiguous index range,
     // ranges in ascending order: true after every Hilbert / cell reorder.)  Rows are
-    // then born sorted; otherwise the cell takes the slow path.
+    // then born sorted; otherwise they are sorted after the fact.
     bool ascending;
     {
         const int first = sorted_key;                 // first occupant of visited cell `lane`
@@ -572,7 +578,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
         const int i = active ? i_raw : -1;
         const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
         int found = 0;
-        if (ascending) {
+        {
             __syncwarp();
             if (lane < kPassRows) {
                 float *fa = reinterpret_cast<float *>(s_pa + (lane >> 1));
@@ -692,14 +698,19 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                 }
             }
         }
-        // slow path: non-contiguous particle order, or some row wants more than `stride`
-        // entries (the reference's scan order then decides which ones are kept; skipped
-        // when the caller is going to grow the stride and rebuild anyway)
-        if (!ascending || (exact_prefix && __any_sync(0xffffffffu, found > stride))) {
+        // slow path: some row wants more than `stride` entries, so the reference's scan
+        // order decides which ones are kept (skipped when the caller is going to grow
+        // the stride and rebuild anyway)
+        if (exact_prefix && __any_sync(0xffffffffu, found > stride)) {
             found = 0;
             if (active)
                 found = scan_row_reference_order(pos_hi, pos_lo, g, cx, cy, cz, cell_start,
                                                  cell_particles, i, hi_i, stride, pitch, nbr);
+        } else if (!ascending && active) {
+            // particle order not cell-contiguous (never after a reorder; ghost rows of a
+            // slab are appended unsorted): rows came out in stream order -- ascending
+            // inside every cell, cells by first occupant -- so they are nearly sorted
+            sort_row_in_list(nbr, pitch, i, min(found, stride));
         }
         if (active) {
             counts[i] = min(found, stride);

@@ -366,6 +366,16 @@ class CudaSlabOps:
         rows = (self.stride + 15) // 16 * 16
         self.nbr = self.torch.zeros((rows, self.capacity), dtype=self.torch.int32,
                                     device=self.device)
+        # merged rows of owned particle pairs for the two-particles-per-thread force
+        # kernel (b2md_pair_rows); large slabs only, like the single-domain loop
+        from .forces import use_pair_rows
+        self.pair_rows = use_pair_rows(self.cap_own)
+        if self.pair_rows:
+            self.pair_pitch = ((self.cap_own + 1) // 2 + 31) // 32 * 32
+            self.pair_nbr = self.torch.zeros((2 * rows // 4, self.pair_pitch, 4),
+                                             dtype=self.torch.int32, device=self.device)
+            self.pair_counts = self.torch.zeros(self.pair_pitch, dtype=self.torch.int32,
+                                                device=self.device)
 
     def grow_stride(self, max_count):
         self.stride = max(self.stride + 1, ((int(max_count * 1.125) + 1) + 7) // 8 * 8)
@@ -533,6 +543,12 @@ class CudaSlabOps:
                   a["image"].data_ptr(), self.n_own, ctypes.byref(self.box), None,
                   self.ref_pos.data_ptr(), self.stream)
         self.kernel_launches += 1 + 6 + 2 + 1
+        if self.pair_rows:
+            _lib.call("b2md_pair_rows", self.nbr.data_ptr(), self.counts.data_ptr(),
+                      self.capacity, self.nbr.shape[0], self.n_own, self.pair_nbr.data_ptr(),
+                      self.pair_counts.data_ptr(), self.pair_pitch, 2 * self.nbr.shape[0],
+                      self.stream)
+            self.kernel_launches += 1
         st = _lib.Status.from_buffer_copy(self.status.cpu().numpy().tobytes())
         return st.overflow != 0, st.max_count
 
@@ -551,6 +567,16 @@ class CudaSlabOps:
 
     def force(self, thermo: bool):
         a = self.a
+        if self.pair_rows:
+            _lib.call("b2md_force_lj_pairs", a["pos_hi"].data_ptr(), self.n_own,
+                      ctypes.byref(self.box), self.pair_nbr.data_ptr(),
+                      self.pair_counts.data_ptr(), self.pair_pitch, self.nbr.data_ptr(),
+                      self.counts.data_ptr(), self.capacity, self.boundary.data_ptr(),
+                      self.table_ptr, self.lj.ntypes, 0 if thermo else _lib.FORCE_SKIP_THERMO,
+                      a["force"].data_ptr(), self.virial.data_ptr(), self.status.data_ptr(),
+                      self.stream)
+            self.kernel_launches += 1
+            return
         _lib.call("b2md_force_lj", a["pos_hi"].data_ptr(), self.n_own, ctypes.byref(self.box),
                   self.nbr.data_ptr(), self.counts.data_ptr(), self.capacity, self.nbr.shape[0],
                   self.boundary.data_ptr(), self.table_ptr, self.lj.ntypes,
