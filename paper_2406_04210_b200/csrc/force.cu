@@ -466,7 +466,9 @@ struct PackAcc {
     int cnt_a, cnt_b;
 };
 
-template <int AXES, bool THERMO>
+// SIG1: sigma^2 == 1.0f, so s2 = sigma^2 * ir2 is ir2 itself (x * 1.0f is exact: same bits,
+// one packed multiply less on the FMA pipe that bounds this kernel).
+template <int AXES, bool THERMO, bool SIG1>
 __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 ay, f32x2 az,
                                                   int e, const float4 pj, const ForceArgs &a) {
     const BoxF &b = a.box;
@@ -479,7 +481,7 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
     upk(r2, r2a, r2b);
     const float ia = masked_rcp(r2a, p.rc2, e, 1), ib = masked_rcp(r2b, p.rc2, e, 2);
     const f32x2 ir2 = pk(ia, ib);
-    const f32x2 s2 = mul2(pk1(p.sig2), ir2);
+    const f32x2 s2 = SIG1 ? ir2 : mul2(pk1(p.sig2), ir2);
     const f32x2 s6 = mul2(mul2(s2, s2), s2);
     const f32x2 t = mul2(s6, fma2(pk1(2.0f), s6, pk1(-1.0f)));
     const f32x2 g = mul2(t, ir2);
@@ -497,7 +499,7 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
 
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
-template <int AXES, bool TABLE, bool THERMO>
+template <int AXES, bool TABLE, bool THERMO, bool SIG1>
 __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4 pa,
                                               const float4 pb, int tiles,
                                               const int4 *__restrict__ col, int64_t pair_pitch,
@@ -507,9 +509,9 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     // The loop body is kept to one trip: unrolling it further (to rotate the tile
     // registers without moves) made instruction fetch the limiter -- 30 % of the
     // stall samples were "no instruction".
-    const int4 zero = make_int4(0, 0, 0, 0);
-    int4 e0 = tiles > 0 ? __ldcs(col) : zero;
-    int4 e1 = tiles > 1 ? __ldcs(col + pair_pitch) : zero;
+    int4 e0 = make_int4(0, 0, 0, 0), e1 = e0;
+    if (tiles > 0) e0 = __ldcs(col);
+    if (tiles > 1) e1 = __ldcs(col + pair_pitch);
     col += 2 * pair_pitch;
     PackAcc acc = {0ull, 0ull, 0ull, 0ull, 0ull, 0, 0};     // +0.0f in both halves
     const f32x2 ax = pk(pa.x, pb.x), ay = pk(pa.y, pb.y), az = pk(pa.z, pb.z);
@@ -517,7 +519,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     for (int q = 0; q < tiles; ++q) {
         const int ev[4] = {e0.x, e0.y, e0.z, e0.w};
         e0 = e1;
-        e1 = (q + 2 < tiles) ? __ldcs(col) : zero;      // warp-uniform
+        if (q + 2 < tiles) e1 = __ldcs(col);            // warp-uniform; a stale e1 is never used
         col += pair_pitch;
         float4 pj[4];
 #pragma unroll
@@ -528,7 +530,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
                 pair_entry<AXES, TABLE, THERMO>(A, B, pa, pb, ev[u], pj[u], a, s_tab_a, s_tab_b,
                                                 ta_row, tb_row);
             else
-                pair_entry_packed<AXES, THERMO>(acc, ax, ay, az, ev[u], pj[u], a);
+                pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, ev[u], pj[u], a);
         }
     }
     if (!TABLE) {
@@ -542,7 +544,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     }
 }
 
-template <bool TABLE, bool THERMO>
+template <bool TABLE, bool THERMO, bool SIG1>
 __global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
@@ -579,8 +581,8 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
 
     RowAcc A = {0.f, 0.f, 0.f, 0.f, 0.f, 0}, B = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
 #define B2MD_PAIR_LOOP(AXES)                                                                  \
-    pair_row_loop<AXES, TABLE, THERMO>(A, B, pa, pb, tiles, col, pair_pitch, pos, a, s_tab_a,  \
-                                       s_tab_b, ta_row, tb_row)
+    pair_row_loop<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch, pos, a,    \
+                                             s_tab_a, s_tab_b, ta_row, tb_row)
     switch (axes) {                 // warp-uniform
         case 0: B2MD_PAIR_LOOP(0); break;
         case 1: B2MD_PAIR_LOOP(1); break;
@@ -840,8 +842,8 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
-#define B2MD_LAUNCH_PAIR(TABLE, THERMO)                                                       \
-    k_force_lj_pair<TABLE, THERMO><<<blocks, kForceThreads, 0, s>>>(                          \
+#define B2MD_LAUNCH_PAIR(TABLE, THERMO, SIG1)                                                       \
+    k_force_lj_pair<TABLE, THERMO, SIG1><<<blocks, kForceThreads, 0, s>>>(                          \
         (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
         (flags & B2MD_FORCE_GATED) ? 1 : 0)
@@ -850,12 +852,14 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
     // of the index stream, L1::no_allocate indices / L1::evict_last positions were all
     // neutral or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
+    const bool sig1 = a.single.sig2 == 1.0f;
     if (ntypes == 1) {
-        if (thermo) B2MD_LAUNCH_PAIR(false, true);
-        else B2MD_LAUNCH_PAIR(false, false);
+        if (thermo) B2MD_LAUNCH_PAIR(false, true, false);
+        else if (sig1) B2MD_LAUNCH_PAIR(false, false, true);
+        else B2MD_LAUNCH_PAIR(false, false, false);
     } else {
-        if (thermo) B2MD_LAUNCH_PAIR(true, true);
-        else B2MD_LAUNCH_PAIR(true, false);
+        if (thermo) B2MD_LAUNCH_PAIR(true, true, false);
+        else B2MD_LAUNCH_PAIR(true, false, false);
     }
 #undef B2MD_LAUNCH_PAIR
     B2MD_CHECK_LAUNCH("b2md_force_lj_pairs");
