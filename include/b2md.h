@@ -216,6 +216,29 @@ int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
                         int32_t ntypes, int32_t flags, void *d_force_f4, float *d_virial,
                         b2md_status *d_status, void *stream);
 
+/* One launch per intermediate MD step: b2md_force_lj_pairs followed, for every
+ * particle and inside the same kernel, by what b2md_vv_finalize_integrate would do
+ * with the forces just computed (vv_finalize of this step + vv_integrate of the next,
+ * integrate.py:58-79, wrap and image counters core.py:72-93, displacement check
+ * neighbor.py:243-254) -- the forces never travel through HBM and are NOT stored.
+ * Position high words are read from d_pos_hi by all threads and the advanced ones
+ * written to d_pos_hi_out (a different buffer, same layout; the caller swaps);
+ * d_pos_lo, d_vel, d_image_i4 and d_ref_pos_f4 are updated in place.
+ * Gating: the launch returns at once when int32 word `gate_in_word` of *d_status is
+ * non-zero (the positions it would use already need a new list), and sets word
+ * `gate_out_word` when the positions it produces do; the two must differ (5 =
+ * rebuild_flag, 12 = reserved[0]).  This makes a speculative launch safe: the host
+ * reads the flag while the kernel is already queued. */
+int b2md_force_lj_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
+                                void *d_vel, void *d_image_i4, int64_t n, const b2md_box *box,
+                                double dt, void *d_ref_pos_f4, double half_skin2,
+                                const int32_t *d_pair_nbr, const int32_t *d_pair_counts,
+                                int64_t pair_pitch, const int32_t *d_nbr,
+                                const int32_t *d_counts, int64_t pitch,
+                                const uint8_t *d_boundary, const double *table, int32_t ntypes,
+                                int32_t flags, int32_t gate_in_word, int32_t gate_out_word,
+                                b2md_status *d_status, void *stream);
+
 /* compute_forces_all_to_all (forces.py:129-138; kernel 29-69): shared-memory
  * tiled all-pairs scan, same outputs. */
 int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
@@ -322,6 +345,8 @@ int b2md_flag_neither(const int32_t *d_a, const int32_t *d_b, int64_t n, int32_t
  * policy of Simulation._compute_forces/_rebuild (sim.py:114-149), driven from
  * C++ so that a step costs two launches and no Python:
  *
+ *   (with pair rows and pos_hi_alt: one b2md_force_lj_pairs_advance launch per
+ *   intermediate step, gated on the rebuild flag instead of the three launches below)
  *   [finalize(s-1) + integrate(s) fused, folds the displacement check]
  *   [async 64-byte status read-back]  [force(s), launched speculatively]
  *   host looks at the flag while the force kernel runs; only if it is set:
@@ -374,6 +399,10 @@ typedef struct b2md_runner_config {
     int32_t *pair_nbr;           /* pair_rows * pair_pitch (b2md_pair_rows layout) */
     int32_t *pair_counts;        /* pair_pitch */
     int64_t pair_pitch;          /* multiple of 32 >= ceil(n/2) */
+    void *pos_hi_alt;            /* float4[capacity]: second buffer for the position high words;
+                                    with pair rows it lets the intermediate steps run as ONE
+                                    kernel each (b2md_force_lj_pairs_advance); NULL = separate
+                                    integrate and force launches */
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };

@@ -69,6 +69,7 @@ class RunnerConfig(Structure):
         ("status", c_void_p), ("stream", c_void_p),
         ("use_graph", c_int32), ("pair_rows", c_int32),
         ("pair_nbr", c_void_p), ("pair_counts", c_void_p), ("pair_pitch", c_int64),
+        ("pos_hi_alt", c_void_p),
     ]
 
 
@@ -127,6 +128,10 @@ _SIGNATURES = {
     "b2md_pair_rows": (c_int32, [_P, _P, c_int64, c_int32, c_int64, _P, _P, c_int64, c_int32, _P]),
     "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
                                       _P, POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
+    "b2md_force_lj_pairs_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double,
+                                              _P, c_double, _P, _P, c_int64, _P, _P, c_int64, _P,
+                                              POINTER(c_double), c_int32, c_int32, c_int32,
+                                              c_int32, _P, _P]),
     "b2md_force_lj_all_pairs": (c_int32, [_P, c_int64, POINTER(Box), POINTER(c_double), c_int32,
                                           _P, _P, _P, _P]),
     "b2md_vv_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,

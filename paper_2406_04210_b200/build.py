@@ -40,7 +40,7 @@ def is_stale() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
     built = os.path.getmtime(LIB_PATH)
-    deps = sources() + [os.path.join(CSRC, "common.cuh"),
+    deps = sources() + [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "integrate.cuh"),
                         os.path.join(HERE, "..", "include", "b2md.h")]
     return any(os.path.getmtime(d) > built for d in deps if os.path.exists(d))
 

@@ -30,6 +30,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "integrate.cuh"
 
 namespace b2md {
 
@@ -544,17 +545,38 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     }
 }
 
-template <bool TABLE, bool THERMO, bool SIG1>
+// ADVANCE: the kernel also applies what the step loop does between two force
+// evaluations -- both half-kicks with the forces it has just computed, the drift, the
+// wrap and the displacement check (= k_integrate<2>) -- so the intermediate steps of
+// the native loop are ONE launch each and the forces never travel through HBM.
+// Positions are read by other threads while this one moves on, hence the new high
+// words go to a second buffer (pos_out) that the next launch reads; velocities, low
+// words, images and the list snapshot are private to the thread and updated in place.
+// The launch is gated on status word `gate_in` ("the positions I am about to use
+// already need a new list": set by the previous launch, which wrote `gate_out` of its
+// own) -- a launch enqueued speculatively then returns at once and the host rebuilds.
+struct AdvanceArgs {
+    float4 *pos_out, *pos_lo, *vel, *ref_pos;
+    int4 *image;
+    StepConst step;
+    int gate_in, gate_out;        // int32 word indices into b2md_status
+};
+
+template <bool TABLE, bool THERMO, bool SIG1, bool ADVANCE>
 __global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
                 int64_t pair_pitch, const int32_t *__restrict__ nbr,
                 const int32_t *__restrict__ counts, int64_t pitch,
                 const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
-                float *__restrict__ virial, b2md_status *status, int gated) {
+                float *__restrict__ virial, b2md_status *status, int gated,
+                const __grid_constant__ AdvanceArgs adv) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float s_max[kForceThreads / 32];
+    // step-graph batches: nothing to do once an in-graph list build overflowed
     if (gated && *(volatile int *)&status->frozen) return;
+    if (ADVANCE && ((volatile int *)status)[adv.gate_in]) return;
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -591,26 +613,49 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
         default: B2MD_PAIR_LOOP(7); break;
     }
 #undef B2MD_PAIR_LOOP
-    if (!active) return;
+    float d2 = 0.0f;
+    if (active) {
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-        if (which == 1 && !has_b) break;
-        const RowAcc &acc = which ? B : A;
-        const int64_t i = which ? ib : ia;
-        float fx, fy, fz, u, w;
-        if (TABLE) {
-            fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
-        } else {
-            const PairParams &p = a.single;
-            fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
-            u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
-            w = p.c_w * acc.w;
+        for (int which = 0; which < 2; ++which) {
+            if (which == 1 && !has_b) break;
+            const RowAcc &acc = which ? B : A;
+            const int64_t i = which ? ib : ia;
+            float fx, fy, fz, u, w;
+            if (TABLE) {
+                fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
+            } else {
+                const PairParams &p = a.single;
+                fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+                u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
+                w = p.c_w * acc.w;
+            }
+            if (ADVANCE) {
+                float4 h = which ? pb : pa;
+                d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo,
+                                                   adv.vel, adv.image, adv.step, adv.ref_pos));
+                adv.pos_out[i] = h;
+            } else {
+                force[i] = make_float4(fx, fy, fz, u);
+                if (THERMO && virial) virial[i] = w;
+            }
+            if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
+                report_singular((int)i, which ? pb : pa, counts[i], nbr + i, pitch, pos, a.box,
+                                status);
         }
-        force[i] = make_float4(fx, fy, fz, u);
-        if (THERMO && virial) virial[i] = w;
-        if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-            report_singular((int)i, which ? pb : pa, counts[i], nbr + i, pitch, pos, a.box,
-                            status);
+    }
+    if (ADVANCE) {
+        // displacement maximum of the block -> status (as k_integrate does)
+        d2 = warp_max(d2);
+        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+            m = warp_max(m);
+            if (threadIdx.x == 0 && m > 0.0f) {
+                atomicMax(&status->max_disp2_bits, __float_as_uint(m));
+                if (m > adv.step.half_skin2) ((int *)status)[adv.gate_out] = 1;
+            }
+        }
     }
 }
 
@@ -825,16 +870,17 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     return 0;
 }
 
-B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
-                                    const int32_t *d_pair_nbr, const int32_t *d_pair_counts,
-                                    int64_t pair_pitch, const int32_t *d_nbr,
-                                    const int32_t *d_counts, int64_t pitch,
-                                    const uint8_t *d_boundary, const double *table,
-                                    int32_t ntypes, int32_t flags, void *d_force_f4,
-                                    float *d_virial, b2md_status *d_status, void *stream) {
+namespace {
+
+int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int32_t *d_pair_nbr,
+                 const int32_t *d_pair_counts, int64_t pair_pitch, const int32_t *d_nbr,
+                 const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+                 const double *table, int32_t ntypes, int32_t flags, void *d_force_f4,
+                 float *d_virial, b2md_status *d_status, const AdvanceArgs *advance, void *stream,
+                 const char *name) {
     if (n <= 0 || !d_pair_nbr || !d_pair_counts || !d_nbr || !d_counts || !d_status ||
         pair_pitch < (n + 1) / 2) {
-        set_error("b2md_force_lj_pairs: bad arguments");
+        set_error("%s: bad arguments", name);
         return -1;
     }
     ForceArgs a;
@@ -842,26 +888,76 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
-#define B2MD_LAUNCH_PAIR(TABLE, THERMO, SIG1)                                                       \
-    k_force_lj_pair<TABLE, THERMO, SIG1><<<blocks, kForceThreads, 0, s>>>(                          \
+    AdvanceArgs adv = {};
+    if (advance) adv = *advance;
+#define B2MD_LAUNCH_PAIR(TABLE, THERMO, SIG1, ADVANCE)                                        \
+    k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE><<<blocks, kForceThreads, 0, s>>>(           \
         (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
-        (flags & B2MD_FORCE_GATED) ? 1 : 0)
-    // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 7, 9,
-    // 10 or 12 CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch
-    // of the index stream, L1::no_allocate indices / L1::evict_last positions were all
-    // neutral or slower.
+        (flags & B2MD_FORCE_GATED) ? 1 : 0, adv)
+    // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 4 to 12
+    // CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch of the
+    // index stream, L1 cache-policy hints, per-SM or per-warp work queues were all neutral
+    // or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
     const bool sig1 = a.single.sig2 == 1.0f;
-    if (ntypes == 1) {
-        if (thermo) B2MD_LAUNCH_PAIR(false, true, false);
-        else if (sig1) B2MD_LAUNCH_PAIR(false, false, true);
-        else B2MD_LAUNCH_PAIR(false, false, false);
+    if (advance) {
+        if (ntypes == 1) {
+            if (sig1) B2MD_LAUNCH_PAIR(false, false, true, true);
+            else B2MD_LAUNCH_PAIR(false, false, false, true);
+        } else {
+            B2MD_LAUNCH_PAIR(true, false, false, true);
+        }
+    } else if (ntypes == 1) {
+        if (thermo) B2MD_LAUNCH_PAIR(false, true, false, false);
+        else if (sig1) B2MD_LAUNCH_PAIR(false, false, true, false);
+        else B2MD_LAUNCH_PAIR(false, false, false, false);
     } else {
-        if (thermo) B2MD_LAUNCH_PAIR(true, true, false);
-        else B2MD_LAUNCH_PAIR(true, false, false);
+        if (thermo) B2MD_LAUNCH_PAIR(true, true, false, false);
+        else B2MD_LAUNCH_PAIR(true, false, false, false);
     }
 #undef B2MD_LAUNCH_PAIR
-    B2MD_CHECK_LAUNCH("b2md_force_lj_pairs");
-    return 0;
+    int rc2 = check_cuda(cudaPeekAtLastError(), name);
+    return rc2;
+}
+
+}  // namespace
+
+B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                                    const int32_t *d_pair_nbr, const int32_t *d_pair_counts,
+                                    int64_t pair_pitch, const int32_t *d_nbr,
+                                    const int32_t *d_counts, int64_t pitch,
+                                    const uint8_t *d_boundary, const double *table,
+                                    int32_t ntypes, int32_t flags, void *d_force_f4,
+                                    float *d_virial, b2md_status *d_status, void *stream) {
+    return launch_pairs(d_pos_hi, n, box, d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts,
+                        pitch, d_boundary, table, ntypes, flags, d_force_f4, d_virial, d_status,
+                        nullptr, stream, "b2md_force_lj_pairs");
+}
+
+B2MD_EXPORT int b2md_force_lj_pairs_advance(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
+    int32_t gate_out_word, b2md_status *d_status, void *stream) {
+    if (!d_pos_hi_out || d_pos_hi_out == d_pos_hi || !d_pos_lo || !d_vel || !d_image_i4 ||
+        !d_ref_pos_f4 || !(dt > 0.0) || gate_in_word == gate_out_word || gate_in_word < 0 ||
+        gate_in_word >= 16 || gate_out_word < 0 || gate_out_word >= 16) {
+        set_error("b2md_force_lj_pairs_advance: bad arguments");
+        return -1;
+    }
+    AdvanceArgs adv;
+    adv.pos_out = (float4 *)d_pos_hi_out;
+    adv.pos_lo = (float4 *)d_pos_lo;
+    adv.vel = (float4 *)d_vel;
+    adv.ref_pos = (float4 *)d_ref_pos_f4;
+    adv.image = (int4 *)d_image_i4;
+    adv.step = make_step(box, dt, half_skin2);
+    adv.gate_in = gate_in_word;
+    adv.gate_out = gate_out_word;
+    return launch_pairs(d_pos_hi, n, box, d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts,
+                        pitch, d_boundary, table, ntypes, flags | B2MD_FORCE_SKIP_THERMO, nullptr,
+                        nullptr, d_status, &adv, stream, "b2md_force_lj_pairs_advance");
 }

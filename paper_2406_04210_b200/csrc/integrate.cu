@@ -11,54 +11,11 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "integrate.cuh"
 
 namespace b2md {
 
 constexpr int kThreads = 256;
-
-struct StepConst {
-    float L_hi[3], L_lo[3], invL[3];
-    float dt_hi, dt_lo, half_dt;
-    float half_skin2;
-};
-
-// x (double-single) into [0, L): k = floor(x/L) with the reference's nudges
-// (core.py:81-93); returns k.
-__device__ __forceinline__ int wrap_ds(float &hi, float &lo, float L_hi, float L_lo, float invL) {
-    if (hi >= 0.0f && hi < L_hi) return 0;          // common case (hi == L_hi handled below)
-    float kf = floorf(hi * invL);
-    if (kf != 0.0f) {
-        // (hi, lo) -= k * (L_hi + L_lo), product formed error-free
-        const float ph = kf * L_hi;
-        const float pl = fmaf(kf, L_hi, -ph) + kf * L_lo;
-        ds_add(hi, lo, -ph, -pl);
-    }
-    // value < 0 ?
-    if (hi < 0.0f || (hi == 0.0f && lo < 0.0f)) {
-        ds_add(hi, lo, L_hi, L_lo);
-        kf -= 1.0f;
-    }
-    // value >= L ?
-    if (hi > L_hi || (hi == L_hi && lo >= L_lo)) {
-        ds_add(hi, lo, -L_hi, -L_lo);
-        kf += 1.0f;
-    }
-    return (int)kf;
-}
-
-__device__ __forceinline__ void kick(float4 &v, const float4 f, float half_dt) {
-    // v += (f / m) * (0.5*dt): divide, then multiply (integrate.py:64,79)
-    const float m = v.w;
-    v.x = __fadd_rn(v.x, __fmul_rn(__fdiv_rn(f.x, m), half_dt));
-    v.y = __fadd_rn(v.y, __fmul_rn(__fdiv_rn(f.y, m), half_dt));
-    v.z = __fadd_rn(v.z, __fmul_rn(__fdiv_rn(f.z, m), half_dt));
-}
-
-__device__ __forceinline__ void drift(float &hi, float &lo, float v, float dt_hi, float dt_lo) {
-    const float ph = v * dt_hi;
-    const float pl = fmaf(v, dt_lo, fmaf(v, dt_hi, -ph));   // exact product tail
-    ds_add(hi, lo, ph, pl);
-}
 
 template <int KICKS, bool GATED>
 __global__ void __launch_bounds__(kThreads)
@@ -71,38 +28,9 @@ k_integrate(float4 *__restrict__ pos_hi, float4 *__restrict__ pos_lo, float4 *__
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     float d2 = 0.0f;
     if (i < n) {
-        float4 v = vel[i];
-        const float4 f = force[i];
-#pragma unroll
-        for (int k = 0; k < KICKS; ++k) kick(v, f, c.half_dt);
-        vel[i] = v;
-        float4 h = pos_hi[i], l = pos_lo[i];
-        drift(h.x, l.x, v.x, c.dt_hi, c.dt_lo);
-        drift(h.y, l.y, v.y, c.dt_hi, c.dt_lo);
-        drift(h.z, l.z, v.z, c.dt_hi, c.dt_lo);
-        const int kx = wrap_ds(h.x, l.x, c.L_hi[0], c.L_lo[0], c.invL[0]);
-        const int ky = wrap_ds(h.y, l.y, c.L_hi[1], c.L_lo[1], c.invL[1]);
-        const int kz = wrap_ds(h.z, l.z, c.L_hi[2], c.L_lo[2], c.invL[2]);
+        float4 h = pos_hi[i];
+        d2 = advance_particle<KICKS>(i, h, force[i], pos_lo, vel, image, c, ref_pos);
         pos_hi[i] = h;
-        pos_lo[i] = l;
-        const bool wrapped = (kx | ky | kz) != 0;
-        if (wrapped) {
-            int4 im = image[i];
-            im.x += kx; im.y += ky; im.z += kz;
-            image[i] = im;
-        }
-        if (ref_pos) {
-            float4 r = ref_pos[i];
-            if (wrapped) {
-                // keep (hi - ref) equal to the unwrapped displacement
-                r.x = fmaf(-(float)kx, c.L_hi[0], r.x);
-                r.y = fmaf(-(float)ky, c.L_hi[1], r.y);
-                r.z = fmaf(-(float)kz, c.L_hi[2], r.z);
-                ref_pos[i] = r;
-            }
-            const float dx = h.x - r.x, dy = h.y - r.y, dz = h.z - r.z;
-            d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        }
     }
     if (ref_pos) {
         d2 = warp_max(d2);
@@ -127,22 +55,6 @@ k_finalize(float4 *__restrict__ vel, const float4 *__restrict__ force, int64_t n
     float4 v = vel[i];
     kick(v, force[i], half_dt);
     vel[i] = v;
-}
-
-static StepConst make_step(const b2md_box *box, double dt, double half_skin2) {
-    StepConst c;
-    for (int a = 0; a < 3; ++a) {
-        c.L_hi[a] = (float)box->edge[a];
-        c.L_lo[a] = (float)(box->edge[a] - (double)c.L_hi[a]);
-        c.invL[a] = (float)(1.0 / box->edge[a]);
-    }
-    c.dt_hi = (float)dt;
-    c.dt_lo = (float)(dt - (double)c.dt_hi);
-    c.half_dt = (float)(0.5 * dt);
-    // never fire later than the exact fp64 test: shave the fp32 rounding of the
-    // snapshot and of the squared norm off the threshold
-    c.half_skin2 = (float)(half_skin2 * (1.0 - 1e-5));
-    return c;
 }
 
 template <int KICKS, bool GATED = false>

@@ -52,6 +52,10 @@ struct b2md_runner {
     int steps_per_graph;
     int64_t graph_launch_kernels;   // kernels per step in the always-executed part
     int64_t graph_rebuild_kernels;  // kernels inside one conditional body
+    // one-launch steps (b2md_force_lj_pairs_advance)
+    void *pos_cur;            // where the live position high words are (canonical or alt)
+    bool ahead;               // positions already advanced to the step about to be processed
+    int gate_in;              // status word holding the rebuild flag of those positions
 };
 
 namespace {
@@ -111,6 +115,40 @@ int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
     return b2md_force_lj(a.pos_hi, c.n, &c.box, c.nbr, c.counts, c.pitch, stride_rows(r),
                          c.boundary, r->table.data(), c.ntypes, flags, a.force, a.virial,
                          c.status, r->stream);
+}
+
+constexpr int kWordRebuildFlag = 5;   // b2md_status::rebuild_flag
+constexpr int kWordAltFlag = 12;      // b2md_status::reserved[0]
+
+bool can_advance(const b2md_runner *r) {
+    const b2md_runner_config &c = r->cfg;
+    return c.pos_hi_alt != nullptr && c.pair_rows > 0 && c.use_graph == 0;
+}
+
+// The canonical buffer of the live set holds the position high words again.
+int canonicalize(b2md_runner *r) {
+    Set a = live(r);
+    if (r->pos_cur == nullptr || r->pos_cur == a.pos_hi) { r->pos_cur = a.pos_hi; return 0; }
+    int rc = check_cuda(cudaMemcpyAsync(a.pos_hi, r->pos_cur, 16 * (size_t)r->cfg.n,
+                                        cudaMemcpyDeviceToDevice, r->stream), "position copy");
+    r->pos_cur = a.pos_hi;
+    return rc;
+}
+
+// force(s) + finalize(s) + integrate(s+1) in one launch, gated on the rebuild flag of
+// the positions it reads; the advanced high words go to the other buffer.
+int launch_advance(b2md_runner *r) {
+    const b2md_runner_config &c = r->cfg;
+    Set a = live(r);
+    void *in = r->pos_cur ? r->pos_cur : a.pos_hi;
+    void *out = in == a.pos_hi ? c.pos_hi_alt : a.pos_hi;
+    const int gate_out = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+    r->launches += 1;
+    return b2md_force_lj_pairs_advance(in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt,
+                                       c.ref_pos, r->half_skin2, c.pair_nbr, c.pair_counts,
+                                       c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
+                                       r->table.data(), c.ntypes, 0, r->gate_in, gate_out,
+                                       c.status, r->stream);
 }
 
 int reorder_key_bits(const b2md_runner *r) {
@@ -210,6 +248,7 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
     rep->max_count = r->h_status->max_count;
     rep->n_boundary = r->h_status->n_boundary;
     r->list_valid = r->h_status->overflow == 0;
+    r->pos_cur = live(r).pos_hi;      // callers hand over canonical positions; sets may swap
     return 0;
 }
 
@@ -315,60 +354,101 @@ int order_after_caller(b2md_runner *r) {
 }
 
 // One ungraphed step.  *stop = 1 when the call must return (overflow / singular).
+// With pair rows and a second position buffer the intermediate (unobservable) steps are
+// one gated launch each: force(s) + finalize(s) + integrate(s+1) + displacement check.
 int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before, int *stop) {
     const b2md_runner_config &c = r->cfg;
     cudaStream_t s = r->stream;
     Set a = live(r);
     int rc;
     *stop = 0;
-    if (r->pending_kick)
-        rc = b2md_vv_finalize_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box,
-                                        c.dt, c.ref_pos, r->half_skin2, c.status, s);
-    else
-        rc = b2md_vv_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
-                               c.ref_pos, r->half_skin2, c.status, s);
-    if (rc) return rc;
-    r->launches += 1;
+    const bool fuse = can_advance(r) && !thermo;
+    if (!r->ahead) {
+        // positions of this step: integrate in place (canonical buffer)
+        if ((rc = canonicalize(r))) return rc;
+        if (r->pending_kick)
+            rc = b2md_vv_finalize_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n,
+                                            &c.box, c.dt, c.ref_pos, r->half_skin2, c.status, s);
+        else
+            rc = b2md_vv_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n, &c.box, c.dt,
+                                   c.ref_pos, r->half_skin2, c.status, s);
+        if (rc) return rc;
+        r->launches += 1;
+        r->gate_in = kWordRebuildFlag;
+    }
     r->pending_kick = false;
+    // a force evaluation that is observable reads the canonical buffer
+    if (!fuse && (rc = canonicalize(r))) return rc;
     if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
                                          cudaMemcpyDeviceToHost, s), "flag read-back"))) return rc;
     if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
-    // Launch the force kernel before the flag is known -- unless the displacement
-    // was already close to the threshold one step ago, in which case a rebuild is
-    // likely and waiting a few microseconds beats discarding a force evaluation.
-    const bool speculate = r->last_disp2 < 0.85 * r->half_skin2;
-    if (speculate && (rc = launch_force(r, thermo))) return rc;
+    // Launch the force kernel before the flag is known.  The one-launch step gates
+    // itself on the flag; the plain force kernel is skipped when the displacement was
+    // already close to the threshold one step ago (a rebuild is likely and waiting a few
+    // microseconds beats discarding a force evaluation).
+    const bool speculate = fuse || r->last_disp2 < 0.85 * r->half_skin2;
+    if (fuse) rc = launch_advance(r);
+    else if (speculate) rc = launch_force(r, thermo);
+    if (rc) return rc;
     if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
     rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
     r->last_disp2 = rep->max_disp2;
     if (r->h_status->singular != ~0ull) {
         // a force evaluation of an earlier step met a coincident pair
         // (forces.py:113-116); stop after draining the stream
+        if (fuse) {
+            // the queued launch advanced the particles: leave the canonical buffer current
+            Set now = live(r);
+            void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
+            r->pos_cur = in == now.pos_hi ? c.pos_hi_alt : now.pos_hi;
+            r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+            r->ahead = true;
+            if ((rc = canonicalize(r))) return rc;
+        }
         if ((rc = read_status(r))) return rc;
         rep->singular = r->h_status->singular;
         rep->reason = B2MD_RUN_SINGULAR;
-        r->pending_kick = true;
+        r->pending_kick = !fuse;
         rep->steps_done += 1;
         finish_report(r, rep, before);
         *stop = 1;
         return 0;
     }
-    if (r->h_status->rebuild_flag) {
-        if (speculate) rep->wasted_force_launches += 1;
+    const bool need_rebuild = reinterpret_cast<const int32_t *>(r->h_status)[r->gate_in] != 0;
+    if (need_rebuild) {
+        if (!fuse && speculate) rep->wasted_force_launches += 1;   // (a gated launch did nothing)
+        if ((rc = canonicalize(r))) return rc;
         if ((rc = rebuild(r, rep))) return rc;
+        r->pos_cur = live(r).pos_hi;          // a reorder may have swapped the sets
+        r->gate_in = kWordRebuildFlag;        // both flag words were cleared
         r->last_disp2 = 0.0;
         if (!r->list_valid) {
             r->mid_step = true;
+            r->ahead = false;
             rep->reason = B2MD_RUN_OVERFLOW;
             finish_report(r, rep, before);
             *stop = 1;
             return 0;
         }
-        if ((rc = launch_force(r, thermo))) return rc;
+        if (fuse) rc = launch_advance(r);
+        else rc = launch_force(r, thermo);
+        if (rc) return rc;
     } else if (!speculate) {
         if ((rc = launch_force(r, thermo))) return rc;
     }
-    r->pending_kick = true;
+    if (fuse) {
+        // the launch advanced the particles to the next step: its output buffer and its
+        // output flag word are the inputs of the next one
+        Set now = live(r);
+        void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
+        r->pos_cur = in == now.pos_hi ? c.pos_hi_alt : now.pos_hi;
+        r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+        r->ahead = true;
+        r->pending_kick = false;
+    } else {
+        r->ahead = false;
+        r->pending_kick = true;
+    }
     rep->steps_done += 1;
     return 0;
 }
@@ -465,6 +545,9 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->graph[0] = r->graph[1] = nullptr;
     r->graph_exec[0] = r->graph_exec[1] = nullptr;
     r->steps_per_graph = cfg->use_graph > 1 ? cfg->use_graph : 1;
+    r->pos_cur = nullptr;
+    r->ahead = false;
+    r->gate_in = kWordRebuildFlag;
     r->h_status = nullptr;
     r->ev = r->ev_in = nullptr;
     r->stream = nullptr;

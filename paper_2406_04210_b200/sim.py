@@ -22,6 +22,7 @@ unaffected); ``lj`` may be a :class:`PairTable` (Kob-Andersen etc.).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 
 import numpy as np
@@ -61,7 +62,7 @@ class Simulation:
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
                  stride_policy: str = "fit", graph: int | bool = False,
-                 pair_rows: bool | None = None):
+                 pair_rows: bool | None = None, advance: bool | None = None):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -91,6 +92,9 @@ class Simulation:
         self.graph = int(graph)          # MD steps per captured CUDA graph (0 = host-driven)
         # force kernel: one thread per particle pair over merged rows (None = by size)
         self.pair_rows = use_pair_rows(state.n, pair_rows)
+        # one-launch intermediate steps (needs pair rows; B2MD_ADVANCE=0 turns them off)
+        self.advance = (os.environ.get("B2MD_ADVANCE", "1") != "0") if advance is None \
+            else bool(advance)
         self.graph_steps = 0
         # the thermostat acts between finalize and the next integrate: operator loop
         self.native = (force_mode == TRUNCATED and not thermostatted) if native is None \
@@ -272,6 +276,11 @@ class Simulation:
         cfg.stream = dev.stream
         cfg.use_graph = self.graph
         if self.pair_rows:
+            # second buffer for the position high words: intermediate steps then run as one
+            # launch each (force + finalize + integrate, b2md_force_lj_pairs_advance)
+            if self.advance:
+                k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
+                cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
             k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
             k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
             cfg.pair_nbr = k["pair_nbr"].data_ptr()

@@ -144,3 +144,49 @@ def test_stride_growth_reallocates_pair_rows():
     e0 = sim.measure().total_energy
     sim.run(50)
     assert abs(sim.measure().total_energy - e0) <= 1e-4 * abs(e0)
+
+
+@pytest.mark.parametrize("n,steps", [(4096, 400), (262_144, 150)])
+def test_one_launch_steps_are_bit_identical_to_separate_launches(n, steps):
+    """b2md_force_lj_pairs_advance applies the same kicks / drift / wrap to the same fp32
+    forces as the separate integrate launch would: identical trajectories, energies,
+    image counters and rebuild schedule."""
+    out = []
+    for advance in (False, True):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 1.2, 42)
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001,
+                            force_mode=b2.TRUNCATED, skin=0.3, sample_interval=37,
+                            sample_initial=True, pair_rows=True, advance=advance)
+        sim.run(steps)
+        sim.run(3)                       # a short call: first / last step handling
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    np.array(st.velocities.acquire_read(b2.HOST)),
+                    np.array(st.images.acquire_read(b2.HOST)),
+                    np.array(st.forces.acquire_read(b2.HOST)), sim.rebuild_count,
+                    sim.kernel_launches))
+    assert out[0][5] == out[1][5] and out[0][5] >= 3
+    for k in range(5):
+        assert np.array_equal(out[0][k], out[1][k]), k
+    assert out[1][6] < 0.8 * out[0][6]          # one launch per intermediate step instead of two
+
+
+def test_one_launch_steps_survive_stride_growth_and_wraps():
+    # stride 64 overflows on the fcc start; dt large enough that particles cross faces
+    n = 8192
+    out = []
+    for advance in (False, True):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 2.0, 7)
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.004,
+                            force_mode=b2.TRUNCATED, skin=0.3, stride=64, sample_interval=50,
+                            pair_rows=True, advance=advance)
+        sim.run(500)
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    np.array(st.images.acquire_read(b2.HOST)), sim.rebuild_count))
+    assert np.abs(out[0][2]).max() >= 1                       # some particle wrapped
+    assert out[0][3] == out[1][3]
+    for k in range(3):
+        assert np.array_equal(out[0][k], out[1][k]), k

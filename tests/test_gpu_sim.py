@@ -137,7 +137,7 @@ def test_nve_energy_conservation_n4096():
     assert 15 <= sim.rebuild_count <= 40      # reference: 24 per 1000 steps
     p = np.array(sim.samples[-1].total_momentum)
     assert np.max(np.abs(p)) <= 1e-2
-    assert sim.kernel_launches >= 2000
+    assert sim.kernel_launches >= 1000      # >= one launch per step (two without pair rows)
     sim.close()
 
 
