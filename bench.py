@@ -292,12 +292,42 @@ def run_gpu_arm(args):
                   ref_scratch.data_ptr(), 1e30, dev.status.data_ptr(), dev.stream)
 
     integ_ms = time_kernel(launch_integrate, 50, torch, stream)
+    if sim.pair_rows and sim.advance:
+        # the one-launch step: force + finalize + integrate + displacement check (scratch
+        # copies of everything it updates in place, its own status block)
+        scratch_status = torch.zeros(16, dtype=torch.int32, device=dev.pos_hi.device)
+        scratch_out = torch.empty_like(dev.pos_hi)
+        cfg = k["cfg"]
+
+        def launch_advance():
+            _lib.call("b2md_force_lj_pairs_advance", dev.pos_hi.data_ptr(), scratch_out.data_ptr(),
+                      scratch_state["pos_lo"].data_ptr(), scratch_state["vel"].data_ptr(),
+                      scratch_state["image"].data_ptr(), n, box.c_box(), 1e-9,
+                      ref_scratch.data_ptr(), 1e30, k["pair_nbr"].data_ptr(),
+                      k["pair_counts"].data_ptr(), cfg.pair_pitch, k["nbr"].data_ptr(),
+                      k["counts"].data_ptr(), k["pitch"], k["boundary"].data_ptr(), tab_ptr, 1, 0,
+                      12, 13, scratch_status.data_ptr(), dev.stream)
+        adv_ms = time_kernel(launch_advance, 30, torch, stream)
+        # SURVEY 8(d) rows it replaces: integrate 128 + force 32+4c (no-thermo) + finalize 48,
+        # minus the 80 B per particle of force / velocity traffic that fusion makes unnecessary
+        # (force written once and read twice, velocities written and re-read between the kicks)
+        adv_bytes = n * (128.0 + 4.0 * cbar)
+        # this is the kernel 98 % of the steps launch: it becomes the roofline entry, the
+        # plain force kernel (first / last step of a call, sample steps) moves to the list
+        extra_kernels["k_force_lj_pair (force only: first / last step of a call)"] = {
+            "launch_ms": force_ms, "algorithmic_bytes_per_launch": force_bytes,
+            "achieved": achieved, "frac": achieved / peak}
+        force_kernel = "k_force_lj_pair<ADVANCE> (force + finalize + integrate: one launch per MD step)"
+        force_ms, force_bytes = adv_ms, adv_bytes
+        achieved = adv_bytes / (adv_ms * 1e-3) / 1e9
     integ_bytes = n * 128.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "force_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            key = "advance" if (sim.pair_rows and sim.advance) else ("pairs" if sim.pair_rows else "rows")
+            traffic = tj.get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     step_bytes = n * (216.0 + 4.0 * cbar)

@@ -190,3 +190,22 @@ def test_one_launch_steps_survive_stride_growth_and_wraps():
     assert out[0][3] == out[1][3]
     for k in range(3):
         assert np.array_equal(out[0][k], out[1][k]), k
+
+
+def test_one_launch_steps_with_pair_tables():
+    n = 16_384
+    species = (np.random.default_rng(42).permutation(n) < n // 5).astype(np.int32)
+    out = []
+    for advance in (False, True):
+        st, box = b2.init_lattice_any(n, 1.2)
+        st = b2.ParticleState(st.positions.acquire_read(b2.HOST), species=species)
+        b2.init_velocities(st, 1.0, 42)
+        sim = b2.Simulation(st, box, b2.PairTable.kob_andersen(), 0.001,
+                            force_mode=b2.TRUNCATED, skin=0.3, sample_interval=40,
+                            sample_initial=True, pair_rows=True, advance=advance)
+        sim.run(200)
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)), sim.rebuild_count))
+    assert out[0][2] == out[1][2] and out[0][2] >= 2
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert abs(out[1][0][-1] - out[1][0][0]) <= 5e-5 * abs(out[1][0][0])
