@@ -2,11 +2,17 @@
 // compute_forces_truncated (forces.py:141-159), kernel _truncated_chunk (72-110);
 // plus the all-pairs kernel (_all_to_all_chunk, forces.py:29-69).
 //
-// One thread per particle, fp32 pair arithmetic on the position high words,
-// force / energy / virial accumulated in registers, one float4 + one float
-// store per particle.  Neighbour indices stream through the column-major list
-// (coalesced, evict-first); neighbour positions are 16-byte gathers served by
-// L1/L2 because particles are kept in Hilbert / cell order.
+// Three kernels over the same list:
+//   k_force_lj              one thread (or sub-warp) per particle over its own row --
+//                           small systems, and the reference of the bitwise tests;
+//   k_force_lj_pair         one thread per particle PAIR over the pair's merged row on
+//                           packed fp32x2 arithmetic -- large systems (n >= 200 000);
+//   k_force_lj_pair<ADVANCE> the same, then finalize + integrate + displacement check for
+//                           the particles just evaluated: one launch per MD step.
+// fp32 pair arithmetic on the position high words, force / energy / virial accumulated in
+// registers.  Neighbour indices stream through the column-major list (coalesced,
+// evict-first); neighbour positions are 16-byte gathers served by L1/L2 because particles
+// are kept in Hilbert / cell order.
 //
 // Minimum image.  A literal fp32 transcription of d - L*rint(d/L) loses ~ulp(L)
 // on pairs that interact across a periodic face (r^-13 amplifies it past the 1e-5
