@@ -44,6 +44,8 @@ struct b2md_runner {
     cudaEvent_t ev;           // flag read-back
     cudaEvent_t ev_in;        // ordering against the caller's stream
     cudaStream_t stream;      // the runner's own (capturable) stream
+    cudaStream_t copy_stream; // flag read-backs, off the kernels' critical path
+    cudaEvent_t ev_mark;      // "everything enqueued so far" for the copy stream
     int64_t launches;
     double last_disp2;        // max squared displacement seen one step ago (fp32 check)
     // step graphs: [0] = one MD step, [1] = steps_per_graph MD steps
@@ -379,9 +381,16 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     r->pending_kick = false;
     // a force evaluation that is observable reads the canonical buffer
     if (!fuse && (rc = canonicalize(r))) return rc;
+    // The 64-byte status block travels on a second stream: it waits for what is enqueued
+    // so far, but the kernel enqueued next does not wait for the copy.  (That kernel may
+    // already update the block while it is being copied: it never touches the flag word
+    // read here, and a displacement maximum that is one step ahead only feeds heuristics.)
+    if ((rc = check_cuda(cudaEventRecord(r->ev_mark, s), "mark record"))) return rc;
+    if ((rc = check_cuda(cudaStreamWaitEvent(r->copy_stream, r->ev_mark, 0), "copy wait"))) return rc;
     if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
-                                         cudaMemcpyDeviceToHost, s), "flag read-back"))) return rc;
-    if ((rc = check_cuda(cudaEventRecord(r->ev, s), "event record"))) return rc;
+                                         cudaMemcpyDeviceToHost, r->copy_stream),
+                         "flag read-back"))) return rc;
+    if ((rc = check_cuda(cudaEventRecord(r->ev, r->copy_stream), "event record"))) return rc;
     // Launch the force kernel before the flag is known.  The one-launch step gates
     // itself on the flag; the plain force kernel is skipped when the displacement was
     // already close to the threshold one step ago (a rebuild is likely and waiting a few
@@ -549,7 +558,8 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->ahead = false;
     r->gate_in = kWordRebuildFlag;
     r->h_status = nullptr;
-    r->ev = r->ev_in = nullptr;
+    r->ev = r->ev_in = r->ev_mark = nullptr;
+    r->copy_stream = nullptr;
     r->stream = nullptr;
     // in-graph rebuilds always reorder (the decision cannot depend on a host counter)
     if (r->cfg.use_graph && r->cfg.reorder_mode != 0 && r->cfg.reorder_every != 1)
@@ -558,6 +568,9 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     if (check_cuda(cudaMallocHost((void **)&r->h_status, sizeof(b2md_status)), "cudaMallocHost") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming), "cudaEventCreate") ||
+        check_cuda(cudaEventCreateWithFlags(&r->ev_mark, cudaEventDisableTiming), "cudaEventCreate") ||
+        check_cuda(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking),
+                   "cudaStreamCreate") ||
         check_cuda(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking),
                    "cudaStreamCreate")) {
         b2md_runner_destroy(r);
@@ -572,6 +585,8 @@ B2MD_EXPORT void b2md_runner_destroy(b2md_runner *r) {
     if (r->h_status) cudaFreeHost(r->h_status);
     if (r->ev) cudaEventDestroy(r->ev);
     if (r->ev_in) cudaEventDestroy(r->ev_in);
+    if (r->ev_mark) cudaEventDestroy(r->ev_mark);
+    if (r->copy_stream) cudaStreamDestroy(r->copy_stream);
     if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
 }
