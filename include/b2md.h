@@ -228,7 +228,10 @@ int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
  * non-zero (the positions it would use already need a new list), and sets word
  * `gate_out_word` when the positions it produces do; the two must differ (5 =
  * rebuild_flag, 12 = reserved[0]).  This makes a speculative launch safe: the host
- * reads the flag while the kernel is already queued. */
+ * reads the flag while the kernel is already queued.  A launch that returns at once
+ * also sets its own `gate_out_word`, so launches queued behind it return as well, and
+ * every launch that does run adds 1 to word 13 (reserved[1]): the host can queue
+ * several steps and learn afterwards how many were taken. */
 int b2md_force_lj_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
                                 void *d_vel, void *d_image_i4, int64_t n, const b2md_box *box,
                                 double dt, void *d_ref_pos_f4, double half_skin2,
@@ -403,6 +406,10 @@ typedef struct b2md_runner_config {
                                     with pair rows it lets the intermediate steps run as ONE
                                     kernel each (b2md_force_lj_pairs_advance); NULL = separate
                                     integrate and force launches */
+    int32_t queue_depth;         /* one-launch steps queued per status read-back (>= 1); small
+                                    systems, whose step is shorter than a host round trip,
+                                    want several */
+    int32_t reserved2;
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };

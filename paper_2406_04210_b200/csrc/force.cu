@@ -561,6 +561,8 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
 // The launch is gated on status word `gate_in` ("the positions I am about to use
 // already need a new list": set by the previous launch, which wrote `gate_out` of its
 // own) -- a launch enqueued speculatively then returns at once and the host rebuilds.
+constexpr int kWordAdvanceCount = 13;      // b2md_status::reserved[1]: advance launches that ran
+
 struct AdvanceArgs {
     float4 *pos_out, *pos_lo, *vel, *ref_pos;
     int4 *image;
@@ -582,7 +584,15 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     __shared__ float s_max[kForceThreads / 32];
     // step-graph batches: nothing to do once an in-graph list build overflowed
     if (gated && *(volatile int *)&status->frozen) return;
-    if (ADVANCE && ((volatile int *)status)[adv.gate_in]) return;
+    if (ADVANCE) {
+        // a launch that must not run hands the flag on, so that launches queued behind it
+        // do not run either; one that runs counts itself (the host may have several queued)
+        if (((volatile int *)status)[adv.gate_in]) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_out] = 1;
+            return;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&((int *)status)[kWordAdvanceCount], 1);
+    }
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -950,7 +960,8 @@ B2MD_EXPORT int b2md_force_lj_pairs_advance(
     int32_t gate_out_word, b2md_status *d_status, void *stream) {
     if (!d_pos_hi_out || d_pos_hi_out == d_pos_hi || !d_pos_lo || !d_vel || !d_image_i4 ||
         !d_ref_pos_f4 || !(dt > 0.0) || gate_in_word == gate_out_word || gate_in_word < 0 ||
-        gate_in_word >= 16 || gate_out_word < 0 || gate_out_word >= 16) {
+        gate_in_word >= 16 || gate_out_word < 0 || gate_out_word >= 16 ||
+        gate_in_word == kWordAdvanceCount || gate_out_word == kWordAdvanceCount) {
         set_error("b2md_force_lj_pairs_advance: bad arguments");
         return -1;
     }

@@ -58,6 +58,7 @@ struct b2md_runner {
     void *pos_cur;            // where the live position high words are (canonical or alt)
     bool ahead;               // positions already advanced to the step about to be processed
     int gate_in;              // status word holding the rebuild flag of those positions
+    int count_seen;           // advance launches counted by the device so far (word 13)
 };
 
 namespace {
@@ -121,6 +122,7 @@ int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
 
 constexpr int kWordRebuildFlag = 5;   // b2md_status::rebuild_flag
 constexpr int kWordAltFlag = 12;      // b2md_status::reserved[0]
+constexpr int kWordAdvanceCount = 13; // b2md_status::reserved[1]
 
 bool can_advance(const b2md_runner *r) {
     const b2md_runner_config &c = r->cfg;
@@ -251,6 +253,7 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
     rep->n_boundary = r->h_status->n_boundary;
     r->list_valid = r->h_status->overflow == 0;
     r->pos_cur = live(r).pos_hi;      // callers hand over canonical positions; sets may swap
+    r->count_seen = 0;                // the status reset of the rebuild cleared the counter
     return 0;
 }
 
@@ -454,11 +457,80 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
         r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
         r->ahead = true;
         r->pending_kick = false;
+        r->count_seen += 1;               // exactly one of this step's launches ran
     } else {
         r->ahead = false;
         r->pending_kick = true;
     }
     rep->steps_done += 1;
+    return 0;
+}
+
+void toggle_advance_state(b2md_runner *r) {
+    Set now = live(r);
+    void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
+    r->pos_cur = in == now.pos_hi ? r->cfg.pos_hi_alt : now.pos_hi;
+    r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+}
+
+// Up to `n_inter` intermediate steps as queued one-launch steps, several per status
+// read-back: a launch whose positions need a new list returns at once and makes the
+// ones queued behind it return too; the device counts the launches that ran.
+// Requires r->ahead.  *stop = 1 on overflow / singular.
+int advance_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_inter, int64_t before,
+                  int *stop) {
+    const b2md_runner_config &c = r->cfg;
+    cudaStream_t s = r->stream;
+    int rc;
+    *stop = 0;
+    const int m = (int)(n_inter < c.queue_depth ? n_inter : c.queue_depth);
+    void *pos0 = r->pos_cur;
+    const int gate0 = r->gate_in;
+    for (int q = 0; q < m; ++q) {
+        if ((rc = launch_advance(r))) return rc;
+        toggle_advance_state(r);
+    }
+    if ((rc = check_cuda(cudaEventRecord(r->ev_mark, s), "mark record"))) return rc;
+    if ((rc = check_cuda(cudaStreamWaitEvent(r->copy_stream, r->ev_mark, 0), "copy wait"))) return rc;
+    if ((rc = check_cuda(cudaMemcpyAsync(r->h_status, c.status, sizeof(b2md_status),
+                                         cudaMemcpyDeviceToHost, r->copy_stream),
+                         "status read-back"))) return rc;
+    if ((rc = check_cuda(cudaEventRecord(r->ev, r->copy_stream), "event record"))) return rc;
+    if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
+    const int32_t *words = reinterpret_cast<const int32_t *>(r->h_status);
+    const int ran = words[kWordAdvanceCount] - r->count_seen;
+    r->count_seen += ran;
+    // host-side state after the launches that really ran
+    r->pos_cur = pos0;
+    r->gate_in = gate0;
+    for (int q = 0; q < ran; ++q) toggle_advance_state(r);
+    rep->steps_done += ran;
+    rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
+    r->last_disp2 = rep->max_disp2;
+    if (r->h_status->singular != ~0ull) {
+        if ((rc = canonicalize(r))) return rc;
+        if ((rc = read_status(r))) return rc;
+        rep->singular = r->h_status->singular;
+        rep->reason = B2MD_RUN_SINGULAR;
+        finish_report(r, rep, before);
+        *stop = 1;
+        return 0;
+    }
+    if (ran < m) {
+        // the positions reached after `ran` steps need a new list
+        if ((rc = canonicalize(r))) return rc;
+        if ((rc = rebuild(r, rep))) return rc;
+        r->gate_in = kWordRebuildFlag;
+        r->last_disp2 = 0.0;
+        if (!r->list_valid) {
+            r->mid_step = true;
+            r->ahead = false;
+            rep->reason = B2MD_RUN_OVERFLOW;
+            finish_report(r, rep, before);
+            *stop = 1;
+            return 0;
+        }
+    }
     return 0;
 }
 
@@ -557,6 +629,8 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->pos_cur = nullptr;
     r->ahead = false;
     r->gate_in = kWordRebuildFlag;
+    r->count_seen = 0;
+    if (r->cfg.queue_depth < 1) r->cfg.queue_depth = 1;
     r->h_status = nullptr;
     r->ev = r->ev_in = r->ev_mark = nullptr;
     r->copy_stream = nullptr;
@@ -663,6 +737,8 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
         // graphed steps need the fused kick and must not be the observable last step
         if (c.use_graph && r->pending_kick && left > 1) {
             if ((rc = graph_batch(r, rep, left - 1, before, &stop))) return rc;
+        } else if (c.queue_depth > 1 && r->ahead && left > 1 && can_advance(r)) {
+            if ((rc = advance_batch(r, rep, left - 1, before, &stop))) return rc;
         } else {
             // energies / virial only on the step the caller can observe (the last one)
             if ((rc = plain_step(r, rep, left == 1, before, &stop))) return rc;

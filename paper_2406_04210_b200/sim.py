@@ -62,7 +62,8 @@ class Simulation:
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
                  stride_policy: str = "fit", graph: int | bool = False,
-                 pair_rows: bool | None = None, advance: bool | None = None):
+                 pair_rows: bool | None = None, advance: bool | None = None,
+                 queue_depth: int | None = None):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -95,6 +96,10 @@ class Simulation:
         # one-launch intermediate steps (needs pair rows; B2MD_ADVANCE=0 turns them off)
         self.advance = (os.environ.get("B2MD_ADVANCE", "1") != "0") if advance is None \
             else bool(advance)
+        # one-launch steps queued per status read-back (small systems: a step is shorter
+        # than a host round trip)
+        self.queue_depth = int(os.environ.get("B2MD_QUEUE_DEPTH", "1")) if queue_depth is None \
+            else int(queue_depth)
         self.graph_steps = 0
         # the thermostat acts between finalize and the next integrate: operator loop
         self.native = (force_mode == TRUNCATED and not thermostatted) if native is None \
@@ -281,6 +286,7 @@ class Simulation:
             if self.advance:
                 k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
                 cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
+                cfg.queue_depth = max(self.queue_depth, 1)
             k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
             k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
             cfg.pair_nbr = k["pair_nbr"].data_ptr()

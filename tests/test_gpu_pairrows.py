@@ -209,3 +209,27 @@ def test_one_launch_steps_with_pair_tables():
     assert out[0][2] == out[1][2] and out[0][2] >= 2
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert abs(out[1][0][-1] - out[1][0][0]) <= 5e-5 * abs(out[1][0][0])
+
+
+@pytest.mark.parametrize("n,depth", [(4096, 8), (4096, 3), (32_768, 16)])
+def test_queued_one_launch_steps_are_bit_identical(n, depth):
+    """Several gated launches per status read-back: a due rebuild turns the launches queued
+    behind it into no-ops, the device counts the steps taken -- same trajectory as one
+    read-back per step."""
+    out = []
+    for queue_depth in (1, depth):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 1.2, 42)
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001,
+                            force_mode=b2.TRUNCATED, skin=0.3, sample_interval=53,
+                            sample_initial=True, pair_rows=True, advance=True,
+                            queue_depth=queue_depth)
+        sim.run(500)
+        sim.run(2)
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    np.array(st.velocities.acquire_read(b2.HOST)),
+                    np.array(st.images.acquire_read(b2.HOST)), sim.rebuild_count))
+    assert out[0][4] == out[1][4] and out[0][4] >= 5
+    for k in range(4):
+        assert np.array_equal(out[0][k], out[1][k]), k
