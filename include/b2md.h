@@ -242,6 +242,16 @@ int b2md_force_lj_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *
                                 int32_t flags, int32_t gate_in_word, int32_t gate_out_word,
                                 b2md_status *d_status, void *stream);
 
+/* The same for the thread- (or sub-warp-) per-particle kernel b2md_force_lj: small
+ * systems, where a step is shorter than a host round trip, queue several of these. */
+int b2md_force_lj_advance(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel,
+                          void *d_image_i4, int64_t n, const b2md_box *box, double dt,
+                          void *d_ref_pos_f4, double half_skin2, const int32_t *d_nbr,
+                          const int32_t *d_counts, int64_t pitch, int32_t stride,
+                          const uint8_t *d_boundary, const double *table, int32_t ntypes,
+                          int32_t flags, int32_t gate_in_word, int32_t gate_out_word,
+                          b2md_status *d_status, void *stream);
+
 /* compute_forces_all_to_all (forces.py:129-138; kernel 29-69): shared-memory
  * tiled all-pairs scan, same outputs. */
 int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
@@ -403,9 +413,9 @@ typedef struct b2md_runner_config {
     int32_t *pair_counts;        /* pair_pitch */
     int64_t pair_pitch;          /* multiple of 32 >= ceil(n/2) */
     void *pos_hi_alt;            /* float4[capacity]: second buffer for the position high words;
-                                    with pair rows it lets the intermediate steps run as ONE
-                                    kernel each (b2md_force_lj_pairs_advance); NULL = separate
-                                    integrate and force launches */
+                                    it lets the intermediate steps run as ONE kernel each
+                                    (b2md_force_lj_pairs_advance / b2md_force_lj_advance);
+                                    NULL = separate integrate and force launches */
     int32_t queue_depth;         /* one-launch steps queued per status read-back (>= 1); small
                                     systems, whose step is shorter than a host round trip,
                                     want several */

@@ -128,6 +128,9 @@ _SIGNATURES = {
     "b2md_pair_rows": (c_int32, [_P, _P, c_int64, c_int32, c_int64, _P, _P, c_int64, c_int32, _P]),
     "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
                                       _P, POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
+    "b2md_force_lj_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,
+                                        c_double, _P, _P, c_int64, c_int32, _P, POINTER(c_double),
+                                        c_int32, c_int32, c_int32, c_int32, _P, _P]),
     "b2md_force_lj_pairs_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double,
                                               _P, c_double, _P, _P, c_int64, _P, _P, c_int64, _P,
                                               POINTER(c_double), c_int32, c_int32, c_int32,

@@ -300,19 +300,69 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
+// ADVANCE (both list kernels): the kernel also applies what the step loop does between two force
+// evaluations -- both half-kicks with the forces it has just computed, the drift, the
+// wrap and the displacement check (= k_integrate<2>) -- so the intermediate steps of
+// the native loop are ONE launch each and the forces never travel through HBM.
+// Positions are read by other threads while this one moves on, hence the new high
+// words go to a second buffer (pos_out) that the next launch reads; velocities, low
+// words, images and the list snapshot are private to the thread and updated in place.
+// The launch is gated on status word `gate_in` ("the positions I am about to use
+// already need a new list": set by the previous launch, which wrote `gate_out` of its
+// own) -- a launch enqueued speculatively then returns at once and the host rebuilds.
+constexpr int kWordAdvanceCount = 13;      // b2md_status::reserved[1]: advance launches that ran
+
+struct AdvanceArgs {
+    float4 *pos_out, *pos_lo, *vel, *ref_pos;
+    int4 *image;
+    StepConst step;
+    int gate_in, gate_out;        // int32 word indices into b2md_status
+};
+
+// Gate of an ADVANCE launch (see AdvanceArgs): true = this launch must not run.
+__device__ __forceinline__ bool advance_gate_closed(b2md_status *status, const AdvanceArgs &adv) {
+    // a launch that must not run hands the flag on, so that launches queued behind it
+    // do not run either; one that runs counts itself (the host may have several queued)
+    if (((volatile int *)status)[adv.gate_in]) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_out] = 1;
+        return true;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&((int *)status)[kWordAdvanceCount], 1);
+    return false;
+}
+
+// Displacement maximum of the block -> status (as k_integrate does); all threads call it.
+__device__ __forceinline__ void advance_publish_disp(float d2, float *s_max, b2md_status *status,
+                                                     const AdvanceArgs &adv) {
+    d2 = warp_max(d2);
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0 && m > 0.0f) {
+            atomicMax(&status->max_disp2_bits, __float_as_uint(m));
+            if (m > adv.step.half_skin2) ((int *)status)[adv.gate_out] = 1;
+        }
+    }
+}
+
 // PIPE doubles as the occupancy knob of the experiments: 0 = 8 CTAs/SM (<= 64
 // registers), 1 = gathers one trip ahead with 6 CTAs/SM, 2 = 12 CTAs/SM (<= 40).
-template <int SUB, int GATHER, int PIPE, bool TABLE, bool THERMO>
+template <int SUB, int GATHER, int PIPE, bool TABLE, bool THERMO, bool ADVANCE = false>
 __global__ void __launch_bounds__(kForceThreads, PIPE == 1 ? 6 : (PIPE == 2 ? 12 : 8))
 k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
            const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
            const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
-           float *__restrict__ virial, b2md_status *status, int gated) {
+           float *__restrict__ virial, b2md_status *status, int gated,
+           const __grid_constant__ AdvanceArgs adv) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float s_max[kForceThreads / 32];
     // step-graph batches: nothing to do once an in-graph list build overflowed
     if (gated && *(volatile int *)&status->frozen) return;
+    if (ADVANCE && advance_gate_closed(status, adv)) return;
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -357,20 +407,30 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
             acc.cnt += __shfl_xor_sync(0xffffffffu, acc.cnt, o);
         }
     }
-    if (!active || sub != 0) return;
-    float fx, fy, fz, u, w;
-    if (TABLE) {
-        fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
-    } else {
-        const PairParams &p = a.single;
-        fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
-        u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
-        w = p.c_w * acc.w;
+    float d2 = 0.0f;
+    if (active && sub == 0) {
+        float fx, fy, fz, u, w;
+        if (TABLE) {
+            fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
+        } else {
+            const PairParams &p = a.single;
+            fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+            u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
+            w = p.c_w * acc.w;
+        }
+        if (ADVANCE) {
+            float4 h = pi;
+            d2 = advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo, adv.vel,
+                                     adv.image, adv.step, adv.ref_pos);
+            adv.pos_out[i] = h;
+        } else {
+            force[i] = make_float4(fx, fy, fz, u);
+            if (THERMO && virial) virial[i] = w;
+        }
+        if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
+            report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
     }
-    force[i] = make_float4(fx, fy, fz, u);
-    if (THERMO && virial) virial[i] = w;
-    if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-        report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
+    if (ADVANCE) advance_publish_disp(d2, s_max, status, adv);
 }
 
 // ---- pair rows: two particles per thread -------------------------------------
@@ -551,25 +611,6 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     }
 }
 
-// ADVANCE: the kernel also applies what the step loop does between two force
-// evaluations -- both half-kicks with the forces it has just computed, the drift, the
-// wrap and the displacement check (= k_integrate<2>) -- so the intermediate steps of
-// the native loop are ONE launch each and the forces never travel through HBM.
-// Positions are read by other threads while this one moves on, hence the new high
-// words go to a second buffer (pos_out) that the next launch reads; velocities, low
-// words, images and the list snapshot are private to the thread and updated in place.
-// The launch is gated on status word `gate_in` ("the positions I am about to use
-// already need a new list": set by the previous launch, which wrote `gate_out` of its
-// own) -- a launch enqueued speculatively then returns at once and the host rebuilds.
-constexpr int kWordAdvanceCount = 13;      // b2md_status::reserved[1]: advance launches that ran
-
-struct AdvanceArgs {
-    float4 *pos_out, *pos_lo, *vel, *ref_pos;
-    int4 *image;
-    StepConst step;
-    int gate_in, gate_out;        // int32 word indices into b2md_status
-};
-
 template <bool TABLE, bool THERMO, bool SIG1, bool ADVANCE>
 __global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
@@ -584,15 +625,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     __shared__ float s_max[kForceThreads / 32];
     // step-graph batches: nothing to do once an in-graph list build overflowed
     if (gated && *(volatile int *)&status->frozen) return;
-    if (ADVANCE) {
-        // a launch that must not run hands the flag on, so that launches queued behind it
-        // do not run either; one that runs counts itself (the host may have several queued)
-        if (((volatile int *)status)[adv.gate_in]) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_out] = 1;
-            return;
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&((int *)status)[kWordAdvanceCount], 1);
-    }
+    if (ADVANCE && advance_gate_closed(status, adv)) return;
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -659,20 +692,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                                 status);
         }
     }
-    if (ADVANCE) {
-        // displacement maximum of the block -> status (as k_integrate does)
-        d2 = warp_max(d2);
-        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
-            m = warp_max(m);
-            if (threadIdx.x == 0 && m > 0.0f) {
-                atomicMax(&status->max_disp2_bits, __float_as_uint(m));
-                if (m > adv.step.half_skin2) ((int *)status)[adv.gate_out] = 1;
-            }
-        }
-    }
+    if (ADVANCE) advance_publish_disp(d2, s_max, status, adv);
 }
 
 // ---- all pairs, shared-memory tiles of 128 positions ------------------------
@@ -841,7 +861,8 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     k_force_lj<SUB, GATHER, PIPE, TABLE, THERMO>                                             \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
             (const float4 *)d_pos_hi, tex, n, a, d_nbr, d_counts, pitch, d_boundary,         \
-            (float4 *)d_force_f4, d_virial, d_status, (flags & B2MD_FORCE_GATED) ? 1 : 0)
+            (float4 *)d_force_f4, d_virial, d_status, (flags & B2MD_FORCE_GATED) ? 1 : 0,    \
+            AdvanceArgs())
 #define B2MD_DISPATCH_TT(SUB, GATHER, PIPE)                                                  \
     do {                                                                                     \
         if (ntypes == 1) {                                                                   \
@@ -951,21 +972,19 @@ B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_
                         nullptr, stream, "b2md_force_lj_pairs");
 }
 
-B2MD_EXPORT int b2md_force_lj_pairs_advance(
-    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
-    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
-    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
-    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
-    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
-    int32_t gate_out_word, b2md_status *d_status, void *stream) {
+namespace {
+
+int fill_advance(AdvanceArgs &adv, const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
+                 void *d_vel, void *d_image_i4, const b2md_box *box, double dt,
+                 void *d_ref_pos_f4, double half_skin2, int32_t gate_in_word,
+                 int32_t gate_out_word, const char *name) {
     if (!d_pos_hi_out || d_pos_hi_out == d_pos_hi || !d_pos_lo || !d_vel || !d_image_i4 ||
-        !d_ref_pos_f4 || !(dt > 0.0) || gate_in_word == gate_out_word || gate_in_word < 0 ||
-        gate_in_word >= 16 || gate_out_word < 0 || gate_out_word >= 16 ||
+        !d_ref_pos_f4 || !box || !(dt > 0.0) || gate_in_word == gate_out_word ||
+        gate_in_word < 0 || gate_in_word >= 16 || gate_out_word < 0 || gate_out_word >= 16 ||
         gate_in_word == kWordAdvanceCount || gate_out_word == kWordAdvanceCount) {
-        set_error("b2md_force_lj_pairs_advance: bad arguments");
+        set_error("%s: bad arguments", name);
         return -1;
     }
-    AdvanceArgs adv;
     adv.pos_out = (float4 *)d_pos_hi_out;
     adv.pos_lo = (float4 *)d_pos_lo;
     adv.vel = (float4 *)d_vel;
@@ -974,6 +993,60 @@ B2MD_EXPORT int b2md_force_lj_pairs_advance(
     adv.step = make_step(box, dt, half_skin2);
     adv.gate_in = gate_in_word;
     adv.gate_out = gate_out_word;
+    return 0;
+}
+
+}  // namespace
+
+B2MD_EXPORT int b2md_force_lj_advance(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, int32_t stride,
+    const uint8_t *d_boundary, const double *table, int32_t ntypes, int32_t flags,
+    int32_t gate_in_word, int32_t gate_out_word, b2md_status *d_status, void *stream) {
+    if (n <= 0 || !d_nbr || !d_counts || !d_status || stride < 1 || stride % 16 != 0) {
+        set_error("b2md_force_lj_advance: bad arguments");
+        return -1;
+    }
+    AdvanceArgs adv;
+    int rc = fill_advance(adv, d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, box, dt,
+                          d_ref_pos_f4, half_skin2, gate_in_word, gate_out_word,
+                          "b2md_force_lj_advance");
+    if (rc) return rc;
+    ForceArgs a;
+    if ((rc = fill_args(a, box, table, ntypes))) return rc;
+    cudaStream_t s = as_stream(stream);
+    const int gated = (flags & B2MD_FORCE_GATED) ? 1 : 0;
+    // lanes per particle as in b2md_force_lj: small systems are latency-bound
+#define B2MD_LAUNCH_ROW_ADVANCE(SUB, PIPE, TABLE)                                             \
+    k_force_lj<SUB, 0, PIPE, TABLE, false, true>                                              \
+        <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                        \
+            (const float4 *)d_pos_hi, 0, n, a, d_nbr, d_counts, pitch, d_boundary, nullptr,   \
+            nullptr, d_status, gated, adv)
+    if (n < 200000) {
+        if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(4, 0, false);
+        else B2MD_LAUNCH_ROW_ADVANCE(4, 0, true);
+    } else {
+        if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(1, 2, false);
+        else B2MD_LAUNCH_ROW_ADVANCE(1, 2, true);
+    }
+#undef B2MD_LAUNCH_ROW_ADVANCE
+    B2MD_CHECK_LAUNCH("b2md_force_lj_advance");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_force_lj_pairs_advance(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
+    int32_t gate_out_word, b2md_status *d_status, void *stream) {
+    AdvanceArgs adv;
+    int rc = fill_advance(adv, d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, box, dt,
+                          d_ref_pos_f4, half_skin2, gate_in_word, gate_out_word,
+                          "b2md_force_lj_pairs_advance");
+    if (rc) return rc;
     return launch_pairs(d_pos_hi, n, box, d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts,
                         pitch, d_boundary, table, ntypes, flags | B2MD_FORCE_SKIP_THERMO, nullptr,
                         nullptr, d_status, &adv, stream, "b2md_force_lj_pairs_advance");

@@ -126,7 +126,7 @@ constexpr int kWordAdvanceCount = 13; // b2md_status::reserved[1]
 
 bool can_advance(const b2md_runner *r) {
     const b2md_runner_config &c = r->cfg;
-    return c.pos_hi_alt != nullptr && c.pair_rows > 0 && c.use_graph == 0;
+    return c.pos_hi_alt != nullptr && c.use_graph == 0;
 }
 
 // The canonical buffer of the live set holds the position high words again.
@@ -148,6 +148,11 @@ int launch_advance(b2md_runner *r) {
     void *out = in == a.pos_hi ? c.pos_hi_alt : a.pos_hi;
     const int gate_out = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
     r->launches += 1;
+    if (c.pair_rows <= 0)
+        return b2md_force_lj_advance(in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt,
+                                     c.ref_pos, r->half_skin2, c.nbr, c.counts, c.pitch,
+                                     stride_rows(r), c.boundary, r->table.data(), c.ntypes, 0,
+                                     r->gate_in, gate_out, c.status, r->stream);
     return b2md_force_lj_pairs_advance(in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt,
                                        c.ref_pos, r->half_skin2, c.pair_nbr, c.pair_counts,
                                        c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,

@@ -46,6 +46,10 @@ DEFAULT_STRIDE = 64
 DEFAULT_SKIN = 0.5
 STRIDE_GROWTH_LIMIT = 10
 
+#: below this size the thread-per-particle kernel also advances the particles it has
+#: evaluated (one launch per step); from PAIR_ROWS_MIN_PARTICLES up the pair kernel does
+ADVANCE_ROWS_MAX_PARTICLES = 60_000
+
 _REORDER_MODES = {None: 0, "none": 0, "hilbert": 1, "cell": 2}
 
 
@@ -94,8 +98,13 @@ class Simulation:
         # force kernel: one thread per particle pair over merged rows (None = by size)
         self.pair_rows = use_pair_rows(state.n, pair_rows)
         # one-launch intermediate steps (needs pair rows; B2MD_ADVANCE=0 turns them off)
-        self.advance = (os.environ.get("B2MD_ADVANCE", "1") != "0") if advance is None \
-            else bool(advance)
+        # (measured, profiles/exp/queue_depth.py: a clear gain with pair rows and for small
+        # systems, a loss for the sub-warp row kernel between 65 k and 200 k particles)
+        if advance is None:
+            env = os.environ.get("B2MD_ADVANCE")
+            advance = (env != "0") if env in ("0", "1") else \
+                (self.pair_rows or state.n < ADVANCE_ROWS_MAX_PARTICLES)
+        self.advance = bool(advance)
         # one-launch steps queued per status read-back (small systems: a step is shorter
         # than a host round trip)
         self.queue_depth = int(os.environ.get("B2MD_QUEUE_DEPTH", "1")) if queue_depth is None \
@@ -280,13 +289,13 @@ class Simulation:
         cfg.status = dev.status.data_ptr()
         cfg.stream = dev.stream
         cfg.use_graph = self.graph
-        if self.pair_rows:
+        if self.advance and not self.graph:
             # second buffer for the position high words: intermediate steps then run as one
-            # launch each (force + finalize + integrate, b2md_force_lj_pairs_advance)
-            if self.advance:
-                k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
-                cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
-                cfg.queue_depth = max(self.queue_depth, 1)
+            # launch each (force + finalize + integrate, b2md_force_lj[_pairs]_advance)
+            k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
+            cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
+            cfg.queue_depth = max(self.queue_depth, 1)
+        if self.pair_rows:
             k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
             k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
             cfg.pair_nbr = k["pair_nbr"].data_ptr()

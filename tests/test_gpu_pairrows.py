@@ -233,3 +233,26 @@ def test_queued_one_launch_steps_are_bit_identical(n, depth):
     assert out[0][4] == out[1][4] and out[0][4] >= 5
     for k in range(4):
         assert np.array_equal(out[0][k], out[1][k]), k
+
+
+@pytest.mark.parametrize("n,depth", [(4096, 1), (4096, 8), (20_000, 5)])
+def test_row_kernel_one_launch_steps_are_bit_identical(n, depth):
+    """The thread-per-particle kernel with the ADVANCE epilogue (small systems), one or
+    several launches per status read-back, against separate integrate / force launches."""
+    out = []
+    for kw in (dict(advance=False), dict(advance=True, queue_depth=depth)):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 1.2, 42)
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001,
+                            force_mode=b2.TRUNCATED, skin=0.3, sample_interval=41,
+                            sample_initial=True, pair_rows=False, **kw)
+        sim.run(400)
+        sim.run(2)
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    np.array(st.velocities.acquire_read(b2.HOST)),
+                    np.array(st.images.acquire_read(b2.HOST)),
+                    np.array(st.forces.acquire_read(b2.HOST)), sim.rebuild_count))
+    assert out[0][5] == out[1][5] and out[0][5] >= 5
+    for k in range(5):
+        assert np.array_equal(out[0][k], out[1][k]), k
