@@ -306,7 +306,7 @@ def run_gpu_arm(args):
                       ref_scratch.data_ptr(), 1e30, k["pair_nbr"].data_ptr(),
                       k["pair_counts"].data_ptr(), cfg.pair_pitch, k["nbr"].data_ptr(),
                       k["counts"].data_ptr(), k["pitch"], k["boundary"].data_ptr(), tab_ptr, 1, 0,
-                      12, 13, scratch_status.data_ptr(), dev.stream)
+                      12, 14, scratch_status.data_ptr(), dev.stream)   # gate words of the scratch block
         adv_ms = time_kernel(launch_advance, 30, torch, stream)
         # SURVEY 8(d) rows it replaces: integrate 128 + force 32+4c (no-thermo) + finalize 48,
         # minus the 80 B per particle of force / velocity traffic that fusion makes unnecessary
