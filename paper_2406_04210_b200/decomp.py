@@ -173,6 +173,7 @@ class SlabSimulation:
         self.rebuilds = 0
         self.samples = []
         self.pending_kick = False
+        self.ahead = False            # one-launch steps: particles already at the next step
         self.halo_rows = (0, 0)
         self.ops.attach(self.geo, lj, self.dt, self.skin)
         self._rebuild()
@@ -221,6 +222,8 @@ class SlabSimulation:
 
     # -- step loop ------------------------------------------------------------
     def run(self, n_steps: int):
+        if getattr(self.ops, "can_advance", False):
+            return self._run_advance(n_steps)
         ops, comm = self.ops, self.comm
         for s in range(n_steps):
             last = (s == n_steps - 1) or ((self.step_count + 1) % self.sample_interval == 0)
@@ -240,6 +243,57 @@ class SlabSimulation:
             else:
                 self.pending_kick = True
 
+    # One-launch steps (backends with `can_advance`): an intermediate step is ONE kernel
+    # -- force(s) + finalize(s) + integrate(s+1) + local displacement check on the owned
+    # rows, forces never stored -- followed by the halo exchange of the new positions
+    # and an in-place all-reduce(max) of the flag word the kernel wrote.  The kernel is
+    # gated on the (already reduced) flag of the positions it reads, so the host enqueues
+    # it before it knows that flag: the 64-byte status block is copied on a side stream
+    # and inspected while the launch is already queued; when a rebuild is due the launch
+    # returns at once on every rank, the ranks rebuild together and enqueue it again.
+    # Nothing in the step waits for the host.  Same trajectories, bit for bit, as the
+    # separate launches above (tests/test_gpu_slab.py).
+    def _advance_once(self):
+        ops, comm = self.ops, self.comm
+        ops.advance()                      # reads the current buffer, writes the other one
+        ops.swap_positions()               # ... which now is the current one
+        self._halo()                       # ghost rows of the new buffer
+        comm.all_max(ops.gate_word_out())  # the flag of the new positions, all ranks agree
+
+    def _run_advance(self, n_steps: int):
+        ops, comm = self.ops, self.comm
+        for s in range(n_steps):
+            last = (s == n_steps - 1) or ((self.step_count + 1) % self.sample_interval == 0)
+            if not self.ahead:
+                ops.integrate(fused=self.pending_kick)
+                self.pending_kick = False
+                ops.gate_reset_to_integrate()
+                comm.all_max(ops.gate_word_in())
+                self._halo()
+            if last:
+                # observable step: forces with energies / virial, stored; then the half-kick
+                if ops.read_gate_in():                    # host sync, once per sample
+                    self._rebuild()
+                    ops.gate_reset_to_integrate()
+                ops.force(thermo=True)
+                ops.finalize()
+                self.ahead = False
+                self.step_count += 1
+                if self.step_count % self.sample_interval == 0:
+                    self.samples.append(self.measure())
+                continue
+            ticket = ops.snapshot_status()     # flag of the current positions, side stream
+            self._advance_once()               # queued before the flag is known
+            if ops.snapshot_gate_in(ticket):
+                # the launch returned at once (on every rank): undo the swap, rebuild, again
+                ops.swap_positions()
+                self._rebuild()
+                ops.gate_reset_to_integrate()
+                self._advance_once()
+            ops.gate_toggle()
+            self.ahead = True
+            self.step_count += 1
+
     def measure(self):
         sums = self.comm.all_sum(self.ops.thermo_sums())   # 8 doubles
         v = [float(x) for x in sums.tolist()]
@@ -254,7 +308,7 @@ class CudaSlabOps:
     """libb2md kernels + CUDA tensors behind the SlabSimulation protocol."""
 
     def __init__(self, pos, vel, ids, edges, device_index=0, capacity_factor=1.25,
-                 ghost_fraction=0.25, stride=64, reorder=True):
+                 ghost_fraction=0.25, stride=64, reorder=True, pair_rows=None, advance=None):
         torch = _torch()
         _lib.load()
         self.torch = torch
@@ -268,6 +322,7 @@ class CudaSlabOps:
         self.capacity = (self.capacity + 31) // 32 * 32
         self.stride = int(stride)
         self.reorder = reorder
+        self._pair_rows_arg, self._advance_arg = pair_rows, advance
         f32 = dict(dtype=torch.float32, device=self.device)
         cap = self.capacity
         self.sets = [{k: torch.zeros((cap, 4), **f32) for k in ("pos_hi", "pos_lo", "vel", "force")}
@@ -278,6 +333,13 @@ class CudaSlabOps:
         self.cur = 0
         self.virial = torch.zeros(cap, **f32)
         self.status = torch.zeros(16, dtype=torch.int32, device=self.device)
+        # one-launch steps: second position buffer (ping-pong), pinned copy of the status
+        # block, side stream for its read-back
+        self.pos_alt = torch.zeros((cap, 4), **f32)
+        self.h_status = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.copy_done = torch.cuda.Event()
+        self.gate_in = 5              # int32 word of the status block: 5 = rebuild_flag
         self.box = _lib.make_box(self.edges)
         # upload through the same conversion kernels as the single-GPU path
         a = self.sets[0]
@@ -369,7 +431,9 @@ class CudaSlabOps:
         # merged rows of owned particle pairs for the two-particles-per-thread force
         # kernel (b2md_pair_rows); large slabs only, like the single-domain loop
         from .forces import use_pair_rows
-        self.pair_rows = use_pair_rows(self.cap_own)
+        self.pair_rows = use_pair_rows(self.cap_own, self._pair_rows_arg)
+        self.can_advance = self.pair_rows if self._advance_arg is None else \
+            bool(self._advance_arg) and self.pair_rows
         if self.pair_rows:
             self.pair_pitch = ((self.cap_own + 1) // 2 + 31) // 32 * 32
             self.pair_nbr = self.torch.zeros((2 * rows // 4, self.pair_pitch, 4),
@@ -583,6 +647,62 @@ class CudaSlabOps:
                   0 if thermo else _lib.FORCE_SKIP_THERMO, a["force"].data_ptr(),
                   self.virial.data_ptr(), self.status.data_ptr(), self.stream)
         self.kernel_launches += 1
+
+    # -- one-launch steps (see SlabSimulation._run_advance) ------------------------
+    GATE_WORDS = (5, 12)              # rebuild_flag, reserved[0] (include/b2md.h)
+
+    @property
+    def gate_out(self):
+        return self.GATE_WORDS[1] if self.gate_in == self.GATE_WORDS[0] else self.GATE_WORDS[0]
+
+    def gate_word_in(self):
+        return self.status[self.gate_in:self.gate_in + 1]
+
+    def gate_word_out(self):
+        return self.status[self.gate_out:self.gate_out + 1]
+
+    def gate_toggle(self):
+        self.gate_in = self.gate_out
+
+    def gate_reset_to_integrate(self):
+        """After k_integrate or a rebuild the flag of the current positions is word 5."""
+        self.gate_in = self.GATE_WORDS[0]
+
+    def advance(self):
+        a = self.a
+        half_skin2 = (0.5 * self.skin) ** 2
+        _lib.call("b2md_force_lj_pairs_advance", a["pos_hi"].data_ptr(), self.pos_alt.data_ptr(),
+                  a["pos_lo"].data_ptr(), a["vel"].data_ptr(), a["image"].data_ptr(), self.n_own,
+                  ctypes.byref(self.box), self.dt, self.ref_pos.data_ptr(), half_skin2,
+                  self.pair_nbr.data_ptr(), self.pair_counts.data_ptr(), self.pair_pitch,
+                  self.nbr.data_ptr(), self.counts.data_ptr(), self.capacity,
+                  self.boundary.data_ptr(), self.table_ptr, self.lj.ntypes, 0, self.gate_in,
+                  self.gate_out, self.status.data_ptr(), self.stream)
+        self.kernel_launches += 1
+
+    def swap_positions(self):
+        """The other position buffer becomes the live one (no copy: every kernel call
+        takes the pointer from the set at call time)."""
+        a = self.a
+        a["pos_hi"], self.pos_alt = self.pos_alt, a["pos_hi"]
+
+    def snapshot_status(self):
+        """Start an asynchronous copy of the status block as it is after everything
+        enqueued so far; the kernels enqueued next do not wait for it."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.device)
+        self.copy_stream.wait_stream(main)
+        with torch.cuda.stream(self.copy_stream):
+            self.h_status.copy_(self.status, non_blocking=True)
+            self.copy_done.record(self.copy_stream)
+        return self.gate_in
+
+    def snapshot_gate_in(self, word):
+        self.copy_done.synchronize()
+        return int(self.h_status[word]) != 0
+
+    def read_gate_in(self):
+        return int(self.status[self.gate_in].item()) != 0
 
     def finalize(self):
         a = self.a

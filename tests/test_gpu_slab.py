@@ -30,7 +30,7 @@ def global_system(world):
     return q32(pos), q32(vel), (edge * world, edge, edge)
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, advance, pair_rows):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -39,9 +39,11 @@ def _worker(rank, world, port, out):
         pos, vel, edges = global_system(world)
         geo = SlabGeometry(rank, world, edges)
         mine = np.flatnonzero((pos[:, 0] >= geo.x_lo) & (pos[:, 0] < geo.x_lo + geo.width))
-        ops = CudaSlabOps(pos[mine], vel[mine], mine, edges, device_index=0, stride=32)
+        ops = CudaSlabOps(pos[mine], vel[mine], mine, edges, device_index=0, stride=32,
+                          pair_rows=pair_rows, advance=advance)
         sim = SlabSimulation(ops, SlabComm(geo), b2.make_shifted(1.0, 1.0, 2.5), DT, SKIN,
                              sample_interval=25)
+        assert bool(ops.can_advance) == advance
         first = sim.measure()
         sim.run(STEPS)
         ids, p, v = ops.owned_state()
@@ -59,13 +61,36 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_cuda_slab_run_tracks_single_domain_oracle(world):
-    from oracle import oracle as orc
+def _run(world, advance, pair_rows=None):
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    res = [out[r] for r in range(world)]
+    mp.spawn(_worker, args=(world, _free_port(), out, advance, pair_rows or advance or None),
+             nprocs=world, join=True)
+    return [out[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_one_launch_slab_steps_are_bit_identical_to_separate_launches(world):
+    """force + finalize + integrate in one gated launch per step, flag all-reduced in
+    place, no host wait inside a step: same trajectory, bit for bit."""
+    # (both with the pair-row force kernel: the sub-warp row kernel small slabs default to
+    # sums in another order)
+    a, b = _run(world, False, pair_rows=True), _run(world, True)
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra["ids"], rb["ids"])
+        assert np.array_equal(ra["pos"], rb["pos"])
+        assert np.array_equal(ra["vel"], rb["vel"])
+        assert ra["rebuilds"] == rb["rebuilds"]
+        assert [s["total_energy"] for s in ra["samples"]] == \
+            [s["total_energy"] for s in rb["samples"]]
+        # separate launches: integrate + force (+ halo gathers) per step; one launch: one
+        assert rb["launches"] < ra["launches"] - STEPS // 2
+
+
+@pytest.mark.parametrize("world,advance", [(1, False), (2, False), (2, True)])
+def test_cuda_slab_run_tracks_single_domain_oracle(world, advance):
+    from oracle import oracle as orc
+    res = _run(world, advance)
 
     pos, vel, edges = global_system(world)
     ref = orc.Sim(pos, vel, edges, orc.pair_table(1.0, 1.0, 2.5), DT, SKIN, stride=128,
@@ -79,7 +104,7 @@ def test_cuda_slab_run_tracks_single_domain_oracle(world):
     if world > 1:
         assert sum(r["left_home"] for r in res) > 0           # migration happened
         assert all(min(r["halo"]) > 0 for r in res)
-    assert all(r["rebuilds"] >= 3 and r["launches"] > 2 * STEPS for r in res)
+    assert all(r["rebuilds"] >= 3 and r["launches"] > (1 if advance else 2) * STEPS for r in res)
     order = np.argsort(ids)
     got_pos = np.concatenate([r["pos"] for r in res])[order]
     d = got_pos - ref.pos
