@@ -12,7 +12,17 @@ from oracle import oracle as orc
 class NumpySlabOps:
     device = torch.device("cpu")
 
-    def __init__(self, pos, vel, ids, edges, stride=32):
+    GATE_WORDS = (5, 12)
+
+    def __init__(self, pos, vel, ids, edges, stride=32, advance=False):
+        # one-launch steps (SlabSimulation._run_advance): the 16 status words of the
+        # device block, a second position buffer with its own ghost rows
+        self.can_advance = bool(advance)
+        self.status = torch.zeros(16, dtype=torch.int32)
+        self.gate_in = 5
+        self.pos_alt = None
+        self.ghost_pos_alt = np.zeros((0, 3))
+        self.noop_launches = 0
         self.pos = np.array(pos, dtype=np.float64)
         self.vel = np.array(vel, dtype=np.float64)
         self.img = np.zeros(self.pos.shape, dtype=np.int64)
@@ -140,6 +150,7 @@ class NumpySlabOps:
         self.nlist = nl
         self.at_build = self.pos + self.img * self.edges
         self.flag = 0
+        self.status.zero_()
         # true wanted length is not exposed by the oracle: on overflow ask for double
         return over, (2 * self.stride if over else int(nl.counts[:self.n_own].max()))
 
@@ -151,6 +162,8 @@ class NumpySlabOps:
         disp = (self.pos + self.img * self.edges) - self.at_build
         half = 0.5 * self.skin
         self.flag = int(np.max((disp * disp).sum(axis=1)) > half * half)
+        if self.flag:
+            self.status[5] = 1
 
     def rebuild_flag(self):
         return torch.tensor([self.flag], dtype=torch.int64)
@@ -159,6 +172,57 @@ class NumpySlabOps:
         allpos = self._all_pos()
         f, pe, w = orc.forces_truncated(allpos, self.edges, self.table, self.nlist)
         self.forces, self.pe, self.virial = f[:self.n_own], pe[:self.n_own], w[:self.n_own]
+
+    # -- one-launch steps: same contract as CudaSlabOps -----------------------------
+    @property
+    def gate_out(self):
+        return self.GATE_WORDS[1] if self.gate_in == self.GATE_WORDS[0] else self.GATE_WORDS[0]
+
+    def gate_word_in(self):
+        return self.status[self.gate_in:self.gate_in + 1]
+
+    def gate_word_out(self):
+        return self.status[self.gate_out:self.gate_out + 1]
+
+    def gate_toggle(self):
+        self.gate_in = self.gate_out
+
+    def gate_reset_to_integrate(self):
+        self.gate_in = self.GATE_WORDS[0]
+
+    def advance(self):
+        """force(s) + finalize(s) + integrate(s+1) + displacement check; gated."""
+        self.kernel_launches += 1
+        if int(self.status[self.gate_in]):
+            self.status[self.gate_out] = 1          # hand the flag on, do nothing
+            self.noop_launches += 1
+            if self.pos_alt is None or self.pos_alt.shape != self.pos.shape:
+                self.pos_alt = np.full_like(self.pos, np.nan)     # never-written buffer
+            return
+        self.force(thermo=False)
+        ones = np.ones(self.n_own)
+        vel = orc.vv_finalize(self.vel, self.forces, ones, self.dt)
+        self.pos_alt, self.img, self.vel = orc.vv_integrate(
+            self.pos, self.img, vel, self.forces, ones, self.edges, self.dt)
+        disp = (self.pos_alt + self.img * self.edges) - self.at_build
+        half = 0.5 * self.skin
+        if np.max((disp * disp).sum(axis=1)) > half * half:
+            self.status[self.gate_out] = 1
+
+    def swap_positions(self):
+        self._all_pos()                             # received ghosts belong to this buffer
+        self.pos, self.pos_alt = self.pos_alt, self.pos
+        self.ghost_pos, self.ghost_pos_alt = self.ghost_pos_alt, self.ghost_pos
+
+    def snapshot_status(self):
+        self._snap = self.status.clone()
+        return self.gate_in
+
+    def snapshot_gate_in(self, word):
+        return int(self._snap[word]) != 0
+
+    def read_gate_in(self):
+        return int(self.status[self.gate_in]) != 0
 
     def finalize(self):
         self.vel = orc.vv_finalize(self.vel, self.forces, np.ones(self.n_own), self.dt)

@@ -31,7 +31,7 @@ def global_system(world):
     return pos, vel, (edge * world, edge, edge)
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, advance):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -41,7 +41,7 @@ def _worker(rank, world, port, out):
         pos, vel, edges = global_system(world)
         geo = SlabGeometry(rank, world, edges)
         mine = np.flatnonzero((pos[:, 0] >= geo.x_lo) & (pos[:, 0] < geo.x_lo + geo.width))
-        ops = NumpySlabOps(pos[mine], vel[mine], mine, edges, stride=24)
+        ops = NumpySlabOps(pos[mine], vel[mine], mine, edges, stride=24, advance=advance)
         sim = SlabSimulation(ops, SlabComm(geo), b2.make_shifted(1.0, 1.0, 2.5), DT, SKIN,
                              sample_interval=20)
         first = sim.measure()
@@ -51,7 +51,8 @@ def _worker(rank, world, port, out):
         dist.all_reduce(counts)
         out[rank] = dict(ids=ids, pos=p, vel=v, samples=[first] + sim.samples,
                          total=int(counts.item()), rebuilds=sim.rebuilds, stride=ops.stride,
-                         left_home=int(np.count_nonzero(~np.isin(ids, mine))))
+                         left_home=int(np.count_nonzero(~np.isin(ids, mine))),
+                         launches=ops.kernel_launches, noops=ops.noop_launches)
     finally:
         dist.destroy_process_group()
 
@@ -62,12 +63,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_run_matches_single_domain_oracle(world):
+@pytest.mark.parametrize("world,advance", [(2, False), (3, False), (2, True), (3, True)])
+def test_slab_run_matches_single_domain_oracle(world, advance):
+    """advance = one-launch steps: gated force+finalize+integrate launches queued before
+    the (all-reduced) rebuild flag is known, position ping-pong, flag words alternating."""
     from oracle import oracle as orc
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, advance), nprocs=world, join=True)
     res = [out[r] for r in range(world)]
 
     pos, vel, edges = global_system(world)
@@ -83,6 +86,9 @@ def test_slab_run_matches_single_domain_oracle(world):
     assert sum(r["left_home"] for r in res) > 0                # migration really happened
     assert all(r["rebuilds"] >= 3 for r in res)
     assert res[0]["stride"] > 24                               # collective stride growth
+    if advance:
+        # every rank saw the same gated launches return at once (one per rebuild in the loop)
+        assert len({r["noops"] for r in res}) == 1 and res[0]["noops"] >= 2
     got_pos = np.concatenate([r["pos"] for r in res])[np.argsort(ids)]
     got_vel = np.concatenate([r["vel"] for r in res])[np.argsort(ids)]
     # same arithmetic, different summation order of the pair terms
