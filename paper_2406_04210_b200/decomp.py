@@ -9,10 +9,14 @@ global periodic box, so the cell / list / force kernels run unchanged (rows are
 built and forces evaluated for owned rows only; the list is full, so ghosts need
 positions only and no force is ever sent back).
 
-Per step (no rebuild):   fused finalize+integrate on owned rows (folds the local
-    displacement test) -> pack the fixed send lists (pos_hi rows) -> NCCL
-    send/recv straight into the ghost rows -> all-reduce(max) of the rebuild flag
-    -> force kernel (launched before the flag is inspected, as in the 1-GPU loop).
+Per step (no rebuild), large slabs: ONE gated launch of the pair force kernel that
+    also finalizes and integrates the owned rows (b2md_force_lj_pairs_advance) ->
+    pack the fixed send lists (pos_hi rows) -> NCCL send/recv straight into the
+    ghost rows -> in-place all-reduce(max) of the flag word the kernel wrote; the
+    host reads the status block on a side stream while the next launch is already
+    queued (SlabSimulation._run_advance).
+Small slabs / sample steps: fused finalize+integrate -> flag all-reduce -> halo ->
+    force kernel (launched before the flag is inspected, as in the 1-GPU loop).
 At a rebuild (all ranks together): migrate rows that left the slab (full
     records), reorder the owned rows (Hilbert), select + exchange ghost records
     (pos_hi, pos_lo), bin, build the list for owned rows, forces.
@@ -802,7 +806,10 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
                        "step_hbm_fraction_per_gpu": step_bytes * value / n_total / 1e9 / peak,
                        "final_energy_per_particle": sample["total_energy"] / n_total},
             "clocks": clock_info, "gpu_launches": int(launches.item()),
-            "roofline": {"bound": "hbm", "kernel": "k_force_lj", "achieved": None, "peak": peak,
+            "roofline": {"bound": "hbm",
+                         "kernel": "k_force_lj_pair<ADVANCE> (one launch per MD step on the "
+                                   "owned rows)" if ops.can_advance else "k_force_lj",
+                         "achieved": None, "peak": peak,
                          "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src,
                          "note": "per-kernel roofline is measured by the 1-GPU arm"},
             "e2e": {"value": value, "unit": metric, "h2d_bytes_per_step": 0,
