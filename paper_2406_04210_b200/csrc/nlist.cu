@@ -26,6 +26,7 @@ struct ListGeom {
     double rl2;
     // fp32 pre-test:  r2f < rl2_in  => certainly listed,  r2f > rl2_out => certainly not.
     float rl2_in, rl2_out;
+    float rl2_in_b, rl2_out_b;   // tighter band of the ballot kernel (no fp32 min-image step)
     float Lf[3], invLf[3];
     float margin[3];   // boundary flag: within this distance of a periodic face
     float Lhi[3];
@@ -530,7 +531,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
     const int cx = (int)(c / ((int64_t)g.nc[2] * g.nc[1]));
     const int i_begin = cell_start[c], i_end = cell_start[c + 1];
     if (i_begin == i_end) return;
-    const float rl2_in = g.rl2_in, rl2_out = g.rl2_out;
+    const float rl2_in = g.rl2_in_b, rl2_out = g.rl2_out_b;
 
     // visiting order: neighbour cells by ascending first-occupant index (lane s = slot s)
     int my_key = 0x7fffffff, my_begin = 0, my_size = 0, my_wrap = 0;
@@ -677,6 +678,10 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                     const int32_t *my_stream = s_stream;         // advanced with the mask word
                     int left = my_chunks - 1;                    // mask words not yet fetched
                     unsigned m = active ? my_mask[0] : 0u;
+                    // row index space: entry k of this row lives at nbr[k * pitch + i]
+                    const unsigned row_i = (unsigned)(active ? i : 0);
+                    const unsigned upitch = (unsigned)pitch;
+                    const bool small = (uint64_t)pitch * (uint64_t)(stride + 1) < 0xffffffffull;
                     for (;;) {
                         if (m == 0u && left > 0) {               // next word (1 % are empty)
                             m = *++my_mask;
@@ -684,14 +689,28 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                             --left;
                         }
                         if (!__any_sync(0xffffffffu, (m != 0u) | (left > 0))) break;
+                        if (small) {
+                            // branch-free body (predicated store, 32-bit element offsets):
+                            // 12 instead of 21 instructions per entry
 #pragma unroll
-                        for (int rep = 0; rep < 3; ++rep) {      // amortise the vote
-                            if (m != 0u) {
-                                const int j = my_stream[__ffs(m) - 1] & 0x03ffffff;
+                            for (int rep = 0; rep < 4; ++rep) {  // amortise the vote
+                                const bool has = m != 0u;
+                                const int j = my_stream[(__ffs(m) - 1) & 31] & 0x03ffffff;
                                 m &= m - 1u;
-                                if (found < stride) *out = j;
-                                out += pitch;
-                                ++found;
+                                if (has && found < stride)
+                                    nbr[(unsigned)found * upitch + row_i] = j;
+                                found += has ? 1 : 0;
+                            }
+                        } else {
+#pragma unroll
+                            for (int rep = 0; rep < 3; ++rep) {
+                                if (m != 0u) {
+                                    const int j = my_stream[__ffs(m) - 1] & 0x03ffffff;
+                                    m &= m - 1u;
+                                    if (found < stride) *out = j;
+                                    out += pitch;
+                                    ++found;
+                                }
                             }
                         }
                     }
@@ -892,6 +911,20 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
     const double band = 4.0 * (3.0 * (2.0 * 1.5 * r_list * ed + ed * ed) + 4.0 * u * 3.0 * g.rl2);
     g.rl2_in = (float)(g.rl2 - band) * (1.0f - 1e-6f);
     g.rl2_out = (float)(g.rl2 + band) * (1.0f + 1e-6f);
+    // Ballot kernel: d = hi_i - fl(hi_j + s), s in {-L_f, 0, +L_f} from the cell image.
+    // Per component, against the exact difference of the double-single positions:
+    //   |lo_i|, |lo_j| <= u*L each, |L_f - L| <= u*L, rounding of hi_j + s <= u*(L + cell)
+    //   <= 1.34*u*L, rounding of the subtraction <= u*|d| <= 0.34*u*L for a pair near the
+    //   threshold (|d| <= r_list <= L/3)  =>  delta <= 4.7*u*L; 6*u*L is used.
+    // r2: sum_k (2|d_k| delta + delta^2) <= 2*sqrt(3)*r_list*delta + 3*delta^2, plus three
+    // roundings of the product / fma chain (<= 4u * r2).  The band is twice that figure
+    // (the shared band above is 7x wider; every chunk with a candidate inside the band
+    // pays the exact fp64 settle loop, 9 % of the kernel's instructions with the wide one).
+    const double db = 6.0 * u * lmax;
+    const double band_b = 2.0 * (2.0 * 1.7320508075688772 * 1.001 * r_list * db + 3.0 * db * db +
+                                 4.0 * u * 3.0 * g.rl2);
+    g.rl2_in_b = (float)(g.rl2 - band_b) * (1.0f - 1e-6f);
+    g.rl2_out_b = (float)(g.rl2 + band_b) * (1.0f + 1e-6f);
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n_rows, kBuildThreads);
     const size_t warp_smem = kCandCap * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
