@@ -532,6 +532,11 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
     const int i_begin = cell_start[c], i_end = cell_start[c + 1];
     if (i_begin == i_end) return;
     const float rl2_in = g.rl2_in_b, rl2_out = g.rl2_out_b;
+    // |r2 - band_mid| <= band_half is implied by rl2_in <= r2 <= rl2_out (the half width is
+    // rounded up generously; a false alarm only costs the exact settle loop)
+    const float band_mid = 0.5f * (rl2_in + rl2_out);
+    const float band_half = 0.5f * (rl2_out - rl2_in) * 1.001f + 4.0e-7f * rl2_out;
+    const unsigned long long mid2 = nl_pk(band_mid, band_mid);
 
     // visiting order: neighbour cells by ascending first-occupant index (lane s = slot s)
     int my_key = 0x7fffffff, my_begin = 0, my_size = 0, my_wrap = 0;
@@ -558,6 +563,11 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
         if (lane >= o) v_end += up;
     }
     const int n_cand = __shfl_sync(0xffffffffu, v_end, 31);
+    // where the cell's own occupants sit in the stream (slot 13 = offset (0,0,0)): row
+    // particle number k of the cell is stream position own_start + k -- its self test is
+    // not excluded pair by pair in phase 1, its bit is cleared afterwards
+    const int own_t = __ffs(__ballot_sync(0xffffffffu, sorted_slot == 13)) - 1;
+    const int own_start = __shfl_sync(0xffffffffu, v_end - v_size, own_t);
     // Is the candidate stream ascending?  (Every visited cell a contiguous index range,
     // ranges in ascending order: true after every Hilbert / cell reorder.)  Rows are
     // then born sorted; otherwise they are sorted after the fact.
@@ -629,7 +639,9 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                     }
                     const unsigned long long qx2 = nl_pk(qx, qx), qy2 = nl_pk(qy, qy),
                                              qz2 = nl_pk(qz, qz);
-                    bool in_band = false;
+                    // distance of r2 from the middle of the guard band, minimum over the
+                    // rows: one packed subtract and two |.|-minimum per row pair
+                    float band_min = 3.0e38f;
                     uint32_t *mask_w = s_mask + w;
 #pragma unroll 2
                     for (int p = 0; p < (ni + 1) >> 1; ++p) {
@@ -639,18 +651,18 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                         const unsigned long long dz = nl_sub2(nl_pk(B.x, B.y), qz2);
                         const unsigned long long r2 =
                             nl_fma2(dz, dz, nl_fma2(dy, dy, nl_mul2(dx, dx)));
-                        float r2a, r2b;
+                        float r2a, r2b, ea, eb;
                         asm("mov.b64 {%0, %1}, %2;" : "=f"(r2a), "=f"(r2b) : "l"(r2));
-                        const bool take_a = (r2a <= rl2_out) && (j != __float_as_int(B.z));
-                        const bool take_b = (r2b <= rl2_out) && (j != __float_as_int(B.w));
-                        in_band |= (take_a && r2a >= rl2_in) || (take_b && r2b >= rl2_in);
-                        const unsigned ha = __ballot_sync(0xffffffffu, take_a);
-                        const unsigned hb = __ballot_sync(0xffffffffu, take_b);
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(ea), "=f"(eb) : "l"(nl_sub2(r2, mid2)));
+                        band_min = fminf(band_min, fminf(fabsf(ea), fabsf(eb)));
+                        const unsigned ha = __ballot_sync(0xffffffffu, r2a <= rl2_out);
+                        const unsigned hb = __ballot_sync(0xffffffffu, r2b <= rl2_out);
                         if (lane == 0) {
                             mask_w[(2 * p) * kMaskPitch] = ha;
                             mask_w[(2 * p + 1) * kMaskPitch] = hb;
                         }
                     }
+                    const bool in_band = band_min <= band_half;
                     if (__any_sync(0xffffffffu, in_band)) {
                         // guard band (a shell ~1e-5 sigma thick): settle with the reference's
                         // exact fp64 sequence and clear the bits that fail
@@ -669,6 +681,11 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                     }
                 }
                 __syncwarp();
+                {   // the row's own particle passed every test of phase 1 (r2 = 0): drop it
+                    const int self = own_start + (i0 - i_begin) + lane - batch0;
+                    if (lane < ni && self >= 0 && self < total)
+                        s_mask[lane * kMaskPitch + (self >> 5)] &= ~(1u << (self & 31));
+                }
                 // ---- phase 2: lane r walks the set bits of row r in stream order
                 // (= ascending j) and stores entry k of its row; all rows are at the
                 // same k, so the column-major stores coalesce across the cell's particles
