@@ -507,9 +507,12 @@ __device__ __forceinline__ unsigned long long nl_fma2(unsigned long long a, unsi
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+#ifndef B2MD_LIST_MIN_BLOCKS
+#define B2MD_LIST_MIN_BLOCKS 4
+#endif
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, B2MD_LIST_MIN_BLOCKS)
 k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
                     int64_t n, int64_t n_rows, const __grid_constant__ ListGeom g,
                     int64_t n_cells, const int32_t *__restrict__ cell_start,
