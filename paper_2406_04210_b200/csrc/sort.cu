@@ -20,8 +20,11 @@ int exclusive_scan_i32(const int32_t *d_in, int32_t *d_out, int64_t n, int32_t *
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kKeysPerThread = 16;
-constexpr int kSortTile = kSortThreads * kKeysPerThread;   // 4096 keys per CTA
+#ifndef B2MD_SORT_KEYS_PER_THREAD
+#define B2MD_SORT_KEYS_PER_THREAD 4
+#endif
+constexpr int kKeysPerThread = B2MD_SORT_KEYS_PER_THREAD;
+constexpr int kSortTile = kSortThreads * kKeysPerThread;   // keys per CTA
 constexpr int kRadix = 256;
 
 // ------------------------------------------------------------------ keys
