@@ -121,43 +121,6 @@ __device__ __forceinline__ float masked_rcp(float r2, float rc2, int e, int bit)
     return out;
 }
 
-// Same arithmetic as lj_pair_single / lj_pair_table from the masked reciprocal on.
-template <bool THERMO>
-__device__ __forceinline__ void lj_apply_single(RowAcc &acc, float dx, float dy, float dz,
-                                                float ir2, const PairParams &p) {
-    const float s2 = p.sig2 * ir2;
-    const float s6 = s2 * s2 * s2;
-    const float t = s6 * fmaf(2.0f, s6, -1.0f);
-    const float g = t * ir2;
-    acc.fx = fmaf(g, dx, acc.fx);
-    acc.fy = fmaf(g, dy, acc.fy);
-    acc.fz = fmaf(g, dz, acc.fz);
-    if (THERMO) {
-        acc.u = fmaf(s6, s6 - 1.0f, acc.u);
-        acc.w += t;
-        acc.cnt += ir2 != 0.0f ? 1 : 0;
-    }
-}
-
-// lj_pair_table with the entry's ownership bit folded into the masked reciprocal
-template <bool THERMO>
-__device__ __forceinline__ void lj_apply_table(RowAcc &acc, float dx, float dy, float dz, float r2,
-                                               int e, int bit, const float4 pa, const float2 pb) {
-    const float ir2 = masked_rcp(r2, pa.y, e, bit);
-    const float s2 = pa.x * ir2;
-    const float s6 = s2 * s2 * s2;
-    const float t = s6 * fmaf(2.0f, s6, -1.0f);
-    const float g = pa.z * t * ir2;
-    acc.fx = fmaf(g, dx, acc.fx);
-    acc.fy = fmaf(g, dy, acc.fy);
-    acc.fz = fmaf(g, dz, acc.fz);
-    if (THERMO) {
-        acc.u = fmaf(pa.w * s6, s6 - 1.0f, acc.u);
-        acc.u += ir2 != 0.0f ? pb.x : 0.0f;
-        acc.w = fmaf(pb.y, t, acc.w);
-    }
-}
-
 template <bool THERMO>
 __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, float dz, float r2,
                                               bool valid, const float4 pa, const float2 pb) {
@@ -443,36 +406,6 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
 // about a third fewer 16-byte gathers and index bytes per particle -- the L1 data
 // pipe, not HBM or issue, limits the one-row kernel -- and one 16-byte index load
 // per four entries instead of four 4-byte ones.
-template <int AXES, bool TABLE, bool THERMO>
-__device__ __forceinline__ void pair_entry(RowAcc &A, RowAcc &B, const float4 pa, const float4 pb,
-                                           int e, const float4 pj, const ForceArgs &a,
-                                           const float4 *s_tab_a, const float2 *s_tab_b,
-                                           int ta_row, int tb_row) {
-    const BoxF &b = a.box;
-    const int tj = TABLE ? __float_as_int(pj.w) : 0;
-    {
-        const float dx = delta<(AXES & 1) != 0>(pa.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-        const float dy = delta<(AXES & 2) != 0>(pa.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-        const float dz = delta<(AXES & 4) != 0>(pa.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        if (TABLE)
-            lj_apply_table<THERMO>(A, dx, dy, dz, r2, e, 1, s_tab_a[ta_row + tj],
-                                   s_tab_b[ta_row + tj]);
-        else
-            lj_apply_single<THERMO>(A, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 1), a.single);
-    }
-    {
-        const float dx = delta<(AXES & 1) != 0>(pb.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-        const float dy = delta<(AXES & 2) != 0>(pb.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-        const float dz = delta<(AXES & 4) != 0>(pb.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        if (TABLE)
-            lj_apply_table<THERMO>(B, dx, dy, dz, r2, e, 2, s_tab_a[tb_row + tj],
-                                   s_tab_b[tb_row + tj]);
-        else
-            lj_apply_single<THERMO>(B, dx, dy, dz, masked_rcp(r2, a.single.rc2, e, 2), a.single);
-    }
-}
 
 // ---- packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2) -------------------------
 // One-species pairs: the two particles of a thread go through identical
@@ -563,6 +496,43 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
     }
 }
 
+// Per-pair-type tables (Kob-Andersen ...): the same packed evaluation with the
+// parameters of (type of 2t, type of j) and (type of 2t+1, type of j) in the two
+// halves.  Operation order per half is lj_pair_table's, so the sums stay bit-identical
+// to the row kernel's.
+template <int AXES, bool THERMO>
+__device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, f32x2 ay,
+                                                        f32x2 az, int e, const float4 pj,
+                                                        const ForceArgs &a,
+                                                        const float4 *s_tab_a,
+                                                        const float2 *s_tab_b, int ta_row,
+                                                        int tb_row) {
+    const BoxF &b = a.box;
+    const int tj = __float_as_int(pj.w);
+    const float4 qa = s_tab_a[ta_row + tj], qb = s_tab_a[tb_row + tj];
+    const f32x2 dx = delta2<(AXES & 1) != 0>(ax, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+    const f32x2 dy = delta2<(AXES & 2) != 0>(ay, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+    const f32x2 dz = delta2<(AXES & 4) != 0>(az, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+    float r2a, r2b;
+    upk(r2, r2a, r2b);
+    const float ia = masked_rcp(r2a, qa.y, e, 1), ib = masked_rcp(r2b, qb.y, e, 2);
+    const f32x2 ir2 = pk(ia, ib);
+    const f32x2 s2 = mul2(pk(qa.x, qb.x), ir2);
+    const f32x2 s6 = mul2(mul2(s2, s2), s2);
+    const f32x2 t = mul2(s6, fma2(pk1(2.0f), s6, pk1(-1.0f)));
+    const f32x2 g = mul2(mul2(pk(qa.z, qb.z), t), ir2);
+    acc.fx = fma2(g, dx, acc.fx);
+    acc.fy = fma2(g, dy, acc.fy);
+    acc.fz = fma2(g, dz, acc.fz);
+    if (THERMO) {
+        const float2 wa = s_tab_b[ta_row + tj], wb = s_tab_b[tb_row + tj];
+        acc.u = fma2(mul2(pk(qa.w, qb.w), s6), add2(s6, pk1(-1.0f)), acc.u);
+        acc.u = add2(acc.u, pk(ia != 0.0f ? wa.x : 0.0f, ib != 0.0f ? wb.x : 0.0f));
+        acc.w = fma2(pk(wa.y, wb.y), t, acc.w);
+    }
+}
+
 
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
@@ -594,21 +564,19 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (TABLE)
-                pair_entry<AXES, TABLE, THERMO>(A, B, pa, pb, ev[u], pj[u], a, s_tab_a, s_tab_b,
-                                                ta_row, tb_row);
+                pair_entry_packed_table<AXES, THERMO>(acc, ax, ay, az, ev[u], pj[u], a, s_tab_a,
+                                                      s_tab_b, ta_row, tb_row);
             else
                 pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, ev[u], pj[u], a);
         }
     }
-    if (!TABLE) {
-        upk(acc.fx, A.fx, B.fx);
-        upk(acc.fy, A.fy, B.fy);
-        upk(acc.fz, A.fz, B.fz);
-        upk(acc.u, A.u, B.u);
-        upk(acc.w, A.w, B.w);
-        A.cnt = acc.cnt_a;
-        B.cnt = acc.cnt_b;
-    }
+    upk(acc.fx, A.fx, B.fx);
+    upk(acc.fy, A.fy, B.fy);
+    upk(acc.fz, A.fz, B.fz);
+    upk(acc.u, A.u, B.u);
+    upk(acc.w, A.w, B.w);
+    A.cnt = acc.cnt_a;
+    B.cnt = acc.cnt_b;
 }
 
 template <bool TABLE, bool THERMO, bool SIG1, bool ADVANCE>
