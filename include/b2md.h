@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 101
+#define B2MD_VERSION 102
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -242,6 +242,29 @@ int b2md_force_lj_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *
                                 int32_t flags, int32_t gate_in_word, int32_t gate_out_word,
                                 b2md_status *d_status, void *stream);
 
+/* b2md_force_lj_pairs_advance with the per-step halo of a slab decomposition fused into
+ * it (the reference has no decomposition).  A particle i
+ * with d_halo_dst_left[i] >= 0 also stores its advanced position high words (16 bytes)
+ * into row d_halo_dst_left[i] of d_halo_out_left, likewise for the right side.  The
+ * buffers are the ghost rows of the neighbour ranks' OUTPUT position buffers, mapped into
+ * this process (CUDA IPC; peer access over NVLink when the ranks own different GPUs), so
+ * the ghost layer needs no pack kernel and no send/recv: the collective that follows the
+ * launch anyway (the all-reduce of the rebuild flag) orders the stores before the
+ * neighbour's next launch.  A launch whose gate is closed stores nothing.  Null slot
+ * arrays = no halo on that side; all four null = b2md_force_lj_pairs_advance. */
+int b2md_force_lj_pairs_advance_halo(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
+                                     void *d_vel, void *d_image_i4, int64_t n,
+                                     const b2md_box *box, double dt, void *d_ref_pos_f4,
+                                     double half_skin2, const int32_t *d_pair_nbr,
+                                     const int32_t *d_pair_counts, int64_t pair_pitch,
+                                     const int32_t *d_nbr, const int32_t *d_counts,
+                                     int64_t pitch, const uint8_t *d_boundary,
+                                     const double *table, int32_t ntypes, int32_t flags,
+                                     int32_t gate_in_word, int32_t gate_out_word,
+                                     const int32_t *d_halo_dst_left, void *d_halo_out_left,
+                                     const int32_t *d_halo_dst_right, void *d_halo_out_right,
+                                     b2md_status *d_status, void *stream);
+
 /* The same for the thread- (or sub-warp-) per-particle kernel b2md_force_lj: small
  * systems, where a step is shorter than a host round trip, queue several of these. */
 int b2md_force_lj_advance(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel,
@@ -343,7 +366,14 @@ int b2md_gather4(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t 
  *   (-half, half); ghost selection (-half + r_ghost, half - r_ghost).
  * b2md_compact_indices: stable stream compaction of the indices whose flag is 1.
  * b2md_flag_neither: out = !(a | b) (rows that stay).
- * Records are then moved with b2md_gather16 and exchanged with NCCL send/recv. */
+ * Records are then moved with b2md_gather16 and exchanged with NCCL send/recv.
+ * b2md_halo_slots: destination slots of the halo fused into the step kernel
+ *   (b2md_force_lj_pairs_advance_halo): d_dst[0..n) = -1, d_dst[d_send_idx[k]] = base + k.
+ * b2md_enable_peer_access: kernels of the current device may access memory of
+ *   peer_device afterwards (synchronous; -2 = no peer path between the two). */
+int b2md_halo_slots(const int32_t *d_send_idx, int64_t n_send, int32_t base, int64_t n,
+                    int32_t *d_dst, void *stream);
+int b2md_enable_peer_access(int32_t peer_device);
 int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n, double centre,
                        double box_x, double lo_cut, double hi_cut, int32_t *d_flag_left,
                        int32_t *d_flag_right, void *stream);

@@ -120,6 +120,8 @@ _SIGNATURES = {
                                      _P, _P, _P]),
     "b2md_compact_scratch_bytes": (c_int64, [c_int64]),
     "b2md_compact_indices": (c_int32, [_P, c_int64, _P, _P, _P, _P]),
+    "b2md_halo_slots": (c_int32, [_P, c_int64, c_int32, c_int64, _P, _P]),
+    "b2md_enable_peer_access": (c_int32, [c_int32]),
     "b2md_flag_neither": (c_int32, [_P, _P, c_int64, _P, _P]),
     "b2md_snapshot": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),
     "b2md_max_displacement": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),
@@ -135,6 +137,11 @@ _SIGNATURES = {
                                               _P, c_double, _P, _P, c_int64, _P, _P, c_int64, _P,
                                               POINTER(c_double), c_int32, c_int32, c_int32,
                                               c_int32, _P, _P]),
+    "b2md_force_lj_pairs_advance_halo": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box),
+                                                   c_double, _P, c_double, _P, _P, c_int64, _P, _P,
+                                                   c_int64, _P, POINTER(c_double), c_int32,
+                                                   c_int32, c_int32, c_int32, _P, _P, _P, _P, _P,
+                                                   _P]),
     "b2md_force_lj_all_pairs": (c_int32, [_P, c_int64, POINTER(Box), POINTER(c_double), c_int32,
                                           _P, _P, _P, _P]),
     "b2md_vv_integrate": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,

@@ -280,6 +280,12 @@ struct AdvanceArgs {
     int4 *image;
     StepConst step;
     int gate_in, gate_out;        // int32 word indices into b2md_status
+    // Slab decomposition, halo fused into the step kernel: a particle whose halo_dst[s][i]
+    // is >= 0 also stores its advanced high words into row halo_dst[s][i] of halo_out[s] --
+    // the ghost rows of a neighbour rank's position buffer, mapped into this process
+    // (peer memory over NVLink).  Null = no halo on that side.
+    const int32_t *halo_dst[2];
+    float4 *halo_out[2];
 };
 
 // Gate of an ADVANCE launch (see AdvanceArgs): true = this launch must not run.
@@ -651,6 +657,12 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo,
                                                    adv.vel, adv.image, adv.step, adv.ref_pos));
                 adv.pos_out[i] = h;
+#pragma unroll
+                for (int side = 0; side < 2; ++side)
+                    if (adv.halo_dst[side]) {              // kernel-uniform
+                        const int slot = adv.halo_dst[side][i];
+                        if (slot >= 0) adv.halo_out[side][slot] = h;
+                    }
             } else {
                 force[i] = make_float4(fx, fy, fz, u);
                 if (THERMO && virial) virial[i] = w;
@@ -961,6 +973,8 @@ int fill_advance(AdvanceArgs &adv, const void *d_pos_hi, void *d_pos_hi_out, voi
     adv.step = make_step(box, dt, half_skin2);
     adv.gate_in = gate_in_word;
     adv.gate_out = gate_out_word;
+    adv.halo_dst[0] = adv.halo_dst[1] = nullptr;
+    adv.halo_out[0] = adv.halo_out[1] = nullptr;
     return 0;
 }
 
@@ -1010,11 +1024,34 @@ B2MD_EXPORT int b2md_force_lj_pairs_advance(
     const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
     const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
     int32_t gate_out_word, b2md_status *d_status, void *stream) {
+    return b2md_force_lj_pairs_advance_halo(
+        d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, n, box, dt, d_ref_pos_f4, half_skin2,
+        d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts, pitch, d_boundary, table, ntypes,
+        flags, gate_in_word, gate_out_word, nullptr, nullptr, nullptr, nullptr, d_status, stream);
+}
+
+B2MD_EXPORT int b2md_force_lj_pairs_advance_halo(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
+    int32_t gate_out_word, const int32_t *d_halo_dst_left, void *d_halo_out_left,
+    const int32_t *d_halo_dst_right, void *d_halo_out_right, b2md_status *d_status,
+    void *stream) {
     AdvanceArgs adv;
     int rc = fill_advance(adv, d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, box, dt,
                           d_ref_pos_f4, half_skin2, gate_in_word, gate_out_word,
                           "b2md_force_lj_pairs_advance");
     if (rc) return rc;
+    if ((d_halo_dst_left && !d_halo_out_left) || (d_halo_dst_right && !d_halo_out_right)) {
+        set_error("b2md_force_lj_pairs_advance_halo: destination slots without a buffer");
+        return -1;
+    }
+    adv.halo_dst[0] = d_halo_dst_left;
+    adv.halo_out[0] = (float4 *)d_halo_out_left;
+    adv.halo_dst[1] = d_halo_dst_right;
+    adv.halo_out[1] = (float4 *)d_halo_out_right;
     return launch_pairs(d_pos_hi, n, box, d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts,
                         pitch, d_boundary, table, ntypes, flags | B2MD_FORCE_SKIP_THERMO, nullptr,
                         nullptr, d_status, &adv, stream, "b2md_force_lj_pairs_advance");

@@ -47,9 +47,59 @@ __global__ void k_flag_not_either(const int32_t *__restrict__ a, const int32_t *
     if (i < n) out[i] = (a[i] | b[i]) ? 0 : 1;
 }
 
+// Destination slots of the fused per-step halo: dst[i] = -1 for every owned row, then
+// dst[send_idx[k]] = base + k (row k of the send list lands in ghost row base + k of the
+// neighbour rank).
+__global__ void k_halo_slots(const int32_t *__restrict__ send_idx, int64_t n_send, int32_t base,
+                             int64_t n, int32_t *__restrict__ dst, bool fill) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (fill) {
+        if (i < n) dst[i] = -1;
+    } else if (i < n_send) {
+        dst[send_idx[i]] = base + (int32_t)i;
+    }
+}
+
 }  // namespace b2md
 
 using namespace b2md;
+
+B2MD_EXPORT int b2md_halo_slots(const int32_t *d_send_idx, int64_t n_send, int32_t base,
+                                int64_t n, int32_t *d_dst, void *stream) {
+    if (n < 0 || n_send < 0 || n_send > n || base < 0 || !d_dst || (n_send && !d_send_idx)) {
+        set_error("b2md_halo_slots: bad arguments");
+        return -1;
+    }
+    if (n == 0) return 0;
+    k_halo_slots<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        d_send_idx, n_send, base, n, d_dst, true);
+    B2MD_CHECK_LAUNCH("b2md_halo_slots");
+    if (n_send) {
+        k_halo_slots<<<blocks_for(n_send, kThreads), kThreads, 0, as_stream(stream)>>>(
+            d_send_idx, n_send, base, n, d_dst, false);
+        B2MD_CHECK_LAUNCH("b2md_halo_slots");
+    }
+    return 0;
+}
+
+// Kernels of the CURRENT device may load / store memory of `peer_device` afterwards
+// (NVLink / NVSwitch peer access).  Same device, or already enabled: ok.
+B2MD_EXPORT int b2md_enable_peer_access(int32_t peer_device) {
+    int dev = -1;
+    int rc = check_cuda(cudaGetDevice(&dev), "b2md_enable_peer_access");
+    if (rc) return rc;
+    if (dev == peer_device) return 0;
+    int can = 0;
+    rc = check_cuda(cudaDeviceCanAccessPeer(&can, dev, peer_device), "b2md_enable_peer_access");
+    if (rc) return rc;
+    if (!can) {
+        set_error("b2md_enable_peer_access: device %d cannot access device %d", dev, peer_device);
+        return -2;
+    }
+    cudaError_t err = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (err == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); return 0; }
+    return check_cuda(err, "b2md_enable_peer_access");
+}
 
 B2MD_EXPORT int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                                    double centre, double box_x, double lo_cut, double hi_cut,

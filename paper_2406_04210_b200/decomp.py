@@ -97,12 +97,18 @@ class SlabComm:
 
     def exchange_counts(self, n_left: int, n_right: int, device):
         """Tell each neighbour how many records it will receive."""
+        got_l, got_r = self.exchange_ints([n_left], [n_right], device)
+        return got_l[0], got_r[0]
+
+    def exchange_ints(self, to_left, to_right, device):
+        """Small integer vectors to both neighbours; returns (from_left, from_right)."""
         torch = _torch()
-        send = torch.tensor([n_left, n_right], dtype=torch.int64, device=device)
-        got_from_right = torch.zeros(1, dtype=torch.int64, device=device)
-        got_from_left = torch.zeros(1, dtype=torch.int64, device=device)
-        self._ring(send[0:1], send[1:2], got_from_right, got_from_left)
-        return int(got_from_left.item()), int(got_from_right.item())
+        k = len(to_left)
+        send = torch.tensor([list(to_left), list(to_right)], dtype=torch.int64, device=device)
+        got_from_right = torch.zeros(k, dtype=torch.int64, device=device)
+        got_from_left = torch.zeros(k, dtype=torch.int64, device=device)
+        self._ring(send[0], send[1], got_from_right, got_from_left)
+        return got_from_left.tolist(), got_from_right.tolist()
 
     def _ring(self, to_left, to_right, from_right, from_left):
         """to_left -> left neighbour (arrives as its from_right), to_right -> right."""
@@ -180,6 +186,12 @@ class SlabSimulation:
         self.ahead = False            # one-launch steps: particles already at the next step
         self.halo_rows = (0, 0)
         self.ops.attach(self.geo, lj, self.dt, self.skin)
+        # Per-step halo fused into the step kernel (backends with `connect_peers`): the
+        # advanced high words of the send-list rows are stored by the kernel itself into
+        # the ghost rows of the neighbour ranks' position buffers, mapped into this process
+        # (peer memory over NVLink) -- no pack kernels, no send/recv inside a step.
+        connect = getattr(self.ops, "connect_peers", None)
+        self.fused_halo = bool(connect(comm)) if connect else False
         self._rebuild()
         self.ops.force(thermo=True)
 
@@ -204,6 +216,15 @@ class SlabSimulation:
         comm.exchange(out_l, out_r, in_l, in_r)
         ops.set_ghosts(in_l, in_r)
         self.halo_rows = (got_l, got_r)
+        if self.fused_halo:
+            # where my send lists land on the neighbours: what I send leftwards is the left
+            # neighbour's "from the right" ghost range, and vice versa; the neighbours must
+            # also be at the same point of the position-buffer rotation as this rank
+            start_l, start_r, live = ops.ghost_row_starts()
+            from_l, from_r = comm.exchange_ints([start_l, live], [start_r, live], ops.device)
+            if from_l[1] != live or from_r[1] != live:
+                raise ConfigError("slab ranks disagree on the live position buffer")
+            ops.set_halo_targets(base_left=from_l[0], base_right=from_r[0])
         # 4. cells + list for the owned rows; every rank grows together on overflow
         while True:
             overflow, max_count = ops.build_list()
@@ -261,7 +282,8 @@ class SlabSimulation:
         ops, comm = self.ops, self.comm
         ops.advance()                      # reads the current buffer, writes the other one
         ops.swap_positions()               # ... which now is the current one
-        self._halo()                       # ghost rows of the new buffer
+        if not self.fused_halo:            # (fused: the launch stored them on the neighbours)
+            self._halo()                   # ghost rows of the new buffer
         comm.all_max(ops.gate_word_out())  # the flag of the new positions, all ranks agree
 
     def _run_advance(self, n_steps: int):
@@ -344,6 +366,14 @@ class CudaSlabOps:
         self.copy_stream = torch.cuda.Stream(self.device)
         self.copy_done = torch.cuda.Event()
         self.gate_in = 5              # int32 word of the status block: 5 = rebuild_flag
+        # the three position buffers rotate (reorder / migration flip the set, a step swaps
+        # the live one with pos_alt); every rank goes through the same rotation, so a buffer
+        # is named by its index here on all ranks (fused halo, connect_peers)
+        self.pos_bufs = [self.sets[0]["pos_hi"], self.sets[1]["pos_hi"], self.pos_alt]
+        self.pos_index = {t.data_ptr(): k for k, t in enumerate(self.pos_bufs)}
+        self.peer_pos = None          # [left, right] -> the neighbour's three buffers, mapped
+        self.halo_dst = None
+        self.peer_bytes = 0
         self.box = _lib.make_box(self.edges)
         # upload through the same conversion kernels as the single-GPU path
         a = self.sets[0]
@@ -652,6 +682,63 @@ class CudaSlabOps:
                   self.virial.data_ptr(), self.status.data_ptr(), self.stream)
         self.kernel_launches += 1
 
+    # -- halo fused into the step kernel (peer memory) ---------------------------------
+    def connect_peers(self, comm) -> bool:
+        """Map the position buffers of both neighbour ranks into this process (CUDA IPC
+        handles exchanged over the process group; peer access over NVLink when the ranks
+        own different GPUs).  Collective; True when every rank succeeded, otherwise every
+        rank keeps the NCCL send/recv halo.  B2MD_SLAB_HALO=nccl turns it off."""
+        import os
+        torch = self.torch
+        geo = comm.geo
+        if geo.world == 1:
+            return False
+        from torch.multiprocessing.reductions import reduce_tensor
+        willing = self.can_advance and os.environ.get("B2MD_SLAB_HALO", "peer").lower() != "nccl"
+        handles = [None] * geo.world
+        comm.dist.all_gather_object(
+            handles, [reduce_tensor(t) for t in self.pos_bufs] if willing else None,
+            group=comm.group)
+        if any(h is None for h in handles):
+            self.peer_halo_unavailable = "turned off, or a rank's slab is too small for " \
+                                         "one-launch steps"
+            return False
+        failed, peers, why = 0, [], ""
+        try:
+            with torch.cuda.device(self.device):
+                mapped = {}
+                for rank in (geo.left, geo.right):
+                    if rank not in mapped:
+                        mapped[rank] = [fn(*args) for fn, args in handles[rank]]
+                        for t in mapped[rank]:
+                            _lib.call("b2md_enable_peer_access", int(t.device.index))
+                    peers.append(mapped[rank])
+        except Exception as exc:          # noqa: BLE001 -- any failure = use NCCL, on all ranks
+            failed, why = 1, f"{type(exc).__name__}: {exc}"
+        flag = comm.all_max(torch.tensor([failed], dtype=torch.int64, device=self.device))
+        if int(flag.item()):
+            self.peer_halo_unavailable = why or "a neighbour rank could not map peer memory"
+            return False
+        self.peer_pos = peers
+        self.halo_dst = [torch.full((self.cap_own,), -1, dtype=torch.int32, device=self.device)
+                         for _ in range(2)]
+        return True
+
+    def ghost_row_starts(self):
+        """(first ghost row from the left, first from the right, index of the live buffer)."""
+        (l0, _), (r0, _) = self.ghost_ranges
+        return l0, r0, self.pos_index[self.a["pos_hi"].data_ptr()]
+
+    def set_halo_targets(self, base_left: int, base_right: int):
+        for side, (idx, count, base, dst) in enumerate(
+                ((self.idx_l, self.n_send[0], base_left, self.halo_dst[0]),
+                 (self.idx_r, self.n_send[1], base_right, self.halo_dst[1]))):
+            if base + count > self.peer_pos[side][0].shape[0]:
+                raise ConfigError("ghost capacity of a neighbour rank exceeded")
+            _lib.call("b2md_halo_slots", idx.data_ptr(), count, int(base), self.n_own,
+                      dst.data_ptr(), self.stream)
+            self.kernel_launches += 2 if count else 1
+
     # -- one-launch steps (see SlabSimulation._run_advance) ------------------------
     GATE_WORDS = (5, 12)              # rebuild_flag, reserved[0] (include/b2md.h)
 
@@ -675,13 +762,21 @@ class CudaSlabOps:
     def advance(self):
         a = self.a
         half_skin2 = (0.5 * self.skin) ** 2
-        _lib.call("b2md_force_lj_pairs_advance", a["pos_hi"].data_ptr(), self.pos_alt.data_ptr(),
-                  a["pos_lo"].data_ptr(), a["vel"].data_ptr(), a["image"].data_ptr(), self.n_own,
-                  ctypes.byref(self.box), self.dt, self.ref_pos.data_ptr(), half_skin2,
-                  self.pair_nbr.data_ptr(), self.pair_counts.data_ptr(), self.pair_pitch,
-                  self.nbr.data_ptr(), self.counts.data_ptr(), self.capacity,
-                  self.boundary.data_ptr(), self.table_ptr, self.lj.ntypes, 0, self.gate_in,
-                  self.gate_out, self.status.data_ptr(), self.stream)
+        halo = (None, None, None, None)
+        if self.peer_pos is not None:
+            # the neighbours write their new positions into the buffer with the same index
+            k = self.pos_index[self.pos_alt.data_ptr()]
+            halo = (self.halo_dst[0].data_ptr(), self.peer_pos[0][k].data_ptr(),
+                    self.halo_dst[1].data_ptr(), self.peer_pos[1][k].data_ptr())
+            self.peer_bytes += 16 * (self.n_send[0] + self.n_send[1])
+        _lib.call("b2md_force_lj_pairs_advance_halo", a["pos_hi"].data_ptr(),
+                  self.pos_alt.data_ptr(), a["pos_lo"].data_ptr(), a["vel"].data_ptr(),
+                  a["image"].data_ptr(), self.n_own, ctypes.byref(self.box), self.dt,
+                  self.ref_pos.data_ptr(), half_skin2, self.pair_nbr.data_ptr(),
+                  self.pair_counts.data_ptr(), self.pair_pitch, self.nbr.data_ptr(),
+                  self.counts.data_ptr(), self.capacity, self.boundary.data_ptr(), self.table_ptr,
+                  self.lj.ntypes, 0, self.gate_in, self.gate_out, *halo, self.status.data_ptr(),
+                  self.stream)
         self.kernel_launches += 1
 
     def swap_positions(self):
@@ -764,6 +859,7 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
     sim = SlabSimulation(ops, SlabComm(geo), lj, dt, skin, sample_interval=100)
     sim.run(args.warmup)
     ops.kernel_launches = 0
+    ops.peer_bytes = 0
     sim.comm.bytes_sent = 0
     rebuilds0 = sim.rebuilds
     stream = torch.cuda.current_stream()
@@ -818,5 +914,9 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
                             "before the timed region; 8 doubles all-reduced and read back per "
                             "sample"},
             "nccl_bytes_sent_rank0_per_step": sim.comm.bytes_sent / max(args.steps, 1),
+            "halo": {"transport": "peer stores from the step kernel (CUDA IPC, NVLink)"
+                     if sim.fused_halo else "NCCL send/recv",
+                     "peer_bytes_stored_rank0_per_step": ops.peer_bytes / max(args.steps, 1),
+                     "why_not_peer": getattr(ops, "peer_halo_unavailable", None)},
         }
         print(json.dumps(line))

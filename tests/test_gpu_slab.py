@@ -30,8 +30,8 @@ def global_system(world):
     return q32(pos), q32(vel), (edge * world, edge, edge)
 
 
-def _worker(rank, world, port, out, advance, pair_rows):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, port, out, advance, pair_rows, halo="peer"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), B2MD_SLAB_HALO=halo)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2406_04210_b200 as b2
@@ -50,7 +50,10 @@ def _worker(rank, world, port, out, advance, pair_rows):
         out[rank] = dict(ids=ids, pos=p, vel=v, samples=[first] + sim.samples,
                          rebuilds=sim.rebuilds, stride=ops.stride, halo=sim.halo_rows,
                          left_home=int(np.count_nonzero(~np.isin(ids, mine))),
-                         launches=ops.kernel_launches)
+                         launches=ops.kernel_launches, fused_halo=sim.fused_halo,
+                         peer_bytes=ops.peer_bytes, nccl_bytes=sim.comm.bytes_sent,
+                         why=getattr(ops, "peer_halo_unavailable", None))
+        del sim, ops                 # peer mappings go before the process group
     finally:
         dist.destroy_process_group()
 
@@ -61,10 +64,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(world, advance, pair_rows=None):
+def _run(world, advance, pair_rows=None, halo="peer"):
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out, advance, pair_rows or advance or None),
+    mp.spawn(_worker, args=(world, _free_port(), out, advance, pair_rows or advance or None, halo),
              nprocs=world, join=True)
     return [out[r] for r in range(world)]
 
@@ -85,6 +88,24 @@ def test_one_launch_slab_steps_are_bit_identical_to_separate_launches(world):
             [s["total_energy"] for s in rb["samples"]]
         # separate launches: integrate + force (+ halo gathers) per step; one launch: one
         assert rb["launches"] < ra["launches"] - STEPS // 2
+
+
+def test_halo_stored_by_the_step_kernel_matches_the_nccl_halo():
+    """The step kernel stores the advanced positions of the send-list rows straight into
+    the neighbour's ghost rows (its buffers mapped through CUDA IPC): same trajectory, bit
+    for bit, as pack + send/recv, with no halo launches and no halo messages."""
+    a, b = _run(2, True, halo="nccl"), _run(2, True, halo="peer")
+    for ra, rb in zip(a, b):
+        assert not ra["fused_halo"] and ra["peer_bytes"] == 0
+        assert rb["fused_halo"], rb["why"]
+        assert rb["peer_bytes"] > 0 and rb["nccl_bytes"] < ra["nccl_bytes"]
+        assert np.array_equal(ra["ids"], rb["ids"])
+        assert np.array_equal(ra["pos"], rb["pos"])
+        assert np.array_equal(ra["vel"], rb["vel"])
+        assert ra["rebuilds"] == rb["rebuilds"] and ra["halo"] == rb["halo"]
+        assert [s["total_energy"] for s in ra["samples"]] == \
+            [s["total_energy"] for s in rb["samples"]]
+        assert rb["launches"] < ra["launches"] - STEPS       # two pack launches less per step
 
 
 @pytest.mark.parametrize("world,advance", [(1, False), (2, False), (2, True)])
