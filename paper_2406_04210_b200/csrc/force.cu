@@ -585,7 +585,9 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     B.cnt = acc.cnt_b;
 }
 
-template <bool TABLE, bool THERMO, bool SIG1, bool ADVANCE>
+// ADVANCE: 0 = forces only, 1 = one-launch step, 2 = one-launch step that also stores the
+// slab halo into the neighbour ranks' ghost rows (AdvanceArgs::halo_*)
+template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE>
 __global__ void __launch_bounds__(kForceThreads, 8)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
@@ -657,12 +659,14 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo,
                                                    adv.vel, adv.image, adv.step, adv.ref_pos));
                 adv.pos_out[i] = h;
+                if (ADVANCE == 2) {
 #pragma unroll
-                for (int side = 0; side < 2; ++side)
-                    if (adv.halo_dst[side]) {              // kernel-uniform
-                        const int slot = adv.halo_dst[side][i];
-                        if (slot >= 0) adv.halo_out[side][slot] = h;
-                    }
+                    for (int side = 0; side < 2; ++side)
+                        if (adv.halo_dst[side]) {          // kernel-uniform
+                            const int slot = __ldg(&adv.halo_dst[side][i]);
+                            if (slot >= 0) adv.halo_out[side][slot] = h;
+                        }
+                }
             } else {
                 force[i] = make_float4(fx, fy, fz, u);
                 if (THERMO && virial) virial[i] = w;
@@ -918,20 +922,27 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     // or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
     const bool sig1 = a.single.sig2 == 1.0f;
-    if (advance) {
+    if (advance && (adv.halo_dst[0] || adv.halo_dst[1])) {
         if (ntypes == 1) {
-            if (sig1) B2MD_LAUNCH_PAIR(false, false, true, true);
-            else B2MD_LAUNCH_PAIR(false, false, false, true);
+            if (sig1) B2MD_LAUNCH_PAIR(false, false, true, 2);
+            else B2MD_LAUNCH_PAIR(false, false, false, 2);
         } else {
-            B2MD_LAUNCH_PAIR(true, false, false, true);
+            B2MD_LAUNCH_PAIR(true, false, false, 2);
+        }
+    } else if (advance) {
+        if (ntypes == 1) {
+            if (sig1) B2MD_LAUNCH_PAIR(false, false, true, 1);
+            else B2MD_LAUNCH_PAIR(false, false, false, 1);
+        } else {
+            B2MD_LAUNCH_PAIR(true, false, false, 1);
         }
     } else if (ntypes == 1) {
-        if (thermo) B2MD_LAUNCH_PAIR(false, true, false, false);
-        else if (sig1) B2MD_LAUNCH_PAIR(false, false, true, false);
-        else B2MD_LAUNCH_PAIR(false, false, false, false);
+        if (thermo) B2MD_LAUNCH_PAIR(false, true, false, 0);
+        else if (sig1) B2MD_LAUNCH_PAIR(false, false, true, 0);
+        else B2MD_LAUNCH_PAIR(false, false, false, 0);
     } else {
-        if (thermo) B2MD_LAUNCH_PAIR(true, true, false, false);
-        else B2MD_LAUNCH_PAIR(true, false, false, false);
+        if (thermo) B2MD_LAUNCH_PAIR(true, true, false, 0);
+        else B2MD_LAUNCH_PAIR(true, false, false, 0);
     }
 #undef B2MD_LAUNCH_PAIR
     int rc2 = check_cuda(cudaPeekAtLastError(), name);
