@@ -199,9 +199,26 @@ def run_gpu_arm(args):
             dist.init_process_group("nccl", rank=0, world_size=1,
                                     device_id=torch.device("cuda", local_rank))
         from paper_2406_04210_b200.decomp import run_slab_benchmark
-        run_slab_benchmark(args, rank, world, local_rank, N_PER_GPU, WORKLOAD, METRIC,
-                           measured_peak, ClockSampler)
-        dist.destroy_process_group()
+        # default: weak scaling, 1 M particles per GPU; --total-particles T fixes the job size
+        # instead (BASELINE.json configs[4]: T = 16 M over 2 / 4 / 8 GPUs)
+        n_rank = args.particles_per_gpu or N_PER_GPU
+        if args.total_particles:
+            n_rank = args.total_particles // world
+        # NCCL writes its version banner to stdout: keep fd 1 clean for the one JSON line
+        sys.stdout.flush()
+        real_stdout = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            line = run_slab_benchmark(args, rank, world, local_rank, n_rank, WORKLOAD, METRIC,
+                                      measured_peak, ClockSampler,
+                                      scaling="strong" if args.total_particles else "weak")
+            dist.destroy_process_group()
+        finally:
+            sys.stdout.flush()
+            os.dup2(real_stdout, 1)
+            os.close(real_stdout)
+        if line is not None:
+            print(json.dumps(line))
         return
 
     n = N_PER_GPU
@@ -413,6 +430,10 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--particles-per-gpu", type=int, default=0,
+                    help="slab arm (--gpus > 1 or --force-slab): particles per rank (default 1 M)")
+    ap.add_argument("--total-particles", type=int, default=0,
+                    help="slab arm: fixed job size split over the ranks (strong scaling)")
     ap.add_argument("--force-slab", action="store_true",
                     help="run the slab-decomposed driver even on one rank (validation)")
     args = ap.parse_args()

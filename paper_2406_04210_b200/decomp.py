@@ -846,8 +846,10 @@ def slab_initial_state(rank, world, n_per_rank, density, temperature, seed=42):
 
 
 def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metric,
-                       measured_peak, clock_sampler_cls):
-    """bench.py's N > 1 arm: weak scaling, 1 M particles per rank."""
+                       measured_peak, clock_sampler_cls, scaling="weak"):
+    """bench.py's N > 1 arm: `n_per_rank` particles per rank (weak scaling: 1 M per rank;
+    strong scaling: a fixed total split over the ranks).  Returns the JSON line (a dict) on
+    rank 0, None elsewhere."""
     torch = _torch()
     import torch.distributed as dist
     from .potential import make_shifted
@@ -889,10 +891,11 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
         line = {
             "metric": metric, "value": value, "unit": metric, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f32 pair arithmetic, double-single positions, f64 reductions",
             "data": "synthetic",
             "config": {"workload": workload, "particles": n_total,
+                       "particles_per_gpu": n_per_rank,
                        "decomposition": f"{world} x-slabs of a {edges[0]:.1f} x {edges[1]:.1f} x "
                                         f"{edges[2]:.1f} box, ghost width {sim.r_list}",
                        "halo_rows_per_face": list(sim.halo_rows),
@@ -919,4 +922,5 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
                      "peer_bytes_stored_rank0_per_step": ops.peer_bytes / max(args.steps, 1),
                      "why_not_peer": getattr(ops, "peer_halo_unavailable", None)},
         }
-        print(json.dumps(line))
+        return line
+    return None
