@@ -26,6 +26,8 @@ ap.add_argument("--reorder", default="hilbert")
 ap.add_argument("--density", type=float, default=0.75)
 ap.add_argument("--reorder-every", type=int, default=1)
 ap.add_argument("--graph", type=int, default=0)
+ap.add_argument("--profiler-range", action="store_true",
+                help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
 args = ap.parse_args()
 
 st, box = b2.init_lattice_any(args.n, args.density)
@@ -38,10 +40,14 @@ if args.melt:
     sim.run(args.melt)
 torch.cuda.synchronize()
 start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+if args.profiler_range:
+    torch.cuda.profiler.start()
 start.record()
 sim.run(args.steps)
 stop.record()
 torch.cuda.synchronize()
+if args.profiler_range:
+    torch.cuda.profiler.stop()
 ms = start.elapsed_time(stop)
 print(f"n={args.n} steps={args.steps} ms/step={ms / args.steps:.4f} "
       f"particle-steps/s={args.n * args.steps / ms * 1e3:.3e} rebuilds={sim.rebuild_count} "
