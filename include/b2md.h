@@ -355,6 +355,12 @@ int b2md_sort_pairs_u64(uint64_t *d_keys, int32_t *d_vals, uint64_t *d_keys_tmp,
                         void *d_scratch, void *stream);
 int b2md_gather16(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
 int b2md_gather4(const void *d_src, void *d_dst, const int32_t *d_perm, int64_t n, void *stream);
+/* reorder_by_cell's "every buffer through the same permutation" (neighbor.py:267-269) in one
+ * launch: dst16[a][k] = src16[a][perm[k]] for five 16-byte-row arrays (host arrays of five
+ * device pointers: pos_hi, pos_lo, vel, force, image), dst4[k] = src4[perm[k]] (virial;
+ * may be null). */
+int b2md_gather_rows(const void *const *d_src16, void *const *d_dst16, const void *d_src4,
+                     void *d_dst4, const int32_t *d_perm, int64_t n, void *stream);
 
 /* ---------------------------------------------- slab decomposition (multi-GPU)
  * No counterpart in the reference; SURVEY.md section 8e.  A rank

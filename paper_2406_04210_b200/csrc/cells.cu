@@ -141,12 +141,33 @@ __global__ void k_scatter(const int32_t *__restrict__ cell_of, const int32_t *__
     cell_particles[cell_start[cell_of[i]] + slot[i]] = (int32_t)i;
 }
 
-// One thread per cell: insertion sort of its (short) occupant slice.
+// One thread per cell: ascending order of its (short) occupant slice.  After a Hilbert /
+// cell reorder the occupants of a cell are consecutive rows, so the slice is a permutation
+// of [min, min + m): one read pass finds that out and one write pass stores min + k.
+// Otherwise: insertion sort.
 __global__ void k_sort_cells(const int32_t *__restrict__ cell_start, int64_t n_cells,
                              int32_t *__restrict__ cell_particles) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n_cells) return;
     const int lo = cell_start[c], hi = cell_start[c + 1];
+    if (hi - lo < 2) return;
+    {
+        int vmin = 0x7fffffff, vmax = -1;
+        bool sorted = true;
+        int prev = -1;
+        for (int a = lo; a < hi; ++a) {
+            const int v = cell_particles[a];
+            vmin = min(vmin, v);
+            vmax = max(vmax, v);
+            sorted = sorted && v > prev;
+            prev = v;
+        }
+        if (sorted) return;
+        if (vmax - vmin == hi - lo - 1) {           // distinct indices: a contiguous range
+            for (int a = lo; a < hi; ++a) cell_particles[a] = vmin + (a - lo);
+            return;
+        }
+    }
     for (int a = lo + 1; a < hi; ++a) {
         int v = cell_particles[a];
         int b = a - 1;
@@ -158,14 +179,77 @@ __global__ void k_sort_cells(const int32_t *__restrict__ cell_start, int64_t n_c
     }
 }
 
+// Single-launch scan for up to kFusedScanTiles tiles: a tile takes a ticket (so that
+// every predecessor is already running), scans itself, publishes its total as one 64-bit
+// word {ready, total}, then warp 0 sums the totals of all predecessors (32 per round,
+// polling until each is ready) -- the tile never waits for a predecessor's PREFIX, only
+// for its local total, so the wait is one block scan deep whatever the tile count.
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_fused(const int32_t *__restrict__ in, int64_t n, int32_t *__restrict__ out,
+             unsigned long long *state, int n_tiles) {
+    __shared__ int warp_sums[33];
+    __shared__ int s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&state[n_tiles], 1ull);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        sum += v[k];
+    }
+    int total;
+    int ex = block_exclusive_scan(sum, warp_sums, total);
+    if (threadIdx.x == 0) {
+        *(volatile unsigned long long *)&state[tile] = (1ull << 32) | (unsigned)total;
+        __threadfence();
+    }
+    if (threadIdx.x < 32) {
+        int prefix = 0;
+        for (int p0 = 0; p0 < tile; p0 += 32) {
+            const int p = p0 + (int)threadIdx.x;
+            int t = 0;
+            if (p < tile) {
+                unsigned long long w;
+                do { w = *(volatile unsigned long long *)&state[p]; } while ((w >> 32) == 0ull);
+                t = (int)(unsigned)w;
+            }
+            prefix += __reduce_add_sync(0xffffffffu, t);
+        }
+        if (threadIdx.x == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    ex += s_prefix;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) out[base + k] = ex;
+        ex += v[k];
+    }
+    if (tile == n_tiles - 1 && threadIdx.x == 0) out[n] = s_prefix + total;
+}
+
 // Exclusive scan of d_in[0..n) into d_out[0..n], d_out[n] = total.
-// d_tiles: ceil(n/4096)+1 ints of scratch.
+// d_tiles: scan_scratch_ints(n) ints of scratch (common.cuh).
 int exclusive_scan_i32(const int32_t *d_in, int32_t *d_out, int64_t n, int32_t *d_tiles,
                        cudaStream_t stream) {
     const int64_t n_tiles = (n + kScanTile - 1) / kScanTile;
     if (n_tiles > (int64_t)kScanTile * 4096) {
         set_error("exclusive_scan_i32: n=%lld too large", (long long)n);
         return -2;
+    }
+    if (n_tiles >= 1 && n_tiles <= kFusedScanTiles) {
+        unsigned long long *state =
+            (unsigned long long *)(((uintptr_t)d_tiles + 7) & ~(uintptr_t)7);
+        int rc = check_cuda(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (n_tiles + 1),
+                                            stream), "exclusive_scan_i32 memset");
+        if (rc) return rc;
+        k_scan_fused<<<(unsigned)n_tiles, kScanThreads, 0, stream>>>(d_in, n, d_out, state,
+                                                                    (int)n_tiles);
+        B2MD_CHECK_LAUNCH("exclusive_scan_i32");
+        return 0;
     }
     k_scan_tiles<<<(unsigned)n_tiles, kScanThreads, 0, stream>>>(d_in, n, d_out, d_tiles);
     k_scan_totals<<<1, kScanThreads, 0, stream>>>(d_tiles, (int)n_tiles, d_tiles + n_tiles);
@@ -208,8 +292,7 @@ B2MD_EXPORT int b2md_grid_shape(const b2md_box *box, double r_list, b2md_grid *g
 
 B2MD_EXPORT int64_t b2md_bin_scratch_bytes(int64_t n, int64_t n_cells) {
     // counts (n_cells) + slot (n) + scan tiles
-    const int64_t tiles = (n_cells + kScanTile - 1) / kScanTile + 2;
-    return (int64_t)sizeof(int32_t) * (n_cells + n + tiles) + 256;
+    return (int64_t)sizeof(int32_t) * (n_cells + n + scan_scratch_ints(n_cells)) + 256;
 }
 
 B2MD_EXPORT int b2md_bin(const void *d_pos_hi, const void *d_pos_lo, int64_t n,

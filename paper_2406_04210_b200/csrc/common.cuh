@@ -35,6 +35,15 @@ inline unsigned blocks_for(int64_t n, int threads) {
     return (unsigned)((n + threads - 1) / threads);
 }
 
+// Scratch (in int32 units) exclusive_scan_i32 needs for n elements: one 64-bit state word
+// per 4096-element tile plus a ticket, with slack for 8-byte alignment (cells.cu).
+inline int64_t scan_scratch_ints(int64_t n) {
+    return 2 * (((n < 1 ? 1 : n) + 4095) / 4096) + 8;
+}
+// ... and the kernels it launches: one up to kFusedScanTiles tiles, else three.
+constexpr int kFusedScanTiles = 1024;
+inline int scan_launches(int64_t n) { return (n + 4095) / 4096 <= kFusedScanTiles ? 1 : 3; }
+
 // Box constants the fp64 (bit-exact) kernels need: L and 1.0/L formed on the
 // host in fp64 exactly like the reference (neighbor.py:213-214, core.py:44).
 struct BoxD {

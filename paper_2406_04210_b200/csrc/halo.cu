@@ -114,8 +114,7 @@ B2MD_EXPORT int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, i
 }
 
 B2MD_EXPORT int64_t b2md_compact_scratch_bytes(int64_t n) {
-    const int64_t tiles = ((n < 1 ? 1 : n) + 4095) / 4096 + 2;
-    return (int64_t)sizeof(int32_t) * ((n < 1 ? 1 : n) + 1 + tiles) + 256;
+    return (int64_t)sizeof(int32_t) * ((n < 1 ? 1 : n) + 1 + scan_scratch_ints(n)) + 256;
 }
 
 // Stable stream compaction: d_out_idx receives, in ascending order, the indices i

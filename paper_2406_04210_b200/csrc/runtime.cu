@@ -184,7 +184,7 @@ int enqueue_reorder(b2md_runner *r, bool write_back, int64_t *kernels) {
         // cell order needs the cell of every particle first
         rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,
                       c.cell_particles, c.bin_scratch, s);
-        *kernels += 6;
+        *kernels += 3 + scan_launches(r->grid.n_cells);
         if (rc) return rc;
         rc = b2md_cell_keys(c.cell_of, c.n, c.keys, s);
     }
@@ -192,14 +192,13 @@ int enqueue_reorder(b2md_runner *r, bool write_back, int64_t *kernels) {
     if ((rc = b2md_iota_i32(c.perm, c.n, s))) return rc;
     if ((rc = b2md_sort_pairs_u64(c.keys, c.perm, c.keys_tmp, c.perm_tmp, c.n, key_bits,
                                   c.sort_scratch, s))) return rc;
-    *kernels += 2 + 5 * ((key_bits + 7) / 8);
-    if ((rc = b2md_gather16(a.pos_hi, b.pos_hi, c.perm, c.n, s))) return rc;
-    if ((rc = b2md_gather16(a.pos_lo, b.pos_lo, c.perm, c.n, s))) return rc;
-    if ((rc = b2md_gather16(a.vel, b.vel, c.perm, c.n, s))) return rc;
-    if ((rc = b2md_gather16(a.force, b.force, c.perm, c.n, s))) return rc;
-    if ((rc = b2md_gather16(a.image, b.image, c.perm, c.n, s))) return rc;
-    if ((rc = b2md_gather4(a.virial, b.virial, c.perm, c.n, s))) return rc;
-    *kernels += 6;
+    *kernels += 2 + ((key_bits + 7) / 8) * (2 + scan_launches(256 * ((c.n + 1023) / 1024)));
+    {
+        const void *src[5] = {a.pos_hi, a.pos_lo, a.vel, a.force, a.image};
+        void *dst[5] = {b.pos_hi, b.pos_lo, b.vel, b.force, b.image};
+        if ((rc = b2md_gather_rows(src, dst, a.virial, b.virial, c.perm, c.n, s))) return rc;
+    }
+    *kernels += 1;
     if (write_back) {
         const size_t row = 16 * (size_t)c.n;
         void *dst[5] = {a.pos_hi, a.pos_lo, a.vel, a.force, a.image};
@@ -234,7 +233,7 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
         return rc;
     if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos, s)))
         return rc;
-    *kernels += 1 + 6 + 2 + 1;
+    *kernels += 1 + 3 + scan_launches(r->grid.n_cells) + 2 + 1;
     if (c.pair_rows > 0) {
         if ((rc = b2md_pair_rows(c.nbr, c.counts, c.pitch, stride_rows(r), c.n, c.pair_nbr,
                                  c.pair_counts, c.pair_pitch, c.pair_rows, s))) return rc;

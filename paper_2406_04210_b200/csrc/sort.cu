@@ -192,6 +192,29 @@ __global__ void k_gather4(const int32_t *__restrict__ src, int32_t *__restrict__
     if (k < n) dst[k] = __ldg(src + perm[k]);
 }
 
+// Whole particle rows in one launch: five 16-byte arrays and one 4-byte array through the
+// same permutation (read once), six independent loads in flight per thread.
+struct GatherRows {
+    const int4 *src16[5];
+    int4 *dst16[5];
+    const int32_t *src4;
+    int32_t *dst4;
+};
+
+__global__ void __launch_bounds__(256)
+k_gather_rows(const __grid_constant__ GatherRows g, const int32_t *__restrict__ perm, int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int32_t p = perm[k];
+    int4 v[5];
+#pragma unroll
+    for (int a = 0; a < 5; ++a) v[a] = __ldg(g.src16[a] + p);
+    const int32_t w = g.src4 ? __ldg(g.src4 + p) : 0;
+#pragma unroll
+    for (int a = 0; a < 5; ++a) g.dst16[a][k] = v[a];
+    if (g.src4) g.dst4[k] = w;
+}
+
 static inline int64_t sort_tiles(int64_t n) { return (n + kSortTile - 1) / kSortTile; }
 
 }  // namespace b2md
@@ -248,8 +271,7 @@ B2MD_EXPORT int b2md_iota_i32(int32_t *d_vals, int64_t n, void *stream) {
 B2MD_EXPORT int64_t b2md_sort_scratch_bytes(int64_t n) {
     const int64_t tiles = sort_tiles(n < 1 ? 1 : n);
     const int64_t hist = kRadix * tiles;
-    const int64_t scan_tiles = (hist + 4095) / 4096 + 2;
-    return (int64_t)sizeof(int32_t) * (2 * hist + 1 + scan_tiles) + 256;
+    return (int64_t)sizeof(int32_t) * (2 * hist + 1 + scan_scratch_ints(hist)) + 256;
 }
 
 B2MD_EXPORT int b2md_sort_pairs_u64(uint64_t *d_keys, int32_t *d_vals, uint64_t *d_keys_tmp,
@@ -297,6 +319,26 @@ B2MD_EXPORT int b2md_gather16(const void *d_src, void *d_dst, const int32_t *d_p
     k_gather16<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>((const int4 *)d_src,
                                                                   (int4 *)d_dst, d_perm, n);
     B2MD_CHECK_LAUNCH("b2md_gather16");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_gather_rows(const void *const *d_src16, void *const *d_dst16,
+                                 const void *d_src4, void *d_dst4, const int32_t *d_perm,
+                                 int64_t n, void *stream) {
+    if (n <= 0 || !d_src16 || !d_dst16 || !d_perm || (d_src4 && !d_dst4)) {
+        set_error("b2md_gather_rows: bad arguments");
+        return -1;
+    }
+    GatherRows g;
+    for (int a = 0; a < 5; ++a) {
+        if (!d_src16[a] || !d_dst16[a]) { set_error("b2md_gather_rows: null array"); return -1; }
+        g.src16[a] = (const int4 *)d_src16[a];
+        g.dst16[a] = (int4 *)d_dst16[a];
+    }
+    g.src4 = (const int32_t *)d_src4;
+    g.dst4 = (int32_t *)d_dst4;
+    k_gather_rows<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(g, d_perm, n);
+    B2MD_CHECK_LAUNCH("b2md_gather_rows");
     return 0;
 }
 
