@@ -41,6 +41,10 @@
 namespace b2md {
 
 constexpr int kForceThreads = 128;
+#ifndef B2MD_PAIR_THREADS
+#define B2MD_PAIR_THREADS 128
+#endif
+constexpr int kPairThreads = B2MD_PAIR_THREADS;    // CTA size of k_force_lj_pair (1024 threads per SM)
 constexpr int kMaxTypes = 8;
 
 struct PairParams {   // one species pair, fp32
@@ -301,13 +305,14 @@ __device__ __forceinline__ bool advance_gate_closed(b2md_status *status, const A
 }
 
 // Displacement maximum of the block -> status (as k_integrate does); all threads call it.
+template <int THREADS = kForceThreads>
 __device__ __forceinline__ void advance_publish_disp(float d2, float *s_max, b2md_status *status,
                                                      const AdvanceArgs &adv) {
     d2 = warp_max(d2);
     if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
     __syncthreads();
     if (threadIdx.x < 32) {
-        float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+        float m = threadIdx.x < THREADS / 32 ? s_max[threadIdx.x] : 0.0f;
         m = warp_max(m);
         if (threadIdx.x == 0 && m > 0.0f) {
             atomicMax(&status->max_disp2_bits, __float_as_uint(m));
@@ -588,7 +593,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
 // ADVANCE: 0 = forces only, 1 = one-launch step, 2 = one-launch step that also stores the
 // slab halo into the neighbour ranks' ghost rows (AdvanceArgs::halo_*)
 template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE>
-__global__ void __launch_bounds__(kForceThreads, 8)
+__global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
                 int64_t pair_pitch, const int32_t *__restrict__ nbr,
@@ -598,7 +603,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 const __grid_constant__ AdvanceArgs adv) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
-    __shared__ float s_max[kForceThreads / 32];
+    __shared__ float s_max[kPairThreads / 32];
     // step-graph batches: nothing to do once an in-graph list build overflowed
     if (gated && *(volatile int *)&status->frozen) return;
     if (ADVANCE && advance_gate_closed(status, adv)) return;
@@ -676,7 +681,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                                 status);
         }
     }
-    if (ADVANCE) advance_publish_disp(d2, s_max, status, adv);
+    if (ADVANCE) advance_publish_disp<kPairThreads>(d2, s_max, status, adv);
 }
 
 // ---- all pairs, shared-memory tiles of 128 positions ------------------------
@@ -912,7 +917,7 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     AdvanceArgs adv = {};
     if (advance) adv = *advance;
 #define B2MD_LAUNCH_PAIR(TABLE, THERMO, SIG1, ADVANCE)                                        \
-    k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE><<<blocks, kForceThreads, 0, s>>>(           \
+    k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE><<<blocks, kPairThreads, 0, s>>>(           \
         (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
         (flags & B2MD_FORCE_GATED) ? 1 : 0, adv)
@@ -920,7 +925,7 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     // CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch of the
     // index stream, L1 cache-policy hints, per-SM or per-warp work queues were all neutral
     // or slower.
-    const unsigned blocks = blocks_for((n + 1) / 2, kForceThreads);
+    const unsigned blocks = blocks_for((n + 1) / 2, kPairThreads);
     const bool sig1 = a.single.sig2 == 1.0f;
     if (advance && (adv.halo_dst[0] || adv.halo_dst[1])) {
         if (ntypes == 1) {
