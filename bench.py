@@ -189,26 +189,27 @@ def run_gpu_arm(args):
         if world == 1 and args.gpus > 1:
             raise SystemExit("launch with torch.distributed.run --nproc-per-node N for --gpus N")
     torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     if world > 1 or args.force_slab:
-        if world == 1:      # exercise the decomposed driver on one rank (validation only)
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("nccl", rank=0, world_size=1,
-                                    device_id=torch.device("cuda", local_rank))
-        from paper_2406_04210_b200.decomp import run_slab_benchmark
-        # default: weak scaling, 1 M particles per GPU; --total-particles T fixes the job size
-        # instead (BASELINE.json configs[4]: T = 16 M over 2 / 4 / 8 GPUs)
-        n_rank = args.particles_per_gpu or N_PER_GPU
-        if args.total_particles:
-            n_rank = args.total_particles // world
-        # NCCL writes its version banner to stdout: keep fd 1 clean for the one JSON line
+        # NCCL writes its version banner to stdout when the communicator is created (eagerly,
+        # with device_id): keep fd 1 clean for the one JSON line from before the init on
         sys.stdout.flush()
         real_stdout = os.dup(1)
         os.dup2(2, 1)
         try:
+            if world > 1:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            else:           # exercise the decomposed driver on one rank (validation only)
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                dist.init_process_group("nccl", rank=0, world_size=1,
+                                        device_id=torch.device("cuda", local_rank))
+            from paper_2406_04210_b200.decomp import run_slab_benchmark
+            # default: weak scaling, 1 M particles per GPU; --total-particles T fixes the job
+            # size instead (BASELINE.json configs[4]: T = 16 M over 2 / 4 / 8 GPUs)
+            n_rank = args.particles_per_gpu or N_PER_GPU
+            if args.total_particles:
+                n_rank = args.total_particles // world
             line = run_slab_benchmark(args, rank, world, local_rank, n_rank, WORKLOAD, METRIC,
                                       measured_peak, ClockSampler,
                                       scaling="strong" if args.total_particles else "weak")
