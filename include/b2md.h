@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 102
+#define B2MD_VERSION 103
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -474,6 +474,12 @@ typedef struct b2md_run_report {
     double max_disp2;            /* last displacement maximum seen (fp32 check) */
     uint64_t singular;           /* status->singular when reason == B2MD_RUN_SINGULAR */
     int64_t graph_steps;         /* steps of this call that ran as captured graphs */
+    /* CUDA-event phase timers (reference sim.py:114-129 force_seconds / nlist_seconds):
+     * GPU time of the whole call on the runner's stream, and the part of it spent in
+     * rebuild sequences (reorder + bin + list build + snapshot + pair rows).  The per-step
+     * displacement test is fused into the step kernels and counts as force time. */
+    double gpu_ms;
+    double rebuild_gpu_ms;
 } b2md_run_report;
 
 typedef struct b2md_runner b2md_runner;
@@ -492,6 +498,16 @@ int b2md_runner_prepare(b2md_runner *r, b2md_run_report *report);
  * is deferred into the next call's first fused kernel.  Synchronous on return. */
 int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finalize_at_end,
                     b2md_run_report *report);
+/* Andersen thermostat as the reference's second finalize slot (sim.py:86-87,100-102;
+ * integrate.py:82-107): after the second half-kick of every step, b2md_andersen(seed,
+ * step, probability, temperature) with step = first_step + steps completed so far in the
+ * call.  probability = min(rate * dt, 1); 0 switches the thermostat off.  A thermostatted
+ * runner launches integrate / force / finalize / thermostat separately (the thermostat
+ * sits between the two half-kicks that the fused kernels merge). */
+int b2md_runner_set_thermostat(b2md_runner *r, double probability, double temperature,
+                               uint64_t seed);
+/* Step counter (SignalEngine.step_count) of the first step of the next b2md_runner_run. */
+int b2md_runner_set_step(b2md_runner *r, int64_t first_step);
 
 #ifdef __cplusplus
 }

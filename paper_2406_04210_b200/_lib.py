@@ -80,6 +80,7 @@ class RunReport(Structure):
         ("wasted_force_launches", c_int32), ("kernel_launches", c_int64),
         ("list_valid", c_int32), ("n_boundary", c_int32), ("max_disp2", c_double),
         ("singular", c_uint64), ("graph_steps", c_int64),
+        ("gpu_ms", c_double), ("rebuild_gpu_ms", c_double),
     ]
 
 
@@ -173,6 +174,8 @@ _SIGNATURES = {
     "b2md_runner_set_pair_list": (c_int32, [c_void_p, _P, c_int32]),
     "b2md_runner_prepare": (c_int32, [c_void_p, POINTER(RunReport)]),
     "b2md_runner_run": (c_int32, [c_void_p, c_int64, c_int32, POINTER(RunReport)]),
+    "b2md_runner_set_thermostat": (c_int32, [c_void_p, c_double, c_double, c_uint64]),
+    "b2md_runner_set_step": (c_int32, [c_void_p, c_int64]),
 }
 
 #: entry points that report errors through their int return value

@@ -62,9 +62,25 @@ inline StepConst make_step(const b2md_box *box, double dt, double half_skin2) {
     c.dt_hi = (float)dt;
     c.dt_lo = (float)(dt - (double)c.dt_hi);
     c.half_dt = (float)(0.5 * dt);
-    // never fire later than the exact fp64 test: shave the fp32 rounding of the
-    // snapshot and of the squared norm off the threshold
-    c.half_skin2 = (float)(half_skin2 * (1.0 - 1e-5));
+    // Never fire later than the exact fp64 test (neighbor.py:251-254).  The in-loop test
+    // sees high words only: per component the snapshot drops its low word (<= ulp(L)/2),
+    // so does the current position, and the wrap correction of the snapshot subtracts
+    // k*L_hi instead of k*L (another ulp(L)/2) -- at most 2 ulp(L) on a component, 2.5 with
+    // the roundings of the difference.  The squared norm of a displacement d at the
+    // threshold is then off by at most 2*sqrt(3)*|d|*delta + 3*delta^2 (plus the fp32
+    // roundings of the sum, 4*2^-24 relative): that much comes off the threshold.
+    double lmax = 0.0;
+    for (int a = 0; a < 3; ++a) lmax = box->edge[a] > lmax ? box->edge[a] : lmax;
+    int e = 0;
+    frexp(lmax, &e);                                   // lmax = m * 2^e, m in [0.5, 1)
+    const double ulp = ldexp(1.0, e - 24);             // fp32 ulp just below lmax
+    const double delta = 2.5 * ulp;
+    const double half_skin = sqrt(half_skin2);
+    double shaved = half_skin2 - (2.0 * 1.7320508075688772 * half_skin * delta +
+                                  3.0 * delta * delta);
+    shaved *= 1.0 - 1e-6;
+    if (!(shaved > 0.0)) shaved = 0.0;                 // zero skin: rebuild on any motion
+    c.half_skin2 = half_skin2 >= 1e29 ? (float)half_skin2 : (float)shaved;
     return c;
 }
 

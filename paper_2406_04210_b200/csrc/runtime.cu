@@ -59,6 +59,14 @@ struct b2md_runner {
     bool ahead;               // positions already advanced to the step about to be processed
     int gate_in;              // status word holding the rebuild flag of those positions
     int count_seen;           // advance launches counted by the device so far (word 13)
+    // Andersen thermostat (second finalize slot of the reference, sim.py:86-87)
+    double thermo_p, thermo_t;
+    uint64_t thermo_seed;
+    int64_t first_step;       // SignalEngine.step_count of the first step of the next run
+    // phase timers: GPU time of a call and of its rebuild sequences (CUDA events)
+    cudaEvent_t ev_run[2];
+    std::vector<cudaEvent_t> ev_rebuild;   // pairs, grown on demand, resolved at the end of a call
+    int rebuild_events_used;
 };
 
 namespace {
@@ -124,9 +132,11 @@ constexpr int kWordRebuildFlag = 5;   // b2md_status::rebuild_flag
 constexpr int kWordAltFlag = 12;      // b2md_status::reserved[0]
 constexpr int kWordAdvanceCount = 13; // b2md_status::reserved[1]
 
+bool thermostatted(const b2md_runner *r) { return r->thermo_p > 0.0; }
+
 bool can_advance(const b2md_runner *r) {
     const b2md_runner_config &c = r->cfg;
-    return c.pos_hi_alt != nullptr && c.use_graph == 0;
+    return c.pos_hi_alt != nullptr && c.use_graph == 0 && !thermostatted(r);
 }
 
 // The canonical buffer of the live set holds the position high words again.
@@ -246,9 +256,24 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
 int rebuild(b2md_runner *r, b2md_run_report *rep) {
     const b2md_runner_config &c = r->cfg;
     const bool do_reorder = c.reorder_mode != 0 && (r->rebuilds_total % c.reorder_every) == 0;
-    // graph mode keeps the live pointers fixed (they are baked into the step graph)
-    int rc = enqueue_rebuild(r, do_reorder, c.use_graph != 0, &r->launches);
+    // phase timer: one event pair per rebuild, read when the call ends
+    if ((size_t)r->rebuild_events_used + 2 > r->ev_rebuild.size()) {
+        for (int k = 0; k < 2; ++k) {
+            cudaEvent_t e = nullptr;
+            int rc0 = check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+            if (rc0) return rc0;
+            r->ev_rebuild.push_back(e);
+        }
+    }
+    cudaEvent_t ev0 = r->ev_rebuild[r->rebuild_events_used];
+    cudaEvent_t ev1 = r->ev_rebuild[r->rebuild_events_used + 1];
+    int rc = check_cuda(cudaEventRecord(ev0, r->stream), "rebuild timer");
     if (rc) return rc;
+    // graph mode keeps the live pointers fixed (they are baked into the step graph)
+    rc = enqueue_rebuild(r, do_reorder, c.use_graph != 0, &r->launches);
+    if (rc) return rc;
+    if ((rc = check_cuda(cudaEventRecord(ev1, r->stream), "rebuild timer"))) return rc;
+    r->rebuild_events_used += 2;
     if (do_reorder) rep->reorders += 1;
     r->rebuilds_total += 1;
     rep->rebuilds += 1;
@@ -348,10 +373,41 @@ int build_graph(b2md_runner *r, int slot, int n_steps) {
     return 0;
 }
 
+// Every path that ends a call has drained the stream (read_status) before it gets here.
 void finish_report(b2md_runner *r, b2md_run_report *rep, int64_t launches_before) {
     rep->current = r->current;
     rep->kernel_launches = r->launches - launches_before;
     rep->list_valid = r->list_valid ? 1 : 0;
+    if (cudaEventRecord(r->ev_run[1], r->stream) == cudaSuccess &&
+        cudaEventSynchronize(r->ev_run[1]) == cudaSuccess) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r->ev_run[0], r->ev_run[1]) == cudaSuccess)
+            rep->gpu_ms = ms;
+        for (int k = 0; k + 1 < r->rebuild_events_used; k += 2)
+            if (cudaEventElapsedTime(&ms, r->ev_rebuild[k], r->ev_rebuild[k + 1]) == cudaSuccess)
+                rep->rebuild_gpu_ms += ms;
+    }
+    (void)cudaGetLastError();      // a timer that could not be read is not an error of the run
+    r->rebuild_events_used = 0;
+}
+
+// Start of a call: phase timers.
+int begin_call(b2md_runner *r) {
+    r->rebuild_events_used = 0;
+    return check_cuda(cudaEventRecord(r->ev_run[0], r->stream), "run timer");
+}
+
+// Second half-kick and the thermostat slot of step number `step` (sim.py:100-102).
+int finish_thermostat_step(b2md_runner *r, int64_t step) {
+    const b2md_runner_config &c = r->cfg;
+    Set a = live(r);
+    int rc = b2md_vv_finalize(a.vel, a.force, c.n, c.dt, r->stream);
+    if (rc) return rc;
+    rc = b2md_andersen(a.vel, a.pos_lo, c.n, r->thermo_seed, (uint64_t)step, r->thermo_p,
+                       r->thermo_t, nullptr, r->stream);
+    r->launches += 2;
+    r->pending_kick = false;
+    return rc;
 }
 
 // Make the runner's stream wait for everything the caller enqueued so far.
@@ -465,6 +521,8 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     } else {
         r->ahead = false;
         r->pending_kick = true;
+        if (thermostatted(r) &&
+            (rc = finish_thermostat_step(r, r->first_step + rep->steps_done))) return rc;
     }
     rep->steps_done += 1;
     return 0;
@@ -635,6 +693,12 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->gate_in = kWordRebuildFlag;
     r->count_seen = 0;
     if (r->cfg.queue_depth < 1) r->cfg.queue_depth = 1;
+    r->thermo_p = 0.0;
+    r->thermo_t = 1.0;
+    r->thermo_seed = 0;
+    r->first_step = 0;
+    r->ev_run[0] = r->ev_run[1] = nullptr;
+    r->rebuild_events_used = 0;
     r->h_status = nullptr;
     r->ev = r->ev_in = r->ev_mark = nullptr;
     r->copy_stream = nullptr;
@@ -647,6 +711,8 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
         check_cuda(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev_mark, cudaEventDisableTiming), "cudaEventCreate") ||
+        check_cuda(cudaEventCreate(&r->ev_run[0]), "cudaEventCreate") ||
+        check_cuda(cudaEventCreate(&r->ev_run[1]), "cudaEventCreate") ||
         check_cuda(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking),
                    "cudaStreamCreate") ||
         check_cuda(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking),
@@ -664,6 +730,8 @@ B2MD_EXPORT void b2md_runner_destroy(b2md_runner *r) {
     if (r->ev) cudaEventDestroy(r->ev);
     if (r->ev_in) cudaEventDestroy(r->ev_in);
     if (r->ev_mark) cudaEventDestroy(r->ev_mark);
+    for (cudaEvent_t e : r->ev_run) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : r->ev_rebuild) if (e) cudaEventDestroy(e);
     if (r->copy_stream) cudaStreamDestroy(r->copy_stream);
     if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
@@ -690,12 +758,40 @@ B2MD_EXPORT int b2md_runner_set_pair_list(b2md_runner *r, int32_t *pair_nbr, int
     return 0;
 }
 
+B2MD_EXPORT int b2md_runner_set_thermostat(b2md_runner *r, double probability,
+                                           double temperature, uint64_t seed) {
+    if (!r || !(probability >= 0.0) || !(temperature > 0.0)) {
+        set_error("b2md_runner_set_thermostat: bad arguments");
+        return -1;
+    }
+    if (probability > 0.0 && (r->pending_kick || r->ahead)) {
+        set_error("b2md_runner_set_thermostat: a half-kick is pending; finish the run first");
+        return -2;
+    }
+    r->thermo_p = probability > 1.0 ? 1.0 : probability;
+    r->thermo_t = temperature;
+    r->thermo_seed = seed;
+    if (probability > 0.0) {
+        // fused half-kicks and captured steps have no slot for the thermostat
+        r->cfg.use_graph = 0;
+        destroy_graph(r);
+    }
+    return 0;
+}
+
+B2MD_EXPORT int b2md_runner_set_step(b2md_runner *r, int64_t first_step) {
+    if (!r || first_step < 0) { set_error("b2md_runner_set_step: bad arguments"); return -1; }
+    r->first_step = first_step;
+    return 0;
+}
+
 B2MD_EXPORT int b2md_runner_prepare(b2md_runner *r, b2md_run_report *rep) {
     if (!r || !rep) { set_error("b2md_runner_prepare: null argument"); return -1; }
     *rep = b2md_run_report();
     const int64_t before = r->launches;
     int rc = order_after_caller(r);
     if (rc) return rc;
+    if ((rc = begin_call(r))) return rc;
     if ((rc = rebuild(r, rep))) return rc;
     if (!r->list_valid) {
         rep->reason = B2MD_RUN_OVERFLOW;
@@ -723,6 +819,7 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
         return -2;
     }
     if ((rc = order_after_caller(r))) return rc;
+    if ((rc = begin_call(r))) return rc;
     if (r->mid_step) {
         // previous call stopped on overflow after integrating: finish that step
         if ((rc = rebuild(r, rep))) return rc;
@@ -734,6 +831,8 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
         if ((rc = launch_force(r, rep->steps_done + 1 >= n_steps))) return rc;
         r->mid_step = false;
         r->pending_kick = true;
+        if (thermostatted(r) && (rc = finish_thermostat_step(r, r->first_step + rep->steps_done)))
+            return rc;
         rep->steps_done += 1;
     }
     while (rep->steps_done < n_steps) {

@@ -8,9 +8,11 @@ moved more than skin/2, stride growth on overflow (at most
 
 Two drivers produce bit-identical trajectories:
 
-* ``native=True`` (default for truncated forces without thermostat): the C++
-  step loop of libb2md (csrc/runtime.cu) -- two kernel launches per step, the
-  rebuild test read back asynchronously while the force kernel runs.
+* ``native=True`` (default for truncated forces): the C++ step loop of libb2md
+  (csrc/runtime.cu) -- one or two kernel launches per step, the rebuild test read
+  back asynchronously while the force kernel runs.  With an Andersen thermostat the
+  loop launches integrate / force / finalize / thermostat per step (the thermostat is
+  the reference's second finalize slot, sim.py:86-87,100-102).
 * ``native=False``: the reference's signal/slot loop calling the operator
   functions one by one (same kernels, one Python call each) -- what the parity
   tests exercise operator by operator.
@@ -75,8 +77,6 @@ class Simulation:
         if skin < 0.0:
             raise ConfigError("skin must be non-negative")
         thermostatted = thermostat is not None and getattr(thermostat, "rate", 0.0) > 0.0
-        if thermostatted and native:
-            raise ConfigError("the native step loop is NVE; a thermostat runs the operator loop")
         if reorder not in _REORDER_MODES:
             raise ConfigError(f"unknown reorder mode {reorder!r}")
         if stride_policy not in ("fit", "double", "tight"):
@@ -104,15 +104,16 @@ class Simulation:
             env = os.environ.get("B2MD_ADVANCE")
             advance = (env != "0") if env in ("0", "1") else \
                 (self.pair_rows or state.n < ADVANCE_ROWS_MAX_PARTICLES)
-        self.advance = bool(advance)
+        self.advance = bool(advance) and not thermostatted
         # one-launch steps queued per status read-back (small systems: a step is shorter
         # than a host round trip)
         self.queue_depth = int(os.environ.get("B2MD_QUEUE_DEPTH", "1")) if queue_depth is None \
             else int(queue_depth)
         self.graph_steps = 0
-        # the thermostat acts between finalize and the next integrate: operator loop
-        self.native = (force_mode == TRUNCATED and not thermostatted) if native is None \
-            else bool(native)
+        # (a thermostatted native loop launches integrate / force / finalize / thermostat
+        # separately: the thermostat is the reference's second finalize slot, sim.py:86-87)
+        self.native = (force_mode == TRUNCATED) if native is None else bool(native)
+        self._thermostatted = thermostatted
         if self.native and force_mode != TRUNCATED:
             raise ConfigError("the native step loop drives truncated forces only")
         if not self.native and self.reorder == "cell":
@@ -307,6 +308,10 @@ class Simulation:
             raise _lib.B2mdError("b2md_runner_create failed: "
                                  + lib.b2md_last_error_string().decode())
         self._runner = ctypes.c_void_p(handle)
+        if self._thermostatted:
+            _lib.call("b2md_runner_set_thermostat", self._runner,
+                      float(self.thermostat.redraw_probability(self.integrator.dt)),
+                      float(self.thermostat.temperature), int(self.thermostat.seed) % (1 << 64))
         self._native_call("b2md_runner_prepare")
 
     def _native_call(self, name, *args):
@@ -319,10 +324,17 @@ class Simulation:
             t0 = time.perf_counter()
             if name == "b2md_runner_run":
                 n_steps, finalize = args
+                # the thermostat stream is indexed by SignalEngine.step_count (sim.py:100-102)
+                _lib.call("b2md_runner_set_step", self._runner, self.engine.step_count + done)
                 _lib.call(name, self._runner, n_steps - done, finalize, ctypes.byref(rep))
             else:
                 _lib.call(name, self._runner, ctypes.byref(rep))
-            self.force_seconds += time.perf_counter() - t0
+            # phase timers from CUDA events on the runner's stream (sim.py:114-129): rebuild
+            # sequences -> nlist_seconds, everything else the call enqueued -> force_seconds;
+            # host time the GPU did not cover (launch latency of short steps) goes to neither
+            wall = time.perf_counter() - t0
+            self.nlist_seconds += 1e-3 * rep.rebuild_gpu_ms
+            self.force_seconds += max(min(1e-3 * rep.gpu_ms, wall) - 1e-3 * rep.rebuild_gpu_ms, 0.0)
             done += rep.steps_done
             self._absorb(rep, dev)
             if rep.reason == _lib.RUN_SINGULAR:

@@ -320,8 +320,34 @@ def thermostat_case():
          vel_after=np.array(st.velocities.acquire_read(COMPUTE)))
 
 
+# ------------------------------------------------------- harness CSV files
+def harness_csv_case():
+    """Records / samples files WRITTEN BY THE REFERENCE's own writers (bench.py:222-285)
+    from a sweep it ran itself (bench.py:372-383, smoke-sized): the B200 harness must read
+    them, summarise them and write them back byte for byte.  Also the reference's
+    speed-up / efficiency rows for both baselines (bench.py:393-442)."""
+    from mdbench import bench
+    cfg = bench.BenchConfig(n_particles=108, density=0.8, temperature=1.5, dt=0.002, steps=40,
+                            r_cut=2.5, skin=0.5, thermostat_rate=5.0, seed=7,
+                            sample_interval=10, equilibration_steps=10)
+    records = bench.run_sweep(cfg, [1, 2, 3])
+    bench.write_records_csv(os.path.join(OUT, "reference_records.csv"), records)
+    _, samples = bench.run_benchmark(cfg)
+    bench.write_samples_csv(os.path.join(OUT, "reference_samples.csv"), samples)
+    rows = {}
+    for base in ("sequential", "single"):
+        sr = bench.compute_speedup_efficiency(records, baseline=base)
+        rows[base] = np.array([[r.worker_count, r.wall_time_s, r.speedup, r.efficiency]
+                               for r in sr])
+    save("harness", speedup_sequential=rows["sequential"], speedup_single=rows["single"])
+    print("reference_records.csv / reference_samples.csv written")
+
+
 if __name__ == "__main__":
     print("reference mdbench", ref.__version__)
+    if len(sys.argv) > 1 and sys.argv[1] == "harness":
+        harness_csv_case()
+        sys.exit(0)
     neighbor_cases()
     rebuild_cases()
     force_cases()
@@ -329,3 +355,4 @@ if __name__ == "__main__":
     observable_cases()
     trajectory_case()
     thermostat_case()
+    harness_csv_case()

@@ -71,10 +71,42 @@ def test_thermostatted_simulation_holds_the_target_temperature():
     thermo = b2.ThermostatParams(temperature=1.5, rate=20.0, seed=7)
     sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.002, force_mode=b2.TRUNCATED,
                         skin=0.3, thermostat=thermo, sample_interval=10)
-    assert not sim.native
+    assert sim.native                  # the thermostat runs inside the native step loop
     sim.run(1500)
     temps = np.array([s.temperature for s in sim.samples[50:]])
     assert abs(temps.mean() - 1.5) < 0.03
-    with pytest.raises(b2.ConfigError):
-        b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.002, force_mode=b2.TRUNCATED,
-                      thermostat=thermo, native=True)
+    sim.close()
+
+
+@pytest.mark.parametrize("n,pair_rows", [(4000, False), (4000, True)])
+def test_native_thermostat_loop_equals_the_operator_loop_bitwise(n, pair_rows):
+    """sim.py:86-87,100-102: the thermostat is the second finalize slot, called with
+    SignalEngine.step_count.  The native runner (integrate / force / finalize / andersen
+    launched from C++) and the signal/slot loop calling the same operators one by one must
+    produce the same bits: same redraw decisions (Philox words indexed by step and logical
+    particle id), same rebuild steps, same samples -- across calls that split the run and
+    across the stride growth of the first build."""
+    out = []
+    for native in (False, True):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 1.5, 42)
+        thermo = b2.ThermostatParams(temperature=1.5, rate=20.0, seed=7)
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.002,
+                            force_mode=b2.TRUNCATED, skin=0.3, thermostat=thermo,
+                            sample_interval=25, native=native, pair_rows=pair_rows,
+                            reorder=None)      # (a reorder changes the summation order, and
+        # the in-loop fp32 displacement test may fire one step before the exact fp64 one)
+        assert sim.native == native
+        sim.run(60)
+        sim.run(41)                    # step numbers continue across calls
+        out.append((np.array(st.velocities.acquire_read(b2.HOST)),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    [(s.step, s.total_energy, s.temperature) for s in sim.samples],
+                    sim.rebuild_count))
+        if native:
+            assert sim.nlist_seconds > 0.0 and sim.force_seconds > 0.0
+        sim.close()
+    assert abs(out[0][3] - out[1][3]) <= 1 and out[0][3] >= 2
+    assert out[0][2] == out[1][2] and len(out[0][2]) == 4
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])

@@ -10,12 +10,12 @@ import pytest
 
 import paper_2406_04210_b200 as b2
 from paper_2406_04210_b200 import _lib
-from conftest import ROOT, load_golden
+from conftest import GOLDEN, ROOT, load_golden
 
 
 def test_library_exports_every_declared_symbol():
     lib = _lib.load()
-    assert lib.b2md_version() == 102
+    assert lib.b2md_version() == 103
     header = open(os.path.join(ROOT, "include", "b2md.h")).read()
     declared = set(re.findall(r"\b(b2md_[a-z0-9_]+)\(", header))
     declared -= {"b2md_box", "b2md_grid", "b2md_status"}
@@ -195,3 +195,56 @@ def test_bench_config_files_and_records_round_trip(tmp_path):
     lines = (tmp_path / "samples.csv").read_text().splitlines()
     assert lines[0] == "step,time,potential_energy,kinetic_energy,total_energy,temperature,px,py,pz,rebuild_count"
     assert lines[1].startswith("10,0.02") and lines[1].endswith(",2")
+
+
+def test_reference_written_csv_files_round_trip_byte_for_byte(tmp_path):
+    """tests/golden/reference_records.csv / reference_samples.csv were written by the
+    REFERENCE's writers from a sweep it ran itself (make_golden.py harness_csv_case;
+    bench.py:222-285, 372-383): the harness reads them and writes the same bytes back."""
+    src = os.path.join(GOLDEN, "reference_records.csv")
+    records = b2.read_records_csv(src)
+    assert [r.config.backend for r in records] == ["sequential", "parallel", "parallel", "parallel"]
+    assert [r.config.worker_count for r in records] == [1, 1, 2, 3]
+    assert records[0].engine_version == "0.1.0" and records[0].config.n_particles == 108
+    out = tmp_path / "records.csv"
+    b2.write_records_csv(out, records)
+    assert out.read_bytes() == open(src, "rb").read()
+    src = os.path.join(GOLDEN, "reference_samples.csv")
+    samples = b2.read_samples_csv(src)
+    assert [s.step for s in samples] == [20, 30, 40, 50]
+    out = tmp_path / "samples.csv"
+    b2.write_samples_csv(out, samples)
+    assert out.read_bytes() == open(src, "rb").read()
+    # same file format as pkg/frontend/test/data/sweep6.csv (header checked verbatim)
+    with pytest.raises(b2.ConfigError):
+        b2.read_records_csv(os.path.join(GOLDEN, "reference_samples.csv"))
+
+
+def test_speedup_efficiency_rows_match_the_reference(tmp_path):
+    """compute_speedup_efficiency on the reference's own records reproduces its rows
+    (bench.py:393-442) for both baselines; B200 records join the same summary."""
+    import dataclasses
+    records = b2.read_records_csv(os.path.join(GOLDEN, "reference_records.csv"))
+    want = np.load(os.path.join(GOLDEN, "harness.npz"))
+    for base in ("sequential", "single"):
+        rows = b2.compute_speedup_efficiency(records, baseline=base)
+        got = np.array([[r.worker_count, r.wall_time_s, r.speedup, r.efficiency] for r in rows])
+        assert np.array_equal(got, want[f"speedup_{base}"]), base
+        assert all(r.backend == "parallel" for r in rows)
+    # a B200 record of the same physics is summarised against the sequential CPU record
+    gpu = dataclasses.replace(records[0], wall_time_s=records[0].wall_time_s / 500.0,
+                              config=dataclasses.replace(records[0].config, backend="b200"))
+    rows = b2.compute_speedup_efficiency(records + [gpu])
+    assert rows[-1].backend == "b200" and rows[-1].speedup == pytest.approx(500.0)
+    assert rows[-1].efficiency == pytest.approx(1.0)
+    with pytest.raises(b2.ConfigError):
+        b2.compute_speedup_efficiency([])
+    with pytest.raises(b2.ConfigError):
+        b2.compute_speedup_efficiency(records, baseline="nope")
+    with pytest.raises(b2.ConfigError):                       # no sequential record
+        b2.compute_speedup_efficiency(records[1:])
+    other = dataclasses.replace(records[1], config=dataclasses.replace(records[1].config, dt=0.004))
+    with pytest.raises(b2.ConfigError, match="dt"):
+        b2.compute_speedup_efficiency([records[0], other])
+    with pytest.raises(b2.ConfigError):
+        b2.run_sweep(b2.preset_config("smoke-256"), [0])
