@@ -418,6 +418,8 @@ int order_after_caller(b2md_runner *r) {
     return check_cuda(cudaStreamWaitEvent(r->stream, r->ev_in, 0), "order stream wait");
 }
 
+void toggle_advance_state(b2md_runner *r);
+
 // One ungraphed step.  *stop = 1 when the call must return (overflow / singular).
 // With pair rows and a second position buffer the intermediate (unobservable) steps are
 // one gated launch each: force(s) + finalize(s) + integrate(s+1) + displacement check.
@@ -468,20 +470,27 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     if (r->h_status->singular != ~0ull) {
         // a force evaluation of an earlier step met a coincident pair
         // (forces.py:113-116); stop after draining the stream
-        if (fuse) {
-            // the queued launch advanced the particles: leave the canonical buffer current
-            Set now = live(r);
-            void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
-            r->pos_cur = in == now.pos_hi ? c.pos_hi_alt : now.pos_hi;
-            r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
-            r->ahead = true;
-            if ((rc = canonicalize(r))) return rc;
-        }
         if ((rc = read_status(r))) return rc;
+        bool stepped = !fuse;
+        if (fuse) {
+            // the queued launch advanced the particles only if it was not gated out (a
+            // rebuild may have been due as well): the device counted it if it ran
+            const int ran = reinterpret_cast<const int32_t *>(r->h_status)[kWordAdvanceCount] -
+                            r->count_seen;
+            if (ran > 0) {
+                r->count_seen += ran;
+                toggle_advance_state(r);
+                r->ahead = true;
+                stepped = true;
+            }
+            // leave the canonical buffer current
+            if ((rc = canonicalize(r))) return rc;
+            if ((rc = check_cuda(cudaStreamSynchronize(r->stream), "position copy"))) return rc;
+        }
         rep->singular = r->h_status->singular;
         rep->reason = B2MD_RUN_SINGULAR;
         r->pending_kick = !fuse;
-        rep->steps_done += 1;
+        if (stepped) rep->steps_done += 1;
         finish_report(r, rep, before);
         *stop = 1;
         return 0;
@@ -820,6 +829,13 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
     }
     if ((rc = order_after_caller(r))) return rc;
     if ((rc = begin_call(r))) return rc;
+    // The advance counter lives in the status block the public operators share and reset
+    // (b2md_status_reset): start every call from a known value instead of trusting the
+    // host mirror across calls.
+    if ((rc = check_cuda(cudaMemsetAsync(reinterpret_cast<int32_t *>(c.status) + kWordAdvanceCount,
+                                         0, sizeof(int32_t), r->stream), "counter reset")))
+        return rc;
+    r->count_seen = 0;
     if (r->mid_step) {
         // previous call stopped on overflow after integrating: finish that step
         if ((rc = rebuild(r, rep))) return rc;

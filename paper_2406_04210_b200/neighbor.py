@@ -133,6 +133,11 @@ class NeighborList:
         self.r_cut = float(r_cut)
         self.rebuild_count = int(rebuild_count)
         self._pair = None          # (d_pair_nbr, d_pair_counts, pair_pitch), built on demand
+        self._consumed = False     # buffers recycled by a later build (internal rebuilds only)
+
+    def _live(self):
+        if self._consumed:
+            raise RuntimeError("this NeighborList's buffers were recycled by a later rebuild")
 
     def pair_rows(self):
         """Merged rows of particles (2t, 2t+1) for the two-particles-per-thread force
@@ -140,6 +145,7 @@ class NeighborList:
         with ``d_pair_nbr`` of shape (tiles, pair_pitch, 4) int32, entry
         ``j << 2 | listed_for_2t | listed_for_2t+1 << 1``.  Derived from this list
         on first use and cached (the list is immutable once built)."""
+        self._live()
         if self._pair is None:
             torch = _torch()
             dev = self._dev
@@ -166,17 +172,20 @@ class NeighborList:
     @property
     def counts(self) -> np.ndarray:
         """(n,) int32 valid entries per row, logical particle order."""
+        self._live()
         return self.d_counts[:self._dev.n].cpu().numpy()
 
     @property
     def indices(self) -> np.ndarray:
         """(n, stride) int32 row-major copy in the reference's layout (physical
         row indices; identical to logical ids unless rows were reordered)."""
+        self._live()
         n = self._dev.n
         return np.ascontiguousarray(self.d_nbr[:self.stride, :n].t().cpu().numpy())
 
     @property
     def positions_at_build(self) -> np.ndarray:
+        self._live()
         return self.d_at_build.cpu().numpy()
 
     def pair_set(self):
@@ -194,13 +203,19 @@ class NeighborList:
 
 def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, stride: int,
                         r_cut: float | None = None, prev: NeighborList | None = None,
-                        backend: BackendSelector | None = None) -> NeighborList:
+                        backend: BackendSelector | None = None,
+                        _recycle: bool = False) -> NeighborList:
     """Build a full neighbour list from a cell grid (neighbor.py:185-240).
 
     Rows that would exceed ``stride`` raise the overflow flag instead of being
     truncated silently; the caller grows the stride and rebuilds.  Grids with
     fewer than three cells on an axis use the all-pairs scan (``grid.fallback``).
     Reading ``overflow`` synchronises with the device once per build.
+
+    ``prev`` only supplies the lineage counter (neighbor.py:239): every list owns its
+    buffers, as in the reference.  ``_recycle=True`` (internal: ``Simulation._rebuild``,
+    which drops the old list) builds into ``prev``'s device buffers instead and marks
+    ``prev`` consumed -- its accessors then raise.
     """
     if int(stride) < 1:
         raise ConfigError("stride must be >= 1")
@@ -216,7 +231,8 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
     n = dev.n
     pitch = _round_up(n, 32)
     rows = _round_up(stride, 16)
-    reuse = prev is not None and prev.d_nbr.shape == (rows, pitch) and prev._dev is dev
+    reuse = (_recycle and prev is not None and not prev._consumed and
+             prev.d_nbr.shape == (rows, pitch) and prev._dev is dev)
     if reuse:
         d_nbr, d_counts, d_boundary = prev.d_nbr, prev.d_counts, prev.d_boundary
         d_at_build, d_ref_pos = prev.d_at_build, prev.d_ref_pos
@@ -243,9 +259,11 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
                        overflow=st.overflow != 0, max_count=st.max_count, r_list=r_list,
                        r_cut=r_cut,
                        rebuild_count=(prev.rebuild_count if prev is not None else 0) + 1)
-    if reuse and prev._pair is not None:
-        out._pair_buf = prev._pair[:2]     # same shapes: merge into the old buffers
-        prev._pair = None
+    if reuse:
+        if prev._pair is not None:
+            out._pair_buf = prev._pair[:2]     # same shapes: merge into the old buffers
+            prev._pair = None
+        prev._consumed = True                  # its buffers now hold the new list
     return out
 
 

@@ -201,7 +201,7 @@ class Simulation:
             grid = bin_particles(self.state, self.box, r_list)
             nlist = build_neighbor_list(self.state, grid, r_list, self._stride,
                                         r_cut=self.lj.max_r_cut, prev=self._nlist,
-                                        backend=self.backend)
+                                        backend=self.backend, _recycle=True)
             self._nlist = nlist
             self._rebuild_total += 1
             if not nlist.overflow:
