@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/b2md.h"
 
@@ -28,6 +29,12 @@ inline int check_cuda(cudaError_t err, const char *what) {
         int rc_ = b2md::check_cuda(cudaPeekAtLastError(), name);       \
         if (rc_) return rc_;                                           \
     } while (0)
+
+// Integer A/B knob from the environment, read per call (no cached state in the library).
+inline int env_choice(const char *name, int fallback) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : fallback;
+}
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -157,25 +157,15 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
 // while trip t does its four position gathers and the arithmetic, the indices of
 // trips t+1 and t+2 are already in flight.  CHECK = false is used for the leading
 // trips in which every lane still has valid entries.
-// Where the 16-byte neighbour-position gathers go.  The LSU data pipe of L1
-// (about one 128-byte wavefront per cycle per SM) is the limiter of this kernel:
-// a gather of 32 scattered float4 costs ~11 wavefronts.  Texture fetches of the
-// same linear buffer run through the TEX pipe of the same cache, so splitting the
-// gathers between both pipes raises the gather rate.
-//   GATHER 0: all through LDG (ld.global.nc)   1: all through TEX
-//   GATHER 2: entries alternate between the two pipes
-template <int GATHER>
-__device__ __forceinline__ float4 gather_pos(const float4 *__restrict__ pos,
-                                             cudaTextureObject_t tex, int j, int u) {
-    if (GATHER == 1 || (GATHER == 2 && (u & 1))) return tex1Dfetch<float4>(tex, j);
-    return __ldg(pos + j);
-}
-
-template <int GATHER>
+// The 16-byte neighbour-position gathers go through LDG (ld.global.nc).  The LSU data pipe
+// of L1 (about one 128-byte wavefront per cycle per SM) is the limiter of this kernel: a
+// gather of 32 scattered float4 costs ~11 wavefronts.  (Routing half of them through the TEX
+// pipe of the same cache was measured in round 1 and did not pay; the texture path and its
+// process-wide object cache are gone.)
 __device__ __forceinline__ void gather4(float4 (&pj)[4], const int (&j)[4],
-                                        const float4 *__restrict__ pos, cudaTextureObject_t tex) {
+                                        const float4 *__restrict__ pos) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pj[u] = gather_pos<GATHER>(pos, tex, j[u], u);
+    for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
 }
 
 // AXES: bit a set = pairs of this warp may need an image shift along axis a.
@@ -207,11 +197,11 @@ __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, 
 // PIPE = true additionally keeps the NEXT trip's four position gathers in flight
 // while the current trip is being computed (deeper memory-level parallelism at
 // the price of 16 more registers).
-template <int SUB, int GATHER, int PIPEK, int AXES, bool TABLE, bool THERMO>
+template <int SUB, int PIPEK, int AXES, bool TABLE, bool THERMO>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *__restrict__ pos,
-                                         cudaTextureObject_t tex, const ForceArgs &a,
+                                         const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
                                          int ti_row) {
     constexpr bool PIPE = (PIPEK == 1);
@@ -224,14 +214,14 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
         jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
     }
     float4 pa[4], pb[4];
-    if (PIPE) gather4<GATHER>(pa, ja, pos, tex);
+    if (PIPE) gather4(pa, ja, pos);
     for (int base = 0; base < kmax; base += kTrip) {
         int jc[4];
         const bool more = base + 2 * kTrip < kmax;          // warp-uniform
 #pragma unroll
         for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (8 + u) * step) : 0;
-        if (PIPE) gather4<GATHER>(pb, jb, pos, tex);         // row 0 is always a valid index
-        else gather4<GATHER>(pa, ja, pos, tex);
+        if (PIPE) gather4(pb, jb, pos);                      // row 0 is always a valid index
+        else gather4(pa, ja, pos);
         if (base + kTrip <= kmin)
             compute4<SUB, AXES, TABLE, THERMO, false>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
                                                          s_tab_b, ti_row);
@@ -323,9 +313,9 @@ __device__ __forceinline__ void advance_publish_disp(float d2, float *s_max, b2m
 
 // PIPE doubles as the occupancy knob of the experiments: 0 = 8 CTAs/SM (<= 64
 // registers), 1 = gathers one trip ahead with 6 CTAs/SM, 2 = 12 CTAs/SM (<= 40).
-template <int SUB, int GATHER, int PIPE, bool TABLE, bool THERMO, bool ADVANCE = false>
+template <int SUB, int PIPE, bool TABLE, bool THERMO, bool ADVANCE = false>
 __global__ void __launch_bounds__(kForceThreads, PIPE == 1 ? 6 : (PIPE == 2 ? 12 : 8))
-k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
+k_force_lj(const float4 *__restrict__ pos, int64_t n,
            const __grid_constant__ ForceArgs a,
            const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
            const uint8_t *__restrict__ boundary, float4 *__restrict__ force,
@@ -360,8 +350,8 @@ k_force_lj(const float4 *__restrict__ pos, cudaTextureObject_t tex, int64_t n,
 
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
 #define B2MD_ROW_LOOP(AXES)                                                                  \
-    row_loop<SUB, GATHER, PIPE, AXES, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch,  \
-                                                     pos, tex, a, s_tab_a, s_tab_b, ti_row)
+    row_loop<SUB, PIPE, AXES, TABLE, THERMO>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, a,  \
+                                             s_tab_a, s_tab_b, ti_row)
     switch (axes) {                 // warp-uniform
         case 0: B2MD_ROW_LOOP(0); break;      // interior: plain differences
         case 1: B2MD_ROW_LOOP(1); break;      // one face family only
@@ -747,38 +737,6 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
                   ((unsigned long long)(unsigned)i << 32) | (unsigned)first_bad);
 }
 
-// Texture objects over position buffers (linear float4), created on first use
-// and reused while the same buffer comes back (the runner alternates between two).
-struct TexEntry { const void *ptr; size_t rows; cudaTextureObject_t tex; };
-static TexEntry g_tex[8];
-static int g_tex_next = 0;
-
-static int position_texture(const void *ptr, size_t rows, cudaTextureObject_t *out) {
-    for (const TexEntry &e : g_tex)
-        if (e.ptr == ptr && e.rows == rows && e.tex) { *out = e.tex; return 0; }
-    TexEntry &slot = g_tex[g_tex_next];
-    g_tex_next = (g_tex_next + 1) % 8;
-    if (slot.tex) cudaDestroyTextureObject(slot.tex);
-    cudaResourceDesc res = {};
-    res.resType = cudaResourceTypeLinear;
-    res.res.linear.devPtr = const_cast<void *>(ptr);
-    res.res.linear.desc = cudaCreateChannelDesc<float4>();
-    res.res.linear.sizeInBytes = rows * sizeof(float4);
-    cudaTextureDesc td = {};
-    td.readMode = cudaReadModeElementType;
-    td.filterMode = cudaFilterModePoint;
-    td.addressMode[0] = cudaAddressModeClamp;
-    td.normalizedCoords = 0;
-    slot.tex = 0;
-    int rc = check_cuda(cudaCreateTextureObject(&slot.tex, &res, &td, nullptr),
-                        "cudaCreateTextureObject");
-    if (rc) { slot.ptr = nullptr; slot.tex = 0; return rc; }
-    slot.ptr = ptr;
-    slot.rows = rows;
-    *out = slot.tex;
-    return 0;
-}
-
 static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int ntypes) {
     if (!box || !table) { set_error("force: null box/table"); return -1; }
     if (ntypes < 1 || ntypes > kMaxTypes) {
@@ -824,52 +782,37 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
-    // tuning knobs (defaults chosen from profiles/)
-    // Measured on B200 at N = 1 M (profiles/README.md): 12 CTAs/SM (<= 40 registers)
-    // beats 8 CTAs/SM by 5 %; one lane per particle beats sub-warps for large systems,
-    // while small systems (few CTAs, latency-bound serial row loops) want 4 lanes per
-    // particle; texture gathers and deeper gather pipelining do not pay.
-    static int sub_env = -1, gather = 0, pipe = 2;
-    if (sub_env < 0) {
-        const char *env = getenv("B2MD_FORCE_SUBWARP");       // lanes per particle: 1, 2, 4
-        const int v = env ? atoi(env) : 0;
-        sub_env = (v == 1 || v == 2 || v == 4) ? v : 0;       // 0 = choose by system size
-        env = getenv("B2MD_FORCE_GATHER");                    // 0 LDG, 2 alternate LDG / TEX
-        gather = (env && atoi(env) == 2) ? 2 : 0;
-        env = getenv("B2MD_FORCE_PIPE");                      // 0: 8 CTAs/SM, 2: 12 CTAs/SM
-        pipe = (env && atoi(env) == 0) ? 0 : 2;
-    }
-    const int sub = sub_env ? sub_env : (n < 200000 ? 4 : 1);
-    cudaTextureObject_t tex = 0;
-    if (gather != 0) {
-        // rows of pos_hi are addressed up to `pitch` (owned + ghost rows)
-        rc = position_texture(d_pos_hi, (size_t)pitch, &tex);
-        if (rc) return rc;
-    }
-#define B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, TABLE, THERMO)                                  \
-    k_force_lj<SUB, GATHER, PIPE, TABLE, THERMO>                                             \
+    // Defaults chosen from profiles/ (DESIGN.md section 6), measured on B200 at N = 1 M: 12 CTAs/SM
+    // (<= 40 registers) beats 8 CTAs/SM by 5 %; one lane per particle beats sub-warps for
+    // large systems, while small systems (few CTAs, latency-bound serial row loops) want 4
+    // lanes per particle.  The A/B knobs are read per call: the library keeps no state.
+    const int sub_env = env_choice("B2MD_FORCE_SUBWARP", 0);     // lanes per particle: 1, 2, 4
+    const int pipe = env_choice("B2MD_FORCE_PIPE", 2) == 0 ? 0 : 2;   // 0: 8 CTAs/SM, 2: 12
+    const int sub = (sub_env == 1 || sub_env == 2 || sub_env == 4) ? sub_env
+                                                                   : (n < 200000 ? 4 : 1);
+#define B2MD_LAUNCH_FORCE(SUB, PIPE, TABLE, THERMO)                                          \
+    k_force_lj<SUB, PIPE, TABLE, THERMO>                                                     \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
-            (const float4 *)d_pos_hi, tex, n, a, d_nbr, d_counts, pitch, d_boundary,         \
+            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary,              \
             (float4 *)d_force_f4, d_virial, d_status, (flags & B2MD_FORCE_GATED) ? 1 : 0,    \
             AdvanceArgs())
-#define B2MD_DISPATCH_TT(SUB, GATHER, PIPE)                                                  \
+#define B2MD_DISPATCH_TT(SUB, PIPE)                                                          \
     do {                                                                                     \
         if (ntypes == 1) {                                                                   \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, false, true);                   \
-            else B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, false, false);                         \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, PIPE, false, true);                           \
+            else B2MD_LAUNCH_FORCE(SUB, PIPE, false, false);                                 \
         } else {                                                                             \
-            if (thermo) B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, true, true);                    \
-            else B2MD_LAUNCH_FORCE(SUB, GATHER, PIPE, true, false);                          \
+            if (thermo) B2MD_LAUNCH_FORCE(SUB, PIPE, true, true);                            \
+            else B2MD_LAUNCH_FORCE(SUB, PIPE, true, false);                                  \
         }                                                                                    \
     } while (0)
     if (sub == 1) {
-        if (gather == 2) B2MD_DISPATCH_TT(1, 2, 2);
-        else if (pipe == 0) B2MD_DISPATCH_TT(1, 0, 0);
-        else B2MD_DISPATCH_TT(1, 0, 2);
+        if (pipe == 0) B2MD_DISPATCH_TT(1, 0);
+        else B2MD_DISPATCH_TT(1, 2);
     } else if (sub == 2) {
-        B2MD_DISPATCH_TT(2, 0, 0);
+        B2MD_DISPATCH_TT(2, 0);
     } else {
-        B2MD_DISPATCH_TT(4, 0, 0);
+        B2MD_DISPATCH_TT(4, 0);
     }
 #undef B2MD_DISPATCH_TT
 #undef B2MD_LAUNCH_FORCE
@@ -1017,9 +960,9 @@ B2MD_EXPORT int b2md_force_lj_advance(
     const int gated = (flags & B2MD_FORCE_GATED) ? 1 : 0;
     // lanes per particle as in b2md_force_lj: small systems are latency-bound
 #define B2MD_LAUNCH_ROW_ADVANCE(SUB, PIPE, TABLE)                                             \
-    k_force_lj<SUB, 0, PIPE, TABLE, false, true>                                              \
+    k_force_lj<SUB, PIPE, TABLE, false, true>                                                 \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                        \
-            (const float4 *)d_pos_hi, 0, n, a, d_nbr, d_counts, pitch, d_boundary, nullptr,   \
+            (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary, nullptr,      \
             nullptr, d_status, gated, adv)
     if (n < 200000) {
         if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(4, 0, false);

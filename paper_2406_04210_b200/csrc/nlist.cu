@@ -948,11 +948,9 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
     const bool prefilter = band < 0.05 * g.rl2;
     const unsigned blocks = blocks_for(n_rows, kBuildThreads);
     const size_t warp_smem = kCandCap * sizeof(float4) + (size_t)(stride + 2) * 32 * sizeof(int32_t);
-    static int list_kernel = -1;           // 0: lane = candidate (default), 1: lane = particle
-    if (list_kernel < 0) {
-        const char *env = getenv("B2MD_LIST_KERNEL");
-        list_kernel = (env && atoi(env) == 1) ? 1 : 0;
-    }
+    // 0: lane = candidate (default), 1: lane = particle; read per call, function attributes
+    // set per launch (they are per device, and cheap): the library keeps no state
+    const int list_kernel = env_choice("B2MD_LIST_KERNEL", 0) == 1 ? 1 : 0;
     if (grid->fallback) {
         k_list_brute<<<blocks, kBuildThreads, 0, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, stride, pitch, d_nbr,
@@ -962,12 +960,8 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
         constexpr int kBallotWarps = 8;
         const int64_t nc = grid->n_cells;
         const size_t smem = ballot_warp_bytes() * kBallotWarps;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_list_cells_ballot<kBallotWarps><<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
             (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
             d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status,
@@ -977,23 +971,15 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
         const int64_t nc = grid->n_cells;
         if (warp_smem * kCellWarps <= 96 * 1024) {
             const size_t smem = warp_smem * kCellWarps;
-            static bool attr4 = false;
-            if (!attr4) {
-                cudaFuncSetAttribute(k_list_cells_warp<kCellWarps>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-                attr4 = true;
-            }
+            cudaFuncSetAttribute(k_list_cells_warp<kCellWarps>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             k_list_cells_warp<kCellWarps><<<blocks_for(nc, kCellWarps), kCellWarps * 32, smem, s>>>(
                 (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
                 d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);
         } else {
             const size_t smem = warp_smem * 2;
-            static bool attr2 = false;
-            if (!attr2) {
-                cudaFuncSetAttribute(k_list_cells_warp<2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                attr2 = true;
-            }
+            cudaFuncSetAttribute(k_list_cells_warp<2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             k_list_cells_warp<2><<<blocks_for(nc, 2), 64, smem, s>>>(
                 (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
                 d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status);

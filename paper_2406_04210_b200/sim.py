@@ -63,7 +63,7 @@ def _torch():
 class Simulation:
     def __init__(self, state: ParticleState, box: SimBox, lj, dt: float,
                  backend: BackendSelector | None = None, force_mode: str = ALL_TO_ALL,
-                 skin: float = DEFAULT_SKIN, stride: int = DEFAULT_STRIDE, thermostat=None,
+                 skin: float = DEFAULT_SKIN, stride: int | None = None, thermostat=None,
                  sample_interval: int = 100, deterministic: bool = True,
                  sample_initial: bool = False, reorder: str | None = "hilbert",
                  reorder_every: int = 1, native: bool | None = None,
@@ -119,6 +119,20 @@ class Simulation:
         if not self.native and self.reorder == "cell":
             raise ConfigError("reorder='cell' is implemented by the native step loop only")
 
+        # Row capacity of the first build.  The reference starts at DEFAULT_STRIDE = 64 and
+        # doubles on overflow (sim.py:30,141-149); a dense fluid overflows that at once, and
+        # on the device a second 1 ms build plus a re-allocation of the list is most of a
+        # short call.  None (default) sizes the first build from the mean density instead:
+        # 1.25 x the ideal-gas count inside r_list + 16 (an fcc start lists 78 where the
+        # fluid lists 67; Kob-Andersen 134 / 110), never below the reference's 64.  Overflow
+        # keeps its semantics either way: flagged, never truncated, grow and rebuild.
+        if stride is None:
+            stride = DEFAULT_STRIDE
+            if force_mode == TRUNCATED:
+                r_list = lj.max_r_cut + float(skin)
+                expected = state.n / box.volume * (4.0 / 3.0) * np.pi * r_list ** 3
+                stride = max(DEFAULT_STRIDE, _round_up(int(1.25 * expected) + 16, 8))
+                stride = min(stride, max(_round_up(state.n, 8), DEFAULT_STRIDE))
         self._stride = int(stride)
         self._nlist: NeighborList | None = None
         self.overflow_events = 0
