@@ -456,6 +456,14 @@ typedef struct b2md_runner_config {
                                     systems, whose step is shorter than a host round trip,
                                     want several */
     int32_t reserved2;
+    /* Optional caller-owned resources (NULL = the runner creates and destroys its own).
+     * Page-locking memory and creating streams are the expensive parts of creating a
+     * runner (1-7 ms measured on B200); a caller that builds many short-lived simulations
+     * hands in recycled ones (the Python host passes blocks of torch's caching host
+     * allocator and pooled torch streams). */
+    void *h_status;              /* >= 64 bytes of page-locked host memory */
+    void *run_stream;            /* cudaStream_t for the step loop (must not be `stream`) */
+    void *copy_stream;           /* cudaStream_t for the status read-backs */
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };

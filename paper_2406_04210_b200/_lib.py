@@ -70,6 +70,7 @@ class RunnerConfig(Structure):
         ("use_graph", c_int32), ("pair_rows", c_int32),
         ("pair_nbr", c_void_p), ("pair_counts", c_void_p), ("pair_pitch", c_int64),
         ("pos_hi_alt", c_void_p), ("queue_depth", c_int32), ("reserved2", c_int32),
+        ("h_status", c_void_p), ("run_stream", c_void_p), ("copy_stream", c_void_p),
     ]
 
 

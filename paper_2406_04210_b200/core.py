@@ -19,6 +19,8 @@ from __future__ import annotations
 
 import ctypes
 
+import weakref
+
 import numpy as np
 
 from . import _lib
@@ -228,7 +230,10 @@ class TrackedBuffer:
             self._host_data, self._lazy = None, array
         else:
             self._host_data, self._lazy = _host_array(array, copy), None
-        self._owner = owner
+        # weak: the state owns its buffers, not the other way round (a strong back reference
+        # makes every ParticleState a reference cycle, and its HBM is then only returned by
+        # the cycle collector -- 1 GB per abandoned Simulation at N = 1 M)
+        self._owner = weakref.ref(owner) if owner is not None else None
         self.kind = kind
         self.version = 0
         # the device copy is materialised on first COMPUTE acquisition
@@ -249,9 +254,10 @@ class TrackedBuffer:
 
     # -- conversions -------------------------------------------------------
     def _device(self) -> DeviceState:
-        if self._owner is None or self.kind is None:
+        owner = self._owner() if self._owner is not None else None
+        if owner is None or self.kind is None:
             raise _lib.B2mdError("this TrackedBuffer is not attached to a ParticleState")
-        return self._owner.device_state()
+        return owner.device_state()
 
     def _upload(self):
         torch = _torch()

@@ -45,6 +45,7 @@ struct b2md_runner {
     cudaEvent_t ev_in;        // ordering against the caller's stream
     cudaStream_t stream;      // the runner's own (capturable) stream
     cudaStream_t copy_stream; // flag read-backs, off the kernels' critical path
+    bool own_h_status, own_stream, own_copy_stream;   // false: lent by the caller (cfg)
     cudaEvent_t ev_mark;      // "everything enqueued so far" for the copy stream
     int64_t launches;
     double last_disp2;        // max squared displacement seen one step ago (fp32 check)
@@ -702,6 +703,7 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->gate_in = kWordRebuildFlag;
     r->count_seen = 0;
     if (r->cfg.queue_depth < 1) r->cfg.queue_depth = 1;
+    r->own_h_status = r->own_stream = r->own_copy_stream = true;
     r->thermo_p = 0.0;
     r->thermo_t = 1.0;
     r->thermo_seed = 0;
@@ -716,16 +718,25 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     if (r->cfg.use_graph && r->cfg.reorder_mode != 0 && r->cfg.reorder_every != 1)
         r->cfg.use_graph = 0;
     if (b2md_grid_shape(&cfg->box, r->r_list, &r->grid)) { delete r; return nullptr; }
-    if (check_cuda(cudaMallocHost((void **)&r->h_status, sizeof(b2md_status)), "cudaMallocHost") ||
+    r->own_h_status = cfg->h_status == nullptr;
+    r->own_stream = cfg->run_stream == nullptr;
+    r->own_copy_stream = cfg->copy_stream == nullptr;
+    if (!r->own_h_status) r->h_status = static_cast<b2md_status *>(cfg->h_status);
+    if (!r->own_stream) r->stream = as_stream(cfg->run_stream);
+    if (!r->own_copy_stream) r->copy_stream = as_stream(cfg->copy_stream);
+    if ((r->own_h_status &&
+         check_cuda(cudaMallocHost((void **)&r->h_status, sizeof(b2md_status)), "cudaMallocHost")) ||
         check_cuda(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreateWithFlags(&r->ev_mark, cudaEventDisableTiming), "cudaEventCreate") ||
         check_cuda(cudaEventCreate(&r->ev_run[0]), "cudaEventCreate") ||
         check_cuda(cudaEventCreate(&r->ev_run[1]), "cudaEventCreate") ||
-        check_cuda(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking),
-                   "cudaStreamCreate") ||
-        check_cuda(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking),
-                   "cudaStreamCreate")) {
+        (r->own_copy_stream &&
+         check_cuda(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking),
+                    "cudaStreamCreate")) ||
+        (r->own_stream &&
+         check_cuda(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking),
+                    "cudaStreamCreate"))) {
         b2md_runner_destroy(r);
         return nullptr;
     }
@@ -735,14 +746,17 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
 B2MD_EXPORT void b2md_runner_destroy(b2md_runner *r) {
     if (!r) return;
     destroy_graph(r);
-    if (r->h_status) cudaFreeHost(r->h_status);
+    if (r->h_status && r->own_h_status) cudaFreeHost(r->h_status);
     if (r->ev) cudaEventDestroy(r->ev);
     if (r->ev_in) cudaEventDestroy(r->ev_in);
     if (r->ev_mark) cudaEventDestroy(r->ev_mark);
     for (cudaEvent_t e : r->ev_run) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : r->ev_rebuild) if (e) cudaEventDestroy(e);
-    if (r->copy_stream) cudaStreamDestroy(r->copy_stream);
-    if (r->stream) cudaStreamDestroy(r->stream);
+    // lent streams may still carry this runner's work: drain before the events go
+    if (r->stream && !r->own_stream) cudaStreamSynchronize(r->stream);
+    if (r->copy_stream && !r->own_copy_stream) cudaStreamSynchronize(r->copy_stream);
+    if (r->copy_stream && r->own_copy_stream) cudaStreamDestroy(r->copy_stream);
+    if (r->stream && r->own_stream) cudaStreamDestroy(r->stream);
     delete r;
 }
 

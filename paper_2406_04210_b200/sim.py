@@ -315,6 +315,14 @@ class Simulation:
             k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
             cfg.pair_nbr = k["pair_nbr"].data_ptr()
             cfg.pair_counts = k["pair_counts"].data_ptr()
+        # page-locked status mirror and the runner's two streams come from torch's caching
+        # host allocator / stream pool: creating them per runner costs 1-7 ms of driver calls
+        k["h_status"] = torch.empty(16, dtype=torch.int32).pin_memory()
+        k["run_stream"] = torch.cuda.Stream(device=dev.device)
+        k["copy_stream"] = torch.cuda.Stream(device=dev.device)
+        cfg.h_status = k["h_status"].data_ptr()
+        cfg.run_stream = k["run_stream"].cuda_stream
+        cfg.copy_stream = k["copy_stream"].cuda_stream
         k["cfg"] = cfg
         dev.reset_status()
         handle = lib.b2md_runner_create(ctypes.byref(cfg))
@@ -450,15 +458,33 @@ class Simulation:
         self._rebuild_base = self._rebuild_total
 
     def run(self, n_steps: int):
+        if getattr(self, "_closed", False):
+            raise RuntimeError("this Simulation was closed")
         if self.native:
             self._run_native(n_steps)
         else:
             self.engine.run_steps(n_steps)
 
     def close(self):
+        """Destroy the native runner and hand the simulation's device buffers (lists, pair
+        rows, sort scratch, the spare state set: 1 GB at N = 1 M) back to the allocator now,
+        not when the cycle collector gets round to it (slots are bound methods: a Simulation
+        and its SignalEngine reference each other).  The ParticleState stays usable."""
         if self._runner is not None:
             _lib.load().b2md_runner_destroy(self._runner)
             self._runner = None
+            k = self._keep
+            if k:
+                # the state keeps whichever set is live; everything else goes
+                dev = self.state.device_state()
+                live = k["sets"][k.get("current", 0)]
+                for name, t in live.items():
+                    setattr(dev, name, t)
+            self._keep = {}
+        self._nlist = None
+        self._closed = True
+        for slots in self.engine._slots.values():
+            slots.clear()
 
     def __del__(self):  # pragma: no cover - best effort
         try:
