@@ -392,6 +392,8 @@ def run_gpu_arm(args):
     tab = np.ascontiguousarray(lj.table())
     tab_ptr = tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     rows = k["nbr"].shape[0]
+    # kernels timed alone follow the runner's block schedule, as inside a step
+    sched = _lib.FORCE_SCHEDULED if (sim.pair_rows and k["cfg"].pair_schedule) else 0
 
     def launch_force_rows():
         _lib.call("b2md_force_lj", dev.pos_hi.data_ptr(), n, box.c_box(), k["nbr"].data_ptr(),
@@ -403,14 +405,16 @@ def run_gpu_arm(args):
         _lib.call("b2md_force_lj_pairs", dev.pos_hi.data_ptr(), n, box.c_box(),
                   k["pair_nbr"].data_ptr(), k["pair_counts"].data_ptr(), cfg.pair_pitch,
                   k["nbr"].data_ptr(), k["counts"].data_ptr(), k["pitch"],
-                  k["boundary"].data_ptr(), tab_ptr, 1, _lib.FORCE_SKIP_THERMO,
+                  k["boundary"].data_ptr(), tab_ptr, 1, _lib.FORCE_SKIP_THERMO | sched,
                   dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
 
     # the kernel the step loop launches (pair rows for systems this large)
     force_kernel = "k_force_lj_pair" if sim.pair_rows else "k_force_lj"
     force_ms = time_kernel(launch_force_pairs if sim.pair_rows else launch_force_rows, 50, torch,
                            stream)
-    pair_entries = float(k["pair_counts"].float().sum().item()) / n if sim.pair_rows else None
+    pair_entries = (float(k["pair_counts"][:k["cfg"].pair_pitch].float().sum().item()) / n
+                    if sim.pair_rows else None)
+
     extra_kernels = {}
     if sim.pair_rows:
         # for comparison: the thread-per-particle kernel on the same list, and the merge
@@ -462,8 +466,8 @@ def run_gpu_arm(args):
                       scratch_state["image"].data_ptr(), n, box.c_box(), 1e-9,
                       ref_scratch.data_ptr(), 1e30, k["pair_nbr"].data_ptr(),
                       k["pair_counts"].data_ptr(), cfg.pair_pitch, k["nbr"].data_ptr(),
-                      k["counts"].data_ptr(), k["pitch"], k["boundary"].data_ptr(), tab_ptr, 1, 0,
-                      12, 14, scratch_status.data_ptr(), dev.stream)   # gate words of the scratch block
+                      k["counts"].data_ptr(), k["pitch"], k["boundary"].data_ptr(), tab_ptr, 1,
+                      sched, 12, 14, scratch_status.data_ptr(), dev.stream)   # gate words of the scratch block
         adv_ms = time_kernel(launch_advance, 30, torch, stream)
         # SURVEY 8(d) rows it replaces: integrate 128 + force 32+4c (no-thermo) + finalize 48,
         # minus the 80 B per particle of force / velocity traffic that fusion makes unnecessary

@@ -183,6 +183,8 @@ int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void
  * A coincident listed pair is reported in status->singular. */
 #define B2MD_FORCE_SKIP_THERMO 1
 #define B2MD_FORCE_GATED 2        /* return at once when d_status->frozen is set */
+#define B2MD_FORCE_SCHEDULED 4    /* pair kernels: d_pair_counts[pair_pitch ...] holds the block
+                                     schedule written by b2md_pair_schedule */
 int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                   const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
                   int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
@@ -199,6 +201,18 @@ int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
  * pair_rows (entries per pair row): multiple of 4, >= 2 * stride, so a merge can
  * never overflow.  Derived data: the per-particle list stays the source of truth
  * (and what build_neighbor_list returns, neighbor.py:185-240). */
+/* Block schedule of the pair kernels (optional).  Blocks whose particles sit near a
+ * periodic face (d_boundary, written by b2md_build_nlist) take the image-shift paths and run
+ * up to 1.7x longer; in particle order they are dispatched last (a space-filling curve ends
+ * on a face) and become the tail of every launch.  b2md_pair_schedule writes a permutation
+ * of the blocks -- flagged blocks first -- behind the pair counts, at
+ * d_pair_counts[pair_pitch ...] (the buffer must have pair_pitch + b2md_pair_schedule_len(n)
+ * entries: the schedule and its scratch); launches that pass B2MD_FORCE_SCHEDULED follow it.
+ * Results do not depend on the schedule. */
+int64_t b2md_pair_schedule_len(int64_t n);
+int b2md_pair_schedule(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_counts,
+                       int64_t pair_pitch, void *stream);
+
 int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, int32_t stride,
                    int64_t n_rows, int32_t *d_pair_nbr, int32_t *d_pair_counts,
                    int64_t pair_pitch, int32_t pair_rows, void *stream);
@@ -455,7 +469,8 @@ typedef struct b2md_runner_config {
     int32_t queue_depth;         /* one-launch steps queued per status read-back (>= 1); small
                                     systems, whose step is shorter than a host round trip,
                                     want several */
-    int32_t reserved2;
+    int32_t pair_schedule;       /* != 0: pair_counts has b2md_pair_schedule_len(n) more entries;
+                                    the runner keeps a block schedule there (see above) */
     /* Optional caller-owned resources (NULL = the runner creates and destroys its own).
      * Page-locking memory and creating streams are the expensive parts of creating a
      * runner (1-7 ms measured on B200); a caller that builds many short-lived simulations

@@ -69,7 +69,7 @@ class RunnerConfig(Structure):
         ("status", c_void_p), ("stream", c_void_p),
         ("use_graph", c_int32), ("pair_rows", c_int32),
         ("pair_nbr", c_void_p), ("pair_counts", c_void_p), ("pair_pitch", c_int64),
-        ("pos_hi_alt", c_void_p), ("queue_depth", c_int32), ("reserved2", c_int32),
+        ("pos_hi_alt", c_void_p), ("queue_depth", c_int32), ("pair_schedule", c_int32),
         ("h_status", c_void_p), ("run_stream", c_void_p), ("copy_stream", c_void_p),
     ]
 
@@ -87,6 +87,7 @@ class RunReport(Structure):
 
 RUN_DONE, RUN_OVERFLOW, RUN_SINGULAR = 0, 1, 2
 FORCE_SKIP_THERMO = 1
+FORCE_SCHEDULED = 4
 
 _P = c_void_p
 _SIGNATURES = {
@@ -131,6 +132,8 @@ _SIGNATURES = {
     "b2md_force_lj": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, c_int32, _P,
                                 POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_pair_rows": (c_int32, [_P, _P, c_int64, c_int32, c_int64, _P, _P, c_int64, c_int32, _P]),
+    "b2md_pair_schedule_len": (c_int64, [c_int64]),
+    "b2md_pair_schedule": (c_int32, [_P, c_int64, _P, c_int64, _P]),
     "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
                                       _P, POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_force_lj_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,

@@ -56,6 +56,7 @@ struct ForceArgs {
     BoxF box;
     PairParams single;
     int ntypes;
+    const int32_t *schedule;    // pair kernel: block executed by blockIdx.x (null = identity)
     float4 tab_a[kMaxTypes * kMaxTypes];   // sig2, rc2, c_f, c_u
     float2 tab_b[kMaxTypes * kMaxTypes];   // half_shift, c_w
 };
@@ -87,6 +88,14 @@ struct RowAcc {
     float fx, fy, fz, u, w;
     int cnt;
 };
+
+// A load the compiler can neither hoist nor merge with an earlier load of the same address.
+__device__ __forceinline__ float4 reload_f4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
 
 // Single-type pair: prefactors deferred.  `in` false => contributes exact zeros.
 // THERMO = false drops the energy / virial / count accumulators (intermediate
@@ -344,7 +353,7 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n,
     const int kmax = __reduce_max_sync(0xffffffffu, cnt);
     const int kmin = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff);
     // which axes can need an image shift for some pair of this warp (0 = interior warp)
-    const int axes = boundary ? __reduce_or_sync(0xffffffffu, active ? (int)boundary[i] : 0) : 7;
+    const int axes = boundary ? (__reduce_or_sync(0xffffffffu, active ? (int)boundary[i] : 0) & 7) : 7;
     const int32_t *col = nbr + (int64_t)sub * pitch + i;
     const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
 
@@ -462,6 +471,44 @@ __device__ __forceinline__ f32x2 delta2(f32x2 xi, float xj, float L_hi, float L_
     return fma2(ns, pk1(-L_lo), sub2(sa, sb));
 }
 
+// ---- image shifts in the frame centred on the periodic face ---------------------
+// delta2<true> derives the image number of every pair from its raw difference (rint via the
+// magic constant, two max pairs, three fmas per half and axis: +22 issue slots per axis and
+// entry; 14 % of the step kernel's time at N = 1 M, where 16 % of the particles sit in
+// flagged warps).  When every particle of the warp lies in the outer quarters of the box
+// along a flagged axis (x < L/4 or x > 3L/4; warp-uniform test, always true for a Hilbert-
+// ordered fluid in a box wider than 4 (r_list + skin)), the image number of a listed pair is
+// simply s_i - s_j with s = [x > L/2]: map every coordinate above L/2 down by L_hi (exact,
+// Sterbenz) and correct by (s_j - s_i) L_lo.  One compare, two selects and one add on the
+// scalar x_j, two packed operations more than the plain difference -- and the same bits as
+// delta2<true>: same shifted operands a, b, same image number, same single rounding of
+// (a - b) - n L_lo; for s_i = s_j the correction is an exact zero and the difference of the
+// two exactly shifted coordinates is the difference of the unshifted ones.
+__device__ __forceinline__ void face_frame(f32x2 &x2, f32x2 &corr2, float L_hi, float L_lo,
+                                           float half) {
+    float x0, x1;
+    upk(x2, x0, x1);
+    const bool s0 = x0 > half, s1 = x1 > half;
+    x2 = pk(s0 ? x0 - L_hi : x0, s1 ? x1 - L_hi : x1);
+    corr2 = pk(s0 ? L_lo : 0.0f, s1 ? L_lo : 0.0f);
+}
+
+// MODE 0: plain difference, 1: delta2<true>, 2: face frame (xi already mapped, corr_i = s_i L_lo)
+template <int MODE>
+__device__ __forceinline__ f32x2 delta2m(f32x2 xi, f32x2 corr_i, float xj, float L_hi, float L_lo,
+                                         float invL, float half) {
+    if (MODE == 0) return sub2(xi, pk1(xj));
+    if (MODE == 1) return delta2<true>(xi, xj, L_hi, L_lo, invL);
+    const bool sj = xj > half;
+    const float xjm = sj ? xj - L_hi : xj;
+    const float corr_j = sj ? L_lo : 0.0f;
+    return add2(sub2(xi, pk1(xjm)), sub2(pk1(corr_j), corr_i));
+}
+
+// AXES: bits 0-2 = axes on delta2<true>, bits 3-5 = axes in the face frame
+template <int AXES, int AXIS>
+struct AxisMode { static constexpr int value = (AXES >> AXIS) & 1 ? 1 : ((AXES >> (3 + AXIS)) & 1 ? 2 : 0); };
+
 struct PackAcc {
     f32x2 fx, fy, fz, u, w;   // halves: particle 2t, particle 2t+1
     int cnt_a, cnt_b;
@@ -471,12 +518,13 @@ struct PackAcc {
 // one packed multiply less on the FMA pipe that bounds this kernel).
 template <int AXES, bool THERMO, bool SIG1>
 __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 ay, f32x2 az,
+                                                  f32x2 cx, f32x2 cy, f32x2 cz,
                                                   int e, const float4 pj, const ForceArgs &a) {
     const BoxF &b = a.box;
     const PairParams &p = a.single;
-    const f32x2 dx = delta2<(AXES & 1) != 0>(ax, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-    const f32x2 dy = delta2<(AXES & 2) != 0>(ay, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-    const f32x2 dz = delta2<(AXES & 4) != 0>(az, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const f32x2 dx = delta2m<AxisMode<AXES, 0>::value>(ax, cx, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0], b.half[0]);
+    const f32x2 dy = delta2m<AxisMode<AXES, 1>::value>(ay, cy, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1], b.half[1]);
+    const f32x2 dz = delta2m<AxisMode<AXES, 2>::value>(az, cz, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2], b.half[2]);
     const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
     float r2a, r2b;
     upk(r2, r2a, r2b);
@@ -503,7 +551,8 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
 // to the row kernel's.
 template <int AXES, bool THERMO>
 __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, f32x2 ay,
-                                                        f32x2 az, int e, const float4 pj,
+                                                        f32x2 az, f32x2 cx, f32x2 cy, f32x2 cz,
+                                                        int e, const float4 pj,
                                                         const ForceArgs &a,
                                                         const float4 *s_tab_a,
                                                         const float2 *s_tab_b, int ta_row,
@@ -511,9 +560,9 @@ __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, 
     const BoxF &b = a.box;
     const int tj = __float_as_int(pj.w);
     const float4 qa = s_tab_a[ta_row + tj], qb = s_tab_a[tb_row + tj];
-    const f32x2 dx = delta2<(AXES & 1) != 0>(ax, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-    const f32x2 dy = delta2<(AXES & 2) != 0>(ay, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-    const f32x2 dz = delta2<(AXES & 4) != 0>(az, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const f32x2 dx = delta2m<AxisMode<AXES, 0>::value>(ax, cx, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0], b.half[0]);
+    const f32x2 dy = delta2m<AxisMode<AXES, 1>::value>(ay, cy, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1], b.half[1]);
+    const f32x2 dz = delta2m<AxisMode<AXES, 2>::value>(az, cz, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2], b.half[2]);
     const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
     float r2a, r2b;
     upk(r2, r2a, r2b);
@@ -535,6 +584,10 @@ __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, 
 }
 
 
+#ifndef B2MD_PAIR_TILE_ROTATE
+#define B2MD_PAIR_TILE_ROTATE 0
+#endif
+
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
 template <int AXES, bool TABLE, bool THERMO, bool SIG1>
@@ -552,24 +605,40 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     if (tiles > 1) e1 = __ldcs(col + pair_pitch);
     col += 2 * pair_pitch;
     PackAcc acc = {0ull, 0ull, 0ull, 0ull, 0ull, 0, 0};     // +0.0f in both halves
-    const f32x2 ax = pk(pa.x, pb.x), ay = pk(pa.y, pb.y), az = pk(pa.z, pb.z);
+    f32x2 ax = pk(pa.x, pb.x), ay = pk(pa.y, pb.y), az = pk(pa.z, pb.z);
+    f32x2 cx = 0ull, cy = 0ull, cz = 0ull;
+    if (AXES & 8) face_frame(ax, cx, a.box.L_hi[0], a.box.L_lo[0], a.box.half[0]);
+    if (AXES & 16) face_frame(ay, cy, a.box.L_hi[1], a.box.L_lo[1], a.box.half[1]);
+    if (AXES & 32) face_frame(az, cz, a.box.L_hi[2], a.box.L_lo[2], a.box.half[2]);
 #pragma unroll 1
     for (int q = 0; q < tiles; ++q) {
+#if B2MD_PAIR_TILE_ROTATE == 0
         const int ev[4] = {e0.x, e0.y, e0.z, e0.w};
         e0 = e1;
         if (q + 2 < tiles) e1 = __ldcs(col);            // warp-uniform; a stale e1 is never used
         col += pair_pitch;
+#else
+        // the tile in use stays in e0 for the whole trip (no copy: four registers less in a
+        // loop that runs at the register cap); the rotation happens at the bottom
+        const int ev[4] = {e0.x, e0.y, e0.z, e0.w};
+#endif
         float4 pj[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + ((unsigned)ev[u] >> 2));
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (TABLE)
-                pair_entry_packed_table<AXES, THERMO>(acc, ax, ay, az, ev[u], pj[u], a, s_tab_a,
-                                                      s_tab_b, ta_row, tb_row);
+                pair_entry_packed_table<AXES, THERMO>(acc, ax, ay, az, cx, cy, cz, ev[u], pj[u],
+                                                      a, s_tab_a, s_tab_b, ta_row, tb_row);
             else
-                pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, ev[u], pj[u], a);
+                pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, cx, cy, cz, ev[u], pj[u],
+                                                      a);
         }
+#if B2MD_PAIR_TILE_ROTATE != 0
+        e0 = e1;
+        if (q + 2 < tiles) e1 = __ldcs(col);            // warp-uniform; a stale e1 is never used
+        col += pair_pitch;
+#endif
     }
     upk(acc.fx, A.fx, B.fx);
     upk(acc.fy, A.fy, B.fy);
@@ -580,10 +649,34 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
     B.cnt = acc.cnt_b;
 }
 
+// The same loop out of line (its registers are allocated on their own): a knob of the A/B
+// harness, B2MD_PAIR_OUTLINE -- see the dispatch.  ptxas' register assignment inside the
+// 64-register loop decides +-10 % of this kernel (identical instruction mix, different
+// operand banks), and any change elsewhere in the kernel reshuffles it.
+template <int AXES, bool TABLE, bool THERMO, bool SIG1>
+__device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const float4 pa,
+                                                    const float4 pb, int tiles,
+                                                    const int4 *__restrict__ col,
+                                                    int64_t pair_pitch,
+                                                    const float4 *__restrict__ pos,
+                                                    const ForceArgs &a, const float4 *s_tab_a,
+                                                    const float2 *s_tab_b, int ta_row,
+                                                    int tb_row) {
+    pair_row_loop<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch, pos, a, s_tab_a,
+                                             s_tab_b, ta_row, tb_row);
+}
+
+#ifndef B2MD_PAIR_MIN_BLOCKS
+#define B2MD_PAIR_MIN_BLOCKS (1024 / kPairThreads)
+#endif
+#ifndef B2MD_PAIR_OUTLINE
+#define B2MD_PAIR_OUTLINE 0      // 0: nothing, 1: fallback 7, 2: + multi-axis face variants, 3: all but 0
+#endif                           // (measured, profiles/README.md: 0 is the fastest build)
+
 // ADVANCE: 0 = forces only, 1 = one-launch step, 2 = one-launch step that also stores the
 // slab halo into the neighbour ranks' ghost rows (AdvanceArgs::halo_*)
 template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE>
-__global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads)
+__global__ void __launch_bounds__(kPairThreads, B2MD_PAIR_MIN_BLOCKS)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
                 int64_t pair_pitch, const int32_t *__restrict__ nbr,
@@ -595,7 +688,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float s_max[kPairThreads / 32];
     // step-graph batches: nothing to do once an in-graph list build overflowed
-    if (gated && *(volatile int *)&status->frozen) return;
+    if ((gated & 1) && *(volatile int *)&status->frozen) return;
     if (ADVANCE && advance_gate_closed(status, adv)) return;
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
@@ -605,7 +698,11 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
         __syncthreads();
     }
     const int64_t n_pairs = (n + 1) >> 1;
-    const int64_t t_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // Block schedule (b2md_pair_schedule): blocks whose warps need image shifts run up to
+    // 1.7x longer; dispatched last (the space-filling curve ends on a face of the box) they
+    // were the tail of the launch -- 10 us of 118 at N = 1 M.  The schedule runs them first.
+    const unsigned bid = a.schedule ? (unsigned)__ldg(a.schedule + blockIdx.x) : blockIdx.x;
+    const int64_t t_raw = bid * (int64_t)blockDim.x + threadIdx.x;
     const bool active = t_raw < n_pairs;
     const int64_t t = active ? t_raw : n_pairs - 1;
     const int64_t ia = 2 * t;
@@ -613,10 +710,20 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     const int64_t ib = has_b ? ia + 1 : ia;
     const float4 pa = pos[ia], pb = pos[ib];
     const int cnt = active ? pair_counts[t] : 0;
-    const int tiles = __reduce_max_sync(0xffffffffu, (cnt + 3) >> 2);
-    const int axes = boundary ? __reduce_or_sync(0xffffffffu,
-                                                 active ? (int)(boundary[ia] | boundary[ib]) : 0)
-                              : 7;
+    int tiles = __reduce_max_sync(0xffffffffu, (cnt + 3) >> 2);
+    if (gated >> 16) tiles = tiles * ((gated >> 16) - 1) / 100;   // timing experiment: shorter rows
+    // boundary flags of the warp's particles (nlist.cu, boundary_flag): bits 0-2 OR-ed = axes
+    // that may need an image shift, bits 3-5 AND-ed = axes on which every particle is clear
+    // of the mid-plane (face frame legal)
+    // (gated bit 1: timing experiment only -- every warp takes the no-image-shift path)
+    int near = 7, clear = 0;                     // no flags: per-pair image numbers on all axes
+    if (boundary) {
+        const int fa = active ? (int)boundary[ia] : 0x38, fb = active ? (int)boundary[ib] : 0x38;
+        near = (fa | fb) & 7;
+        clear = (fa & fb) >> 3;
+    }
+    const int axes = (gated & 2) ? 0 : __reduce_or_sync(0xffffffffu, near);
+    clear = __reduce_and_sync(0xffffffffu, clear);
     const int4 *col = pair_nbr + t;
     const int ta_row = TABLE ? __float_as_int(pa.w) * a.ntypes : 0;
     const int tb_row = TABLE ? __float_as_int(pb.w) * a.ntypes : 0;
@@ -625,14 +732,34 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
 #define B2MD_PAIR_LOOP(AXES)                                                                  \
     pair_row_loop<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch, pos, a,    \
                                              s_tab_a, s_tab_b, ta_row, tb_row)
-    switch (axes) {                 // warp-uniform
+#define B2MD_PAIR_LOOP_OUT(AXES)                                                              \
+    pair_row_loop_outlined<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch,   \
+                                                      pos, a, s_tab_a, s_tab_b, ta_row, tb_row)
+#define B2MD_PAIR_LOOP_LVL(AXES, LVL)                                                         \
+    do { if (B2MD_PAIR_OUTLINE >= LVL) B2MD_PAIR_LOOP_OUT(AXES); else B2MD_PAIR_LOOP(AXES); } while (0)
+    // face frame (see face_frame): legal when every particle of the warp is clear of the
+    // mid-plane on each flagged axis
+    const bool face_ok = (axes & ~clear) == 0;
+    int variant = face_ok ? (axes << 3) : (axes ? 7 : 0);
+    if ((gated >> 2) & 0x3fff) {                     // timing experiments only (profiles/exp)
+        const int v = ((gated >> 2) & 0x3fff) - 1;
+        // 64: flagged warps run a second copy of the no-shift loop (instruction-cache probe)
+        variant = v == 64 ? (axes ? 64 : 0) : v;
+    }
+    switch (variant) {                                     // warp-uniform
         case 0: B2MD_PAIR_LOOP(0); break;
-        case 1: B2MD_PAIR_LOOP(1); break;
-        case 2: B2MD_PAIR_LOOP(2); break;
-        case 4: B2MD_PAIR_LOOP(4); break;
-        default: B2MD_PAIR_LOOP(7); break;
+        case 8: B2MD_PAIR_LOOP_LVL(8, 3); break;
+        case 16: B2MD_PAIR_LOOP_LVL(16, 3); break;
+        case 24: B2MD_PAIR_LOOP_LVL(24, 2); break;
+        case 32: B2MD_PAIR_LOOP_LVL(32, 3); break;
+        case 40: B2MD_PAIR_LOOP_LVL(40, 2); break;
+        case 48: B2MD_PAIR_LOOP_LVL(48, 2); break;
+        case 56: B2MD_PAIR_LOOP_LVL(56, 2); break;
+        default: B2MD_PAIR_LOOP_LVL(7, 1); break;   // tiny boxes / unordered particles: per-pair images
     }
 #undef B2MD_PAIR_LOOP
+#undef B2MD_PAIR_LOOP_OUT
+#undef B2MD_PAIR_LOOP_LVL
     float d2 = 0.0f;
     if (active) {
 #pragma unroll
@@ -650,7 +777,9 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 w = p.c_w * acc.w;
             }
             if (ADVANCE) {
-                float4 h = which ? pb : pa;
+                // the particle's own position is read again (an L1 / L2 hit) instead of being
+                // kept in registers across the row loop: 8 registers of slack there
+                float4 h = reload_f4(pos + i);
                 d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo,
                                                    adv.vel, adv.image, adv.step, adv.ref_pos));
                 adv.pos_out[i] = h;
@@ -667,11 +796,60 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 if (THERMO && virial) virial[i] = w;
             }
             if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-                report_singular((int)i, which ? pb : pa, counts[i], nbr + i, pitch, pos, a.box,
+                report_singular((int)i, reload_f4(pos + i), counts[i], nbr + i, pitch, pos, a.box,
                                 status);
         }
     }
     if (ADVANCE) advance_publish_disp<kPairThreads>(d2, s_max, status, adv);
+}
+
+// ---- block schedule of the pair kernel ---------------------------------------
+// k_pair_block_flags: one warp per block of the pair kernel (kPairThreads pairs = 2 kPairThreads
+// particles): flag = some particle of the block near a periodic face.  k_pair_schedule: one
+// block partitions the flags stably -- flagged blocks first, in their own order, the others
+// behind them -- and writes schedule[position] = block.
+constexpr int kScheduleThreads = 1024;
+
+__global__ void __launch_bounds__(256)
+k_pair_block_flags(const uint8_t *__restrict__ boundary, int64_t n, int n_blocks,
+                   int32_t *__restrict__ flags) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= n_blocks) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t lo = (int64_t)b * 2 * kPairThreads;
+    const int64_t hi = min(lo + 2 * kPairThreads, n);
+    int f = 0;
+    for (int64_t i = lo + lane; i < hi; i += 32) f |= boundary[i] & 7;
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0) flags[b] = f != 0;
+}
+
+__global__ void __launch_bounds__(kScheduleThreads)
+k_pair_schedule(const int32_t *__restrict__ flags, int n_blocks, int32_t *__restrict__ schedule) {
+    __shared__ int s_warp[kScheduleThreads / 32];
+    __shared__ int s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_base = 0;
+    for (int pass = 0; pass < 2; ++pass) {          // pass 0: flagged blocks, pass 1: the rest
+        for (int b0 = 0; b0 < n_blocks; b0 += kScheduleThreads) {
+            __syncthreads();
+            const int b = b0 + threadIdx.x;
+            const int want = b < n_blocks && ((flags[b] != 0) == (pass == 0));
+            const unsigned vote = __ballot_sync(0xffffffffu, want);
+            if (lane == 0) s_warp[warp] = __popc(vote);
+            __syncthreads();
+            int before = 0, total = 0;
+            for (int w = 0; w < kScheduleThreads / 32; ++w) {
+                const int c = s_warp[w];
+                before += w < warp ? c : 0;
+                total += c;
+            }
+            const int base = s_base;
+            if (want) schedule[base + before + __popc(vote & ((1u << lane) - 1u))] = b;
+            __syncthreads();
+            if (threadIdx.x == 0) s_base = base + total;
+        }
+    }
 }
 
 // ---- all pairs, shared-memory tiles of 128 positions ------------------------
@@ -745,6 +923,7 @@ static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int
     }
     a.box = make_box_f(box);
     a.ntypes = ntypes;
+    a.schedule = nullptr;
     for (int t = 0; t < ntypes * ntypes; ++t) {
         const double eps = table[4 * t], sig2 = table[4 * t + 1], rc2 = table[4 * t + 2],
                      shift = table[4 * t + 3];
@@ -863,13 +1042,21 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE><<<blocks, kPairThreads, 0, s>>>(           \
         (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
         d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
-        (flags & B2MD_FORCE_GATED) ? 1 : 0, adv)
+        ((flags & B2MD_FORCE_GATED) ? 1 : 0) | exp_bits, adv)
     // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 4 to 12
     // CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch of the
     // index stream, L1 cache-policy hints, per-SM or per-warp work queues were all neutral
     // or slower.
     const unsigned blocks = blocks_for((n + 1) / 2, kPairThreads);
     const bool sig1 = a.single.sig2 == 1.0f;
+    if (flags & B2MD_FORCE_SCHEDULED) a.schedule = d_pair_counts + pair_pitch;
+    // profiles/exp only: B2MD_EXP_NO_BOUNDARY=1 -> no image shifts anywhere (wrong forces at the
+    // faces), B2MD_EXP_VARIANT=v -> every warp runs image-shift variant v
+    const int exp_variant = env_choice("B2MD_EXP_VARIANT", -1);
+    const int exp_bits = (env_choice("B2MD_EXP_NO_BOUNDARY", 0) ? 2 : 0) |
+                         (exp_variant >= 0 ? (exp_variant + 1) << 2 : 0) |
+                         (env_choice("B2MD_EXP_TILES_PCT", -1) >= 0
+                              ? (env_choice("B2MD_EXP_TILES_PCT", -1) + 1) << 16 : 0);
     if (advance && (adv.halo_dst[0] || adv.halo_dst[1])) {
         if (ntypes == 1) {
             if (sig1) B2MD_LAUNCH_PAIR(false, false, true, 2);
@@ -898,6 +1085,29 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
 }
 
 }  // namespace
+
+B2MD_EXPORT int64_t b2md_pair_schedule_len(int64_t n) {
+    return 2 * (int64_t)blocks_for((n + 1) / 2, kPairThreads);    // the schedule + its flag scratch
+}
+
+B2MD_EXPORT int b2md_pair_schedule(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_counts,
+                                   int64_t pair_pitch, void *stream) {
+    if (n <= 0 || !d_pair_counts || pair_pitch < (n + 1) / 2) {
+        set_error("b2md_pair_schedule: bad arguments");
+        return -1;
+    }
+    const int n_blocks = (int)blocks_for((n + 1) / 2, kPairThreads);
+    int32_t *schedule = d_pair_counts + pair_pitch, *flags = schedule + n_blocks;
+    if (!d_boundary) {
+        set_error("b2md_pair_schedule: no boundary flags");
+        return -2;
+    }
+    k_pair_block_flags<<<blocks_for(n_blocks, 8), 256, 0, as_stream(stream)>>>(d_boundary, n,
+                                                                                n_blocks, flags);
+    k_pair_schedule<<<1, kScheduleThreads, 0, as_stream(stream)>>>(flags, n_blocks, schedule);
+    B2MD_CHECK_LAUNCH("b2md_pair_schedule");
+    return 0;
+}
 
 B2MD_EXPORT int b2md_force_lj_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
                                     const int32_t *d_pair_nbr, const int32_t *d_pair_counts,

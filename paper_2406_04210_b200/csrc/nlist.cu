@@ -30,6 +30,8 @@ struct ListGeom {
     float Lf[3], invLf[3];
     float margin[3];   // boundary flag: within this distance of a periodic face
     float Lhi[3];
+    float mid[3];      // L/2 per axis, and how far from that plane a particle must be for the
+    float mid_clear[3];   // force kernel's face frame (bits 3-5 of the flag); < 0 = never
 };
 
 // One fp64 candidate test, the reference's arithmetic verbatim
@@ -94,12 +96,19 @@ __device__ __forceinline__ void finish_row(int32_t *__restrict__ nbr, int64_t pi
 // Bit a is set when the particle is within `margin` of a periodic face on axis a:
 // only then can one of its listed pairs need an image shift along that axis
 // during the list's lifetime.
+// Bit 3 + a is set when the particle stays clear of the mid-plane x_a = L_a / 2 for the list's
+// whole lifetime by more than any listed pair can span (margin = r_list + skin, plus the
+// particle's own skin / 2 of travel, rounded up to skin): every listed partner is then on
+// the same side of that plane or across the periodic face, which is what the force kernel's
+// face frame (force.cu, face_frame) needs.  Never set in boxes narrower than 4 x that reach.
 __device__ __forceinline__ uint8_t boundary_flag(const float4 h, const ListGeom &g) {
     const float p[3] = {h.x, h.y, h.z};
     int bits = 0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < 3; ++a) {
         if ((p[a] < g.margin[a]) | (p[a] > g.Lhi[a] - g.margin[a])) bits |= 1 << a;
+        if (g.mid_clear[a] >= 0.0f && fabsf(p[a] - g.mid[a]) > g.mid_clear[a]) bits |= 8 << a;
+    }
     return (uint8_t)bits;
 }
 
@@ -790,7 +799,7 @@ k_list_brute(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_l
 __global__ void k_count_boundary(const uint8_t *__restrict__ boundary, int64_t n,
                                  b2md_status *status) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int v = (i < n) ? (boundary[i] != 0) : 0;
+    int v = (i < n) ? ((boundary[i] & 7) != 0) : 0;
     v = warp_sum_i(v);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&status->n_boundary, v);
 }
@@ -923,6 +932,11 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
         g.Lhi[a] = (float)box->edge[a];
         g.invLf[a] = (float)(1.0 / box->edge[a]);
         g.margin[a] = (float)boundary_margin;
+        g.mid[a] = (float)(0.5 * box->edge[a]);
+        // reach of a listed pair (the margin) + the particle's own travel, with slack; the
+        // frame needs the near-face layer (margin) and the mid-plane layer to be disjoint
+        const double clear = boundary_margin + fmax(boundary_margin - r_list, 0.0) + 1e-3 * box->edge[a];
+        g.mid_clear[a] = (0.5 * box->edge[a] - clear > boundary_margin) ? (float)clear : -1.0f;
         lmax = fmax(lmax, box->edge[a]);
     }
     // guard band of the fp32 pre-test (see dist2_f32)

@@ -118,7 +118,8 @@ int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     r->launches += 1;
-    const int flags = (thermo ? 0 : B2MD_FORCE_SKIP_THERMO) | (gated ? B2MD_FORCE_GATED : 0);
+    const int flags = (thermo ? 0 : B2MD_FORCE_SKIP_THERMO) | (gated ? B2MD_FORCE_GATED : 0) |
+                      (c.pair_rows > 0 && c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0);
     if (c.pair_rows > 0)
         return b2md_force_lj_pairs(a.pos_hi, c.n, &c.box, c.pair_nbr, c.pair_counts,
                                    c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
@@ -167,8 +168,9 @@ int launch_advance(b2md_runner *r) {
     return b2md_force_lj_pairs_advance(in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt,
                                        c.ref_pos, r->half_skin2, c.pair_nbr, c.pair_counts,
                                        c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
-                                       r->table.data(), c.ntypes, 0, r->gate_in, gate_out,
-                                       c.status, r->stream);
+                                       r->table.data(), c.ntypes,
+                                       c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0, r->gate_in,
+                                       gate_out, c.status, r->stream);
 }
 
 int reorder_key_bits(const b2md_runner *r) {
@@ -249,6 +251,11 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
         if ((rc = b2md_pair_rows(c.nbr, c.counts, c.pitch, stride_rows(r), c.n, c.pair_nbr,
                                  c.pair_counts, c.pair_pitch, c.pair_rows, s))) return rc;
         *kernels += 1;
+        if (c.pair_schedule) {
+            if ((rc = b2md_pair_schedule(c.boundary, c.n, c.pair_counts, c.pair_pitch, s)))
+                return rc;
+            *kernels += 2;
+        }
     }
     return 0;
 }

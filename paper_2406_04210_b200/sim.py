@@ -312,7 +312,10 @@ class Simulation:
             cfg.queue_depth = max(self.queue_depth, 1)
         if self.pair_rows:
             k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
-            k["pair_counts"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
+            # pair counts, then the block schedule of the pair kernel (b2md_pair_schedule)
+            k["pair_counts"] = torch.zeros(
+                cfg.pair_pitch + int(lib.b2md_pair_schedule_len(n)), dtype=torch.int32, **d)
+            cfg.pair_schedule = 1
             cfg.pair_nbr = k["pair_nbr"].data_ptr()
             cfg.pair_counts = k["pair_counts"].data_ptr()
         # page-locked status mirror and the runner's two streams come from torch's caching
