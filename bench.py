@@ -332,7 +332,11 @@ def run_gpu_arm(args):
                 n_rank = args.total_particles // world
             line = run_slab_benchmark(args, rank, world, local_rank, n_rank, WORKLOAD, METRIC,
                                       measured_peak, ClockSampler,
-                                      scaling="strong" if args.total_particles else "weak")
+                                      scaling="strong" if args.total_particles else "weak",
+                                      cpu_baseline_fn=cpu_baseline_sample,
+                                      workload_config_fn=workload_config,
+                                      min_timed_seconds=MIN_TIMED_SECONDS,
+                                      min_repeats=MIN_REPEATS, max_repeats=MAX_REPEATS)
             dist.destroy_process_group()
         finally:
             sys.stdout.flush()

@@ -393,6 +393,10 @@ int b2md_gather_rows(const void *const *d_src16, void *const *d_dst16, const voi
  *   peer_device afterwards (synchronous; -2 = no peer path between the two). */
 int b2md_halo_slots(const int32_t *d_send_idx, int64_t n_send, int32_t base, int64_t n,
                     int32_t *d_dst, void *stream);
+/* d_out[d_dst[i]] = d_rows[i] (16-byte rows) wherever d_dst[i] >= 0: the same stores the step
+ * kernel issues, on their own -- the start-up probe of a peer mapping. */
+int b2md_halo_store(const void *d_rows_f4, const int32_t *d_dst, int64_t n, void *d_out_f4,
+                    void *stream);
 int b2md_enable_peer_access(int32_t peer_device);
 int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n, double centre,
                        double box_x, double lo_cut, double hi_cut, int32_t *d_flag_left,

@@ -125,6 +125,7 @@ _SIGNATURES = {
     "b2md_compact_indices": (c_int32, [_P, c_int64, _P, _P, _P, _P]),
     "b2md_gather_rows": (c_int32, [_P, _P, _P, _P, _P, c_int64, _P]),
     "b2md_halo_slots": (c_int32, [_P, c_int64, c_int32, c_int64, _P, _P]),
+    "b2md_halo_store": (c_int32, [_P, _P, c_int64, _P, _P]),
     "b2md_enable_peer_access": (c_int32, [c_int32]),
     "b2md_flag_neither": (c_int32, [_P, _P, c_int64, _P, _P]),
     "b2md_snapshot": (c_int32, [_P, _P, _P, c_int64, POINTER(Box), _P, _P, _P]),

@@ -101,6 +101,31 @@ B2MD_EXPORT int b2md_enable_peer_access(int32_t peer_device) {
     return check_cuda(err, "b2md_enable_peer_access");
 }
 
+namespace b2md {
+// out[dst[i]] = rows[i] for every i with dst[i] >= 0: the halo stores of the step kernel
+// on their own (start-up probe of the peer mapping, decomp.py).
+__global__ void k_halo_store(const float4 *__restrict__ rows, const int32_t *__restrict__ dst,
+                             int64_t n, float4 *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int slot = dst[i];
+    if (slot >= 0) out[slot] = rows[i];
+}
+}  // namespace b2md
+
+B2MD_EXPORT int b2md_halo_store(const void *d_rows_f4, const int32_t *d_dst, int64_t n,
+                                void *d_out_f4, void *stream) {
+    if (n < 0 || (n > 0 && (!d_rows_f4 || !d_dst || !d_out_f4))) {
+        set_error("b2md_halo_store: bad arguments");
+        return -1;
+    }
+    if (n == 0) return 0;
+    b2md::k_halo_store<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(
+        (const float4 *)d_rows_f4, d_dst, n, (float4 *)d_out_f4);
+    B2MD_CHECK_LAUNCH("b2md_halo_store");
+    return 0;
+}
+
 B2MD_EXPORT int b2md_slab_classify(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                                    double centre, double box_x, double lo_cut, double hi_cut,
                                    int32_t *d_flag_left, int32_t *d_flag_right, void *stream) {

@@ -211,14 +211,34 @@ __device__ __forceinline__ void warp_sort_pairs(int &key, int &val, int lane) {
 }
 
 // Exact listing decision for particle pair (i, j), kept out of line so that the
-// hot loops do not carry its registers.
-__device__ __noinline__ bool listed_exact(const float4 *__restrict__ pos_hi,
-                                          const float4 *__restrict__ pos_lo, int i, int j,
-                                          const ListGeom &g) {
+// hot loops do not carry its registers.  The geometry travels BY VALUE: the callers hold it
+// as a __grid_constant__ kernel parameter, and a reference would make this function read
+// parameter memory through a generic pointer (legal, but compute-sanitizer cannot follow it
+// into the parameter buffers of graph kernel nodes).
+struct ExactGeom { BoxD box; double rl2; };
+
+__device__ __noinline__ bool listed_exact_v(const float4 *__restrict__ pos_hi,
+                                            const float4 *__restrict__ pos_lo, int i, int j,
+                                            const ExactGeom e) {
     const float4 hi_i = pos_hi[i], lo_i = pos_lo[i];
-    const double pi[3] = {ds_to_double(hi_i.x, lo_i.x), ds_to_double(hi_i.y, lo_i.y),
-                          ds_to_double(hi_i.z, lo_i.z)};
-    return listed_f64(pi, pos_hi[j], pos_lo[j], g);
+    const float4 hj = pos_hi[j], lj = pos_lo[j];
+    double dx = __dsub_rn(ds_to_double(hi_i.x, lo_i.x), ds_to_double(hj.x, lj.x));
+    double dy = __dsub_rn(ds_to_double(hi_i.y, lo_i.y), ds_to_double(hj.y, lj.y));
+    double dz = __dsub_rn(ds_to_double(hi_i.z, lo_i.z), ds_to_double(hj.z, lj.z));
+    dx = min_image_f64(dx, e.box.L[0], e.box.invL[0]);
+    dy = min_image_f64(dy, e.box.L[1], e.box.invL[1]);
+    dz = min_image_f64(dz, e.box.L[2], e.box.invL[2]);
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return r2 < e.rl2;
+}
+
+__device__ __forceinline__ bool listed_exact(const float4 *__restrict__ pos_hi,
+                                             const float4 *__restrict__ pos_lo, int i, int j,
+                                             const ListGeom &g) {
+    ExactGeom e;
+    e.box = g.box;
+    e.rl2 = g.rl2;
+    return listed_exact_v(pos_hi, pos_lo, i, j, e);
 }
 
 constexpr int kBandTag = (int)0x80000000;

@@ -145,6 +145,20 @@ class SlabComm:
         self.bytes_sent += to_left.numel() * to_left.element_size() + \
             to_right.numel() * to_right.element_size()
 
+    def self_check(self, device):
+        """Start-up check of the ring plumbing: every rank sends its own id both ways and must
+        receive its left neighbour's id "from the left" and its right neighbour's "from the
+        right".  Catches the world == 2 trap (both neighbours are the same rank and NCCL
+        matches a pair's messages in posting order, ignoring tags) on whatever backend is in
+        use, before any particle data moves."""
+        g = self.geo
+        from_l, from_r = self.exchange_ints([g.rank, 1], [g.rank, 2], device)
+        # what my LEFT neighbour sent rightwards carries marker 2, and vice versa
+        if from_l != [g.left, 2] or from_r != [g.right, 1]:
+            raise ConfigError(f"slab ring self-check failed on rank {g.rank}: received {from_l} "
+                              f"from the left (want [{g.left}, 2]) and {from_r} from the right "
+                              f"(want [{g.right}, 1])")
+
     def exchange(self, to_left, to_right, from_left, from_right):
         """Variable-size record exchange (sizes agreed on beforehand)."""
         self._ring(to_left, to_right, from_right, from_left)
@@ -186,6 +200,7 @@ class SlabSimulation:
         self.ahead = False            # one-launch steps: particles already at the next step
         self.halo_rows = (0, 0)
         self.ops.attach(self.geo, lj, self.dt, self.skin)
+        comm.self_check(self.ops.device)
         # Per-step halo fused into the step kernel (backends with `connect_peers`): the
         # advanced high words of the send-list rows are stored by the kernel itself into
         # the ghost rows of the neighbour ranks' position buffers, mapped into this process
@@ -193,7 +208,27 @@ class SlabSimulation:
         connect = getattr(self.ops, "connect_peers", None)
         self.fused_halo = bool(connect(comm)) if connect else False
         self._rebuild()
+        if self.fused_halo:
+            self._probe_peer_halo()
         self.ops.force(thermo=True)
+
+    def _probe_peer_halo(self):
+        """One halo through each transport before the first step: the NCCL exchange fills the
+        ghost rows, the peer stores (same destination slots as the step kernel uses) overwrite
+        them; the ghost rows must not change.  A mismatch anywhere -- wrong mapping, a peer
+        path that silently drops writes -- turns the fused halo off on every rank, loudly."""
+        ops, comm = self.ops, self.comm
+        probe = getattr(ops, "probe_peer_halo", None)
+        if probe is None:
+            return
+        self._halo()                                   # reference content, over NCCL
+        bad = probe(comm)                              # 0 / 1, already agreed on by all ranks
+        if bad:
+            import warnings
+            warnings.warn("slab halo: peer stores did not reproduce the NCCL halo; falling back "
+                          "to NCCL send/recv on all ranks", RuntimeWarning)
+            ops.disconnect_peers()
+            self.fused_halo = False
 
     # -- rebuild: migrate, reorder, ghosts, list ------------------------------
     def _rebuild(self):
@@ -472,8 +507,10 @@ class CudaSlabOps:
             self.pair_pitch = ((self.cap_own + 1) // 2 + 31) // 32 * 32
             self.pair_nbr = self.torch.zeros((2 * rows // 4, self.pair_pitch, 4),
                                              dtype=self.torch.int32, device=self.device)
-            self.pair_counts = self.torch.zeros(self.pair_pitch, dtype=self.torch.int32,
-                                                device=self.device)
+            # pair counts + the block schedule of the pair kernel (b2md_pair_schedule)
+            self.pair_counts = self.torch.zeros(
+                self.pair_pitch + int(_lib.load().b2md_pair_schedule_len(self.cap_own)),
+                dtype=self.torch.int32, device=self.device)
 
     def grow_stride(self, max_count):
         self.stride = max(self.stride + 1, ((int(max_count * 1.125) + 1) + 7) // 8 * 8)
@@ -567,11 +604,12 @@ class CudaSlabOps:
         _lib.call("b2md_sort_pairs_u64", self.keys.data_ptr(), self.perm.data_ptr(),
                   self.keys_tmp.data_ptr(), self.perm_tmp.data_ptr(), n, key_bits,
                   self.sort_scratch.data_ptr(), self.stream)
-        for name in ("pos_hi", "pos_lo", "vel", "force", "image"):
-            _lib.call("b2md_gather16", src[name].data_ptr(), dst[name].data_ptr(),
-                      self.perm.data_ptr(), n, self.stream)
+        names = ("pos_hi", "pos_lo", "vel", "force", "image")
+        srcs = (ctypes.c_void_p * 5)(*[src[name].data_ptr() for name in names])
+        dsts = (ctypes.c_void_p * 5)(*[dst[name].data_ptr() for name in names])
+        _lib.call("b2md_gather_rows", srcs, dsts, None, None, self.perm.data_ptr(), n, self.stream)
         self.cur = 1 - self.cur
-        self.kernel_launches += 2 + 5 * ((key_bits + 7) // 8) + 5
+        self.kernel_launches += 2 + 5 * ((key_bits + 7) // 8) + 1
 
     def select_ghosts(self, r_ghost):
         if self.geo.world == 1:
@@ -646,7 +684,9 @@ class CudaSlabOps:
                       self.capacity, self.nbr.shape[0], self.n_own, self.pair_nbr.data_ptr(),
                       self.pair_counts.data_ptr(), self.pair_pitch, 2 * self.nbr.shape[0],
                       self.stream)
-            self.kernel_launches += 1
+            _lib.call("b2md_pair_schedule", self.boundary.data_ptr(), self.n_own,
+                      self.pair_counts.data_ptr(), self.pair_pitch, self.stream)
+            self.kernel_launches += 3
         st = _lib.Status.from_buffer_copy(self.status.cpu().numpy().tobytes())
         return st.overflow != 0, st.max_count
 
@@ -670,7 +710,8 @@ class CudaSlabOps:
                       ctypes.byref(self.box), self.pair_nbr.data_ptr(),
                       self.pair_counts.data_ptr(), self.pair_pitch, self.nbr.data_ptr(),
                       self.counts.data_ptr(), self.capacity, self.boundary.data_ptr(),
-                      self.table_ptr, self.lj.ntypes, 0 if thermo else _lib.FORCE_SKIP_THERMO,
+                      self.table_ptr, self.lj.ntypes,
+                      (0 if thermo else _lib.FORCE_SKIP_THERMO) | _lib.FORCE_SCHEDULED,
                       a["force"].data_ptr(), self.virial.data_ptr(), self.status.data_ptr(),
                       self.stream)
             self.kernel_launches += 1
@@ -739,6 +780,31 @@ class CudaSlabOps:
                       dst.data_ptr(), self.stream)
             self.kernel_launches += 2 if count else 1
 
+    def probe_peer_halo(self, comm) -> int:
+        """Store the send-list rows of the live buffer into the neighbours' ghost rows through
+        the peer mapping (b2md_halo_store, the step kernel's stores on their own) and check
+        that my own ghost rows -- filled over NCCL just before -- are unchanged once every
+        rank has stored.  Returns 1 if any rank saw a difference."""
+        torch = self.torch
+        a = self.a
+        k = self.pos_index[a["pos_hi"].data_ptr()]
+        (l0, l1), (r0, r1) = self.ghost_ranges
+        want = a["pos_hi"][l0:r1].clone()
+        comm.all_max(torch.zeros(1, dtype=torch.int64, device=self.device))   # everyone cloned
+        for side in range(2):
+            _lib.call("b2md_halo_store", a["pos_hi"].data_ptr(), self.halo_dst[side].data_ptr(),
+                      self.n_own, self.peer_pos[side][k].data_ptr(), self.stream)
+        torch.cuda.synchronize(self.device)
+        comm.all_max(torch.zeros(1, dtype=torch.int64, device=self.device))   # everyone stored
+        bad = int(not torch.equal(want, a["pos_hi"][l0:r1]))
+        flag = comm.all_max(torch.tensor([bad], dtype=torch.int64, device=self.device))
+        return int(flag.item())
+
+    def disconnect_peers(self):
+        self.peer_pos = None
+        self.halo_dst = None
+        self.peer_halo_unavailable = "start-up probe: peer stores did not reproduce the NCCL halo"
+
     # -- one-launch steps (see SlabSimulation._run_advance) ------------------------
     GATE_WORDS = (5, 12)              # rebuild_flag, reserved[0] (include/b2md.h)
 
@@ -775,9 +841,38 @@ class CudaSlabOps:
                   self.ref_pos.data_ptr(), half_skin2, self.pair_nbr.data_ptr(),
                   self.pair_counts.data_ptr(), self.pair_pitch, self.nbr.data_ptr(),
                   self.counts.data_ptr(), self.capacity, self.boundary.data_ptr(), self.table_ptr,
-                  self.lj.ntypes, 0, self.gate_in, self.gate_out, *halo, self.status.data_ptr(),
-                  self.stream)
+                  self.lj.ntypes, _lib.FORCE_SCHEDULED, self.gate_in, self.gate_out, *halo,
+                  self.status.data_ptr(), self.stream)
         self.kernel_launches += 1
+
+    def time_step_kernel(self, iters: int):
+        """CUDA-event time (ms) of the one-launch step kernel on this rank's owned rows, on
+        scratch copies of everything it updates in place (no halo stores, its own status
+        block, dt ~ 0 so that repeated launches see the same positions)."""
+        torch = self.torch
+        a = self.a
+        sc = {k: a[k].clone() for k in ("pos_lo", "vel", "image")}
+        ref, out = self.ref_pos.clone(), torch.empty_like(a["pos_hi"])
+        status = torch.zeros(16, dtype=torch.int32, device=self.device)
+
+        def launch():
+            _lib.call("b2md_force_lj_pairs_advance", a["pos_hi"].data_ptr(), out.data_ptr(),
+                      sc["pos_lo"].data_ptr(), sc["vel"].data_ptr(), sc["image"].data_ptr(),
+                      self.n_own, ctypes.byref(self.box), 1e-9, ref.data_ptr(), 1e30,
+                      self.pair_nbr.data_ptr(), self.pair_counts.data_ptr(), self.pair_pitch,
+                      self.nbr.data_ptr(), self.counts.data_ptr(), self.capacity,
+                      self.boundary.data_ptr(), self.table_ptr, self.lj.ntypes,
+                      _lib.FORCE_SCHEDULED, 12, 14, status.data_ptr(), self.stream)
+        stream = torch.cuda.current_stream(self.device)
+        launch()
+        torch.cuda.synchronize(self.device)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(iters):
+            launch()
+        t1.record(stream)
+        torch.cuda.synchronize(self.device)
+        return t0.elapsed_time(t1) / iters
 
     def swap_positions(self):
         """The other position buffer becomes the live one (no copy: every kernel call
@@ -846,10 +941,14 @@ def slab_initial_state(rank, world, n_per_rank, density, temperature, seed=42):
 
 
 def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metric,
-                       measured_peak, clock_sampler_cls, scaling="weak"):
+                       measured_peak, clock_sampler_cls, scaling="weak", cpu_baseline_fn=None,
+                       workload_config_fn=None, min_timed_seconds=1.0, min_repeats=3,
+                       max_repeats=400):
     """bench.py's N > 1 arm: `n_per_rank` particles per rank (weak scaling: 1 M per rank;
-    strong scaling: a fixed total split over the ranks).  Returns the JSON line (a dict) on
-    rank 0, None elsewhere."""
+    strong scaling: a fixed total split over the ranks).  The timed region is run(K) repeated
+    back to back (barrier + device synchronise around every repeat, CUDA events, maximum over
+    ranks per repeat) until `min_timed_seconds` of GPU time are collected -- as on one GPU.
+    Returns the JSON line (a dict) on rank 0, None elsewhere."""
     torch = _torch()
     import torch.distributed as dist
     from .potential import make_shifted
@@ -859,68 +958,94 @@ def run_slab_benchmark(args, rank, world, local_rank, n_per_rank, workload, metr
     geo = SlabGeometry(rank, world, edges)
     ops = CudaSlabOps(pos, vel, ids, edges, device_index=local_rank)
     sim = SlabSimulation(ops, SlabComm(geo), lj, dt, skin, sample_interval=100)
-    sim.run(args.warmup)
+    sim.run(max(args.warmup, 3))
     ops.kernel_launches = 0
     ops.peer_bytes = 0
     sim.comm.bytes_sent = 0
     rebuilds0 = sim.rebuilds
     stream = torch.cuda.current_stream()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = clock_sampler_cls(local_rank)
-    dist.barrier()
-    torch.cuda.synchronize()
+    if hasattr(clocks, "sample_now"):
+        clocks.sample_now()
     clocks.start()
-    start.record(stream)
-    sim.run(args.steps)
-    stop.record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
+    rep_ms = []
+    while True:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        sim.run(args.steps)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=ops.device)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)          # every rank sees the same figure
+        rep_ms.append(float(ms.item()))
+        if (len(rep_ms) >= min_repeats and sum(rep_ms) >= 1e3 * min_timed_seconds) \
+                or len(rep_ms) >= max_repeats:
+            break
+    if hasattr(clocks, "sample_now"):
+        clocks.sample_now()
     clock_info = clocks.stop()
-    ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=ops.device)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    repeats = len(rep_ms)
     launches = torch.tensor([ops.kernel_launches], dtype=torch.int64, device=ops.device)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
     sample = sim.measure()
-    if rank == 0:
-        ms = float(ms.item())
-        n_total = n_per_rank * world
-        value = n_total * args.steps / (ms * 1e-3)
-        peak, peak_src = measured_peak()
-        cbar = float(ops.counts[:ops.n_own].float().mean().item())
-        step_bytes = n_per_rank * (216.0 + 4.0 * cbar)
-        line = {
-            "metric": metric, "value": value, "unit": metric, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-            "dtype": "f32 pair arithmetic, double-single positions, f64 reductions",
-            "data": "synthetic",
-            "config": {"workload": workload, "particles": n_total,
-                       "particles_per_gpu": n_per_rank,
-                       "decomposition": f"{world} x-slabs of a {edges[0]:.1f} x {edges[1]:.1f} x "
-                                        f"{edges[2]:.1f} box, ghost width {sim.r_list}",
-                       "halo_rows_per_face": list(sim.halo_rows),
-                       "l2": "inputs larger than L2 (neighbour list streamed every step)",
-                       "mean_listed_neighbours": cbar,
-                       "rebuilds_in_timed_region": sim.rebuilds - rebuilds0,
-                       "step_hbm_fraction_per_gpu": step_bytes * value / n_total / 1e9 / peak,
-                       "final_energy_per_particle": sample["total_energy"] / n_total},
-            "clocks": clock_info, "gpu_launches": int(launches.item()),
-            "roofline": {"bound": "hbm",
-                         "kernel": "k_force_lj_pair<ADVANCE> (one launch per MD step on the "
-                                   "owned rows)" if ops.can_advance else "k_force_lj",
-                         "achieved": None, "peak": peak,
-                         "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src,
-                         "note": "per-kernel roofline is measured by the 1-GPU arm"},
-            "e2e": {"value": value, "unit": metric, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 64,
-                    "note": "multi-GPU arm: state generated per rank on the host and uploaded "
-                            "before the timed region; 8 doubles all-reduced and read back per "
-                            "sample"},
-            "nccl_bytes_sent_rank0_per_step": sim.comm.bytes_sent / max(args.steps, 1),
-            "halo": {"transport": "peer stores from the step kernel (CUDA IPC, NVLink)"
-                     if sim.fused_halo else "NCCL send/recv",
-                     "peer_bytes_stored_rank0_per_step": ops.peer_bytes / max(args.steps, 1),
-                     "why_not_peer": getattr(ops, "peer_halo_unavailable", None)},
-        }
-        return line
-    return None
+    # the step kernel alone on this rank's own rows (rank 0 reports it): same accounting as the
+    # 1-GPU arm -- (128 + 4 c) bytes per owned particle over its CUDA-event time
+    cbar = float(ops.counts[:ops.n_own].float().mean().item())
+    kernel_ms = ops.time_step_kernel(30) if ops.can_advance else None
+    if rank != 0:
+        return None
+    ms = sum(rep_ms) / repeats
+    n_total = n_per_rank * world
+    value = n_total * args.steps / (ms * 1e-3)
+    peak, peak_src = measured_peak()
+    step_bytes = n_per_rank * (216.0 + 4.0 * cbar)
+    adv_bytes = ops.n_own * (128.0 + 4.0 * cbar)
+    achieved = adv_bytes / (kernel_ms * 1e-3) / 1e9 if kernel_ms else None
+    cfg = workload_config_fn(n_total, n_per_rank) if workload_config_fn else \
+        {"workload": workload, "particles": n_total, "particles_per_gpu": n_per_rank}
+    cfg.update({
+        "decomposition": f"{world} x-slabs of a {edges[0]:.1f} x {edges[1]:.1f} x "
+                         f"{edges[2]:.1f} box, ghost width {sim.r_list}",
+        "halo_rows_per_face": list(sim.halo_rows),
+        "l2": "inputs larger than L2 (neighbour list streamed every step)",
+        "timed_region": f"{repeats} back-to-back repeats of run({args.steps}), "
+                        f"{sum(rep_ms) / 1e3:.2f} s; per repeat the maximum over ranks",
+        "timed_repeats": repeats,
+        "ms_per_step_median_repeat": sorted(rep_ms)[repeats // 2] / args.steps,
+        "ms_per_step_best_repeat": min(rep_ms) / args.steps,
+        "mean_listed_neighbours": cbar,
+        "rebuilds_in_timed_region": sim.rebuilds - rebuilds0,
+        "step_hbm_fraction_per_gpu": step_bytes * value / n_total / 1e9 / peak,
+        "final_energy_per_particle": sample["total_energy"] / n_total})
+    line = {
+        "metric": metric, "value": value, "unit": metric, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "f32 pair arithmetic, double-single positions, f64 reductions",
+        "data": "synthetic",
+        "config": cfg,
+        "clocks": clock_info, "gpu_launches": int(launches.item()),
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_force_lj_pair<ADVANCE> on rank 0's owned rows (force + finalize "
+                               "+ integrate + halo stores: one launch per MD step), timed alone"
+                               if ops.can_advance else "k_force_lj",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "peak_source": peak_src, "launch_ms": kernel_ms,
+                     "algorithmic_bytes_per_launch": adv_bytes if kernel_ms else None},
+        "cpu_baseline": cpu_baseline_fn(n_per_rank) if cpu_baseline_fn else None,
+        "e2e": {"value": value, "unit": metric, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 64,
+                "note": "multi-GPU arm: state generated per rank on the host and uploaded "
+                        "before the timed region; 8 doubles all-reduced and read back per "
+                        "sample"},
+        "nccl_bytes_sent_rank0_per_step": sim.comm.bytes_sent / max(args.steps * repeats, 1),
+        "halo": {"transport": "peer stores from the step kernel (CUDA IPC, NVLink)"
+                 if sim.fused_halo else "NCCL send/recv",
+                 "peer_bytes_stored_rank0_per_step": ops.peer_bytes / max(args.steps * repeats, 1),
+                 "why_not_peer": getattr(ops, "peer_halo_unavailable", None)},
+    }
+    return line
