@@ -201,6 +201,30 @@ int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
  * pair_rows (entries per pair row): multiple of 4, >= 2 * stride, so a merge can
  * never overflow.  Derived data: the per-particle list stays the source of truth
  * (and what build_neighbor_list returns, neighbor.py:185-240). */
+/* Persistent step kernel for small systems (no counterpart in the reference: it is the
+ * per-step launch overhead of a device that it removes).  ONE cooperative launch runs up to
+ * n_steps MD steps -- each the body of b2md_force_lj_advance (force, both half-kicks, drift,
+ * wrap, displacement check), separated by grid-wide barriers -- over the per-particle list.
+ * Step s reads the position high words in d_pos_a (s even) / d_pos_b (s odd) and writes the
+ * other buffer; gate_a_word / gate_b_word are the status words holding the rebuild flag of
+ * the positions in d_pos_a / d_pos_b.  The loop stops before a step whose input positions
+ * need a new list; every completed step adds one to status word 13 (the advance counter), so
+ * the caller learns how many steps ran and which buffer is live.  d_barrier: 4 bytes of
+ * device scratch.  stride (allocated rows of the list) must be a multiple of 16 entries per
+ * lane group: b2md_steps_persistent_lanes(n, stride, ntypes) returns the lanes per particle
+ * the launch would use on the current device (16 or 4), 0 when the grid cannot be
+ * co-resident -- b2md_steps_persistent then fails with -6 and launches nothing.
+ * status->frozen != 0 afterwards: a barrier timed out (never expected; the launch is
+ * cooperative) and the loop was abandoned. */
+int b2md_steps_persistent_lanes(int64_t n, int32_t stride, int32_t ntypes);
+int b2md_steps_persistent(void *d_pos_a, void *d_pos_b, void *d_pos_lo, void *d_vel,
+                          void *d_image_i4, int64_t n, const b2md_box *box, double dt,
+                          void *d_ref_pos_f4, double half_skin2, const int32_t *d_nbr,
+                          const int32_t *d_counts, int64_t pitch, int32_t stride,
+                          const uint8_t *d_boundary, const double *table, int32_t ntypes,
+                          int32_t gate_a_word, int32_t gate_b_word, int32_t n_steps,
+                          uint32_t *d_barrier, b2md_status *d_status, void *stream);
+
 /* Block schedule of the pair kernels (optional).  Blocks whose particles sit near a
  * periodic face (d_boundary, written by b2md_build_nlist) take the image-shift paths and run
  * up to 1.7x longer; in particle order they are dispatched last (a space-filling curve ends
@@ -475,6 +499,13 @@ typedef struct b2md_runner_config {
                                     want several */
     int32_t pair_schedule;       /* != 0: pair_counts has b2md_pair_schedule_len(n) more entries;
                                     the runner keeps a block schedule there (see above) */
+    int32_t persistent_steps;    /* > 0: intermediate steps of systems without pair rows run in
+                                    batches of up to this many steps per launch of
+                                    b2md_steps_persistent (needs pos_hi_alt, barrier and
+                                    list_row_multiple = 64); 0: one launch per step */
+    int32_t list_row_multiple;   /* nbr holds round_up(stride, this) rows; 0 = 16 (64 lets the
+                                    persistent kernel use 16 lanes per particle) */
+    uint32_t *barrier;           /* 4 bytes of device scratch (persistent_steps > 0) */
     /* Optional caller-owned resources (NULL = the runner creates and destroys its own).
      * Page-locking memory and creating streams are the expensive parts of creating a
      * runner (1-7 ms measured on B200); a caller that builds many short-lived simulations

@@ -70,6 +70,7 @@ class RunnerConfig(Structure):
         ("use_graph", c_int32), ("pair_rows", c_int32),
         ("pair_nbr", c_void_p), ("pair_counts", c_void_p), ("pair_pitch", c_int64),
         ("pos_hi_alt", c_void_p), ("queue_depth", c_int32), ("pair_schedule", c_int32),
+        ("persistent_steps", c_int32), ("list_row_multiple", c_int32), ("barrier", c_void_p),
         ("h_status", c_void_p), ("run_stream", c_void_p), ("copy_stream", c_void_p),
     ]
 
@@ -133,6 +134,10 @@ _SIGNATURES = {
     "b2md_force_lj": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, c_int32, _P,
                                 POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_pair_rows": (c_int32, [_P, _P, c_int64, c_int32, c_int64, _P, _P, c_int64, c_int32, _P]),
+    "b2md_steps_persistent_lanes": (c_int32, [c_int64, c_int32, c_int32]),
+    "b2md_steps_persistent": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,
+                                        c_double, _P, _P, c_int64, c_int32, _P, POINTER(c_double),
+                                        c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
     "b2md_pair_schedule_len": (c_int64, [c_int64]),
     "b2md_pair_schedule": (c_int32, [_P, c_int64, _P, c_int64, _P]),
     "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
@@ -185,7 +190,8 @@ _SIGNATURES = {
 
 #: entry points that report errors through their int return value
 _CHECKED = {name for name, (res, _) in _SIGNATURES.items()
-            if res is c_int32 and name not in ("b2md_version", "b2md_hilbert_key_bits")}
+            if res is c_int32 and name not in ("b2md_version", "b2md_hilbert_key_bits",
+                                             "b2md_steps_persistent_lanes")}
 
 _lib = None
 

@@ -47,6 +47,24 @@ constexpr int kForceThreads = 128;
 constexpr int kPairThreads = B2MD_PAIR_THREADS;    // CTA size of k_force_lj_pair (1024 threads per SM)
 constexpr int kMaxTypes = 8;
 
+// Lanes per particle of the row kernels (k_force_lj, its ADVANCE form and the persistent
+// step kernel all take the same decision, so their per-particle sums -- partial sums of the
+// lanes combined by shuffles -- are bit-identical): the widest sub-warp whose grid of n * lanes
+// threads fits the device at once (148 SMs x 1024 threads; small systems are latency-bound
+// serial row loops, the more lanes the shorter) and whose trips of 4 * lanes entries stay
+// inside the `rows` allocated per row.  B2MD_FORCE_SUBWARP pins it (A/B runs).
+inline int lanes_for(int64_t n, int rows) {
+    const int pinned = env_choice("B2MD_FORCE_SUBWARP", 0);
+    const int cand[4] = {16, 4, 2, 1};
+    for (int k = 0; k < 4; ++k) {
+        const int sub = cand[k];
+        if (pinned && sub != pinned) continue;
+        if (rows % (4 * sub) != 0) continue;
+        if (pinned || n * sub <= (int64_t)kNumSM * 1024) return sub;
+    }
+    return 1;
+}
+
 struct PairParams {   // one species pair, fp32
     float sig2, rc2, c_f, c_u;   // sigma^2, rc^2, 24*eps, 2*eps
     float half_shift, c_w;       // shift/2, 12*eps
@@ -171,10 +189,20 @@ __device__ __forceinline__ void lj_pair_table(RowAcc &acc, float dx, float dy, f
 // gather of 32 scattered float4 costs ~11 wavefronts.  (Routing half of them through the TEX
 // pipe of the same cache was measured in round 1 and did not pay; the texture path and its
 // process-wide object cache are gone.)
-__device__ __forceinline__ void gather4(float4 (&pj)[4], const int (&j)[4],
-                                        const float4 *__restrict__ pos) {
+// A coherent 16-byte load (ld.global, L1-cacheable but inside the memory model): what the
+// persistent step kernel gathers with -- its positions are rewritten by other blocks of the
+// same launch, so the read-only path of __ldg is off limits there.
+__device__ __forceinline__ float4 ld_coherent_f4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool NC = true>
+__device__ __forceinline__ void gather4(float4 (&pj)[4], const int (&j)[4], const float4 *pos) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + j[u]);
+    for (int u = 0; u < 4; ++u) pj[u] = NC ? __ldg(pos + j[u]) : ld_coherent_f4(pos + j[u]);
 }
 
 // AXES: bit a set = pairs of this warp may need an image shift along axis a.
@@ -206,10 +234,10 @@ __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, 
 // PIPE = true additionally keeps the NEXT trip's four position gathers in flight
 // while the current trip is being computed (deeper memory-level parallelism at
 // the price of 16 more registers).
-template <int SUB, int PIPEK, int AXES, bool TABLE, bool THERMO>
+template <int SUB, int PIPEK, int AXES, bool TABLE, bool THERMO, bool NC = true>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
-                                         int64_t pitch, const float4 *__restrict__ pos,
+                                         int64_t pitch, const float4 *pos,
                                          const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
                                          int ti_row) {
@@ -223,14 +251,14 @@ __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, 
         jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
     }
     float4 pa[4], pb[4];
-    if (PIPE) gather4(pa, ja, pos);
+    if (PIPE) gather4<NC>(pa, ja, pos);
     for (int base = 0; base < kmax; base += kTrip) {
         int jc[4];
         const bool more = base + 2 * kTrip < kmax;          // warp-uniform
 #pragma unroll
         for (int u = 0; u < 4; ++u) jc[u] = more ? __ldcs(col + (8 + u) * step) : 0;
-        if (PIPE) gather4(pb, jb, pos);                      // row 0 is always a valid index
-        else gather4(pa, ja, pos);
+        if (PIPE) gather4<NC>(pb, jb, pos);                  // row 0 is always a valid index
+        else gather4<NC>(pa, ja, pos);
         if (base + kTrip <= kmin)
             compute4<SUB, AXES, TABLE, THERMO, false>(acc, pi, cnt, base + k0, pa, a, s_tab_a,
                                                          s_tab_b, ti_row);
@@ -404,6 +432,140 @@ k_force_lj(const float4 *__restrict__ pos, int64_t n,
             report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
     }
     if (ADVANCE) advance_publish_disp(d2, s_max, status, adv);
+}
+
+// ---- persistent step kernel (small systems) -------------------------------------
+// Below ~10^5 particles an MD step is shorter than what a launch plus a host round trip
+// costs (17 us per step at N = 4096 with one gated launch per step).  Here ONE cooperative
+// launch runs up to n_steps steps: every step is the body of k_force_lj<SUB, ADVANCE> --
+// force, both half-kicks, drift, wrap, displacement check -- followed by a grid-wide barrier;
+// the position high words ping-pong between two buffers, everything else a thread updates
+// is private to its particle.  The loop ends early when the positions it is about to use
+// need a new list (the flag word of those positions, exactly as the gated launches hand it
+// on); the device counts the steps it took, the host reads count and flags once.
+//
+// Memory model: positions written by other blocks are gathered with plain ld.global (never
+// the read-only path); the barrier is a release (fence + atomic add) / acquire (fence after
+// the spin) pair at gpu scope, which also drops stale L1 lines of the executing SM.
+// A barrier that does not complete within kBarrierTimeout clocks (it cannot, unless the grid
+// is not co-resident -- the launch is cooperative -- or a block died) sets status->frozen and
+// lets every block leave: a bug here must not hang the device.
+struct PersistArgs {
+    float4 *pos[2];           // step s reads pos[s & 1], writes pos[(s & 1) ^ 1]
+    int gate[2];              // status word holding the rebuild flag of pos[0] / pos[1]
+    int n_steps;
+    unsigned *barrier;        // zeroed by the host before the launch
+};
+
+constexpr long long kBarrierTimeout = 4000000000ll;      // ~2 s at 1.97 GHz
+
+__device__ __forceinline__ bool grid_barrier(unsigned *counter, unsigned target, b2md_status *status) {
+    __shared__ int s_ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();                                   // release: my block's stores
+        atomicAdd(counter, 1u);
+        const long long t0 = clock64();
+        int ok = 1;
+        while (*(volatile unsigned *)counter < target) {
+            if (clock64() - t0 > kBarrierTimeout || *(volatile int *)&status->frozen) {
+                status->frozen = 1;
+                ok = 0;
+                break;
+            }
+        }
+        __threadfence();                                   // acquire: everybody else's stores
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+template <int SUB, bool TABLE>
+__global__ void __launch_bounds__(kForceThreads, 8)
+k_steps_persistent(int64_t n, const __grid_constant__ ForceArgs a,
+                   const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
+                   int64_t pitch, const uint8_t *__restrict__ boundary, b2md_status *status,
+                   const __grid_constant__ AdvanceArgs adv, const __grid_constant__ PersistArgs ps) {
+    __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float s_max[kForceThreads / 32];
+    if (TABLE) {
+        for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
+            s_tab_a[t] = a.tab_a[t];
+            s_tab_b[t] = a.tab_b[t];
+        }
+        __syncthreads();
+    }
+    constexpr int kPerBlock = kForceThreads / SUB;
+    const int sub = threadIdx.x % SUB;
+    const int64_t i_raw = blockIdx.x * (int64_t)kPerBlock + threadIdx.x / SUB;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    // the list does not change during the launch
+    const int cnt = active ? counts[i] : 0;
+    const int kmax = __reduce_max_sync(0xffffffffu, cnt);
+    const int kmin = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff);
+    const int axes = boundary ? (__reduce_or_sync(0xffffffffu, active ? (int)boundary[i] : 0) & 7) : 7;
+    const int32_t *col = nbr + (int64_t)sub * pitch + i;
+    const int ti_row = TABLE ? __float_as_int(ld_coherent_f4(ps.pos[0] + i).w) * a.ntypes : 0;
+
+    for (int s = 0; s < ps.n_steps; ++s) {
+        const int w_in = ps.gate[s & 1], w_out = ps.gate[(s & 1) ^ 1];
+        // grid-uniform: written before the previous barrier (or by an earlier launch)
+        if (((volatile int *)status)[w_in]) break;
+        const float4 *pos = ps.pos[s & 1];
+        float4 *pos_out = ps.pos[(s & 1) ^ 1];
+        const float4 pi = ld_coherent_f4(pos + i);
+        RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+#define B2MD_ROW_LOOP(AXES)                                                                 \
+    row_loop<SUB, 0, AXES, TABLE, false, false>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, \
+                                                a, s_tab_a, s_tab_b, ti_row)
+        switch (axes) {                 // warp-uniform
+            case 0: B2MD_ROW_LOOP(0); break;
+            case 1: B2MD_ROW_LOOP(1); break;
+            case 2: B2MD_ROW_LOOP(2); break;
+            case 4: B2MD_ROW_LOOP(4); break;
+            default: B2MD_ROW_LOOP(7); break;
+        }
+#undef B2MD_ROW_LOOP
+#pragma unroll
+        for (int o = SUB >> 1; o > 0; o >>= 1) {
+            acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
+            acc.fy += __shfl_xor_sync(0xffffffffu, acc.fy, o);
+            acc.fz += __shfl_xor_sync(0xffffffffu, acc.fz, o);
+        }
+        float d2 = 0.0f;
+        if (active && sub == 0) {
+            float fx, fy, fz;
+            if (TABLE) {
+                fx = acc.fx; fy = acc.fy; fz = acc.fz;
+            } else {
+                const PairParams &p = a.single;
+                fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
+            }
+            float4 h = pi;
+            d2 = advance_particle<2>(i, h, make_float4(fx, fy, fz, 0.0f), adv.pos_lo, adv.vel,
+                                     adv.image, adv.step, adv.ref_pos);
+            pos_out[i] = h;
+            if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
+                report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
+        }
+        // displacement maximum of the block -> status; the flag of the new positions
+        d2 = warp_max(d2);
+        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+            m = warp_max(m);
+            if (threadIdx.x == 0 && m > 0.0f) {
+                atomicMax(&status->max_disp2_bits, __float_as_uint(m));
+                if (m > adv.step.half_skin2) ((int *)status)[w_out] = 1;
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&((int *)status)[kWordAdvanceCount], 1);
+        if (!grid_barrier(ps.barrier, gridDim.x * (unsigned)(s + 1), status)) break;
+    }
 }
 
 // ---- pair rows: two particles per thread -------------------------------------
@@ -963,12 +1125,11 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
     // Defaults chosen from profiles/ (DESIGN.md section 6), measured on B200 at N = 1 M: 12 CTAs/SM
     // (<= 40 registers) beats 8 CTAs/SM by 5 %; one lane per particle beats sub-warps for
-    // large systems, while small systems (few CTAs, latency-bound serial row loops) want 4
-    // lanes per particle.  The A/B knobs are read per call: the library keeps no state.
-    const int sub_env = env_choice("B2MD_FORCE_SUBWARP", 0);     // lanes per particle: 1, 2, 4
+    // large systems, while small systems (few CTAs, latency-bound serial row loops) want as
+    // many lanes per particle as the device holds at once (lanes_for).  The A/B knobs are
+    // read per call: the library keeps no state.
     const int pipe = env_choice("B2MD_FORCE_PIPE", 2) == 0 ? 0 : 2;   // 0: 8 CTAs/SM, 2: 12
-    const int sub = (sub_env == 1 || sub_env == 2 || sub_env == 4) ? sub_env
-                                                                   : (n < 200000 ? 4 : 1);
+    const int sub = lanes_for(n, stride);
 #define B2MD_LAUNCH_FORCE(SUB, PIPE, TABLE, THERMO)                                          \
     k_force_lj<SUB, PIPE, TABLE, THERMO>                                                     \
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                       \
@@ -990,8 +1151,10 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
         else B2MD_DISPATCH_TT(1, 2);
     } else if (sub == 2) {
         B2MD_DISPATCH_TT(2, 0);
-    } else {
+    } else if (sub == 4) {
         B2MD_DISPATCH_TT(4, 0);
+    } else {
+        B2MD_DISPATCH_TT(16, 0);
     }
 #undef B2MD_DISPATCH_TT
 #undef B2MD_LAUNCH_FORCE
@@ -1174,16 +1337,110 @@ B2MD_EXPORT int b2md_force_lj_advance(
         <<<blocks_for(n, kForceThreads / SUB), kForceThreads, 0, s>>>(                        \
             (const float4 *)d_pos_hi, n, a, d_nbr, d_counts, pitch, d_boundary, nullptr,      \
             nullptr, d_status, gated, adv)
-    if (n < 200000) {
-        if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(4, 0, false);
-        else B2MD_LAUNCH_ROW_ADVANCE(4, 0, true);
-    } else {
-        if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(1, 2, false);
-        else B2MD_LAUNCH_ROW_ADVANCE(1, 2, true);
+    switch (lanes_for(n, stride)) {
+        case 16:
+            if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(16, 0, false);
+            else B2MD_LAUNCH_ROW_ADVANCE(16, 0, true);
+            break;
+        case 4:
+            if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(4, 0, false);
+            else B2MD_LAUNCH_ROW_ADVANCE(4, 0, true);
+            break;
+        case 2:
+            if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(2, 0, false);
+            else B2MD_LAUNCH_ROW_ADVANCE(2, 0, true);
+            break;
+        default:
+            if (ntypes == 1) B2MD_LAUNCH_ROW_ADVANCE(1, 2, false);
+            else B2MD_LAUNCH_ROW_ADVANCE(1, 2, true);
     }
 #undef B2MD_LAUNCH_ROW_ADVANCE
     B2MD_CHECK_LAUNCH("b2md_force_lj_advance");
     return 0;
+}
+
+namespace {
+
+template <bool TABLE>
+const void *persistent_kernel(int sub) {
+    switch (sub) {
+        case 16: return (const void *)k_steps_persistent<16, TABLE>;
+        case 4: return (const void *)k_steps_persistent<4, TABLE>;
+        case 2: return (const void *)k_steps_persistent<2, TABLE>;
+        default: return (const void *)k_steps_persistent<1, TABLE>;
+    }
+}
+
+// Lanes per particle of the persistent kernel for n particles and `rows` allocated list rows
+// (lanes_for), 0 when that grid is not co-resident on the current device.
+template <bool TABLE>
+int persistent_lanes(int64_t n, int32_t rows, int *blocks_out) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return 0;
+    // the lanes every row kernel uses for this system (bit-identical sums), provided the
+    // grid really is co-resident on this device
+    const int sub = lanes_for(n, rows);
+    int per_sm = 0;
+    const void *fn = persistent_kernel<TABLE>(sub);
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kForceThreads, 0);
+    if (err != cudaSuccess) { cudaGetLastError(); return 0; }
+    const int64_t blocks = (n + kForceThreads / sub - 1) / (kForceThreads / sub);
+    if (blocks > (int64_t)per_sm * sms) return 0;
+    *blocks_out = (int)blocks;
+    return sub;
+}
+
+}  // namespace
+
+B2MD_EXPORT int b2md_steps_persistent_lanes(int64_t n, int32_t stride, int32_t ntypes) {
+    int blocks = 0;
+    if (n <= 0 || stride < 1) return 0;
+    return ntypes == 1 ? persistent_lanes<false>(n, stride, &blocks)
+                       : persistent_lanes<true>(n, stride, &blocks);
+}
+
+B2MD_EXPORT int b2md_steps_persistent(
+    void *d_pos_a, void *d_pos_b, void *d_pos_lo, void *d_vel, void *d_image_i4, int64_t n,
+    const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2, const int32_t *d_nbr,
+    const int32_t *d_counts, int64_t pitch, int32_t stride, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t gate_a_word, int32_t gate_b_word,
+    int32_t n_steps, uint32_t *d_barrier, b2md_status *d_status, void *stream) {
+    if (n <= 0 || !d_nbr || !d_counts || !d_status || !d_barrier || stride < 1 || n_steps < 1 ||
+        !d_pos_a || !d_pos_b || d_pos_a == d_pos_b) {
+        set_error("b2md_steps_persistent: bad arguments");
+        return -1;
+    }
+    AdvanceArgs adv;
+    int rc = fill_advance(adv, d_pos_a, d_pos_b, d_pos_lo, d_vel, d_image_i4, box, dt, d_ref_pos_f4,
+                          half_skin2, gate_a_word, gate_b_word, "b2md_steps_persistent");
+    if (rc) return rc;
+    ForceArgs a;
+    if ((rc = fill_args(a, box, table, ntypes))) return rc;
+    int blocks = 0;
+    const int sub = ntypes == 1 ? persistent_lanes<false>(n, stride, &blocks)
+                                : persistent_lanes<true>(n, stride, &blocks);
+    if (sub == 0) {
+        set_error("b2md_steps_persistent: the grid for %lld particles is not co-resident (or the "
+                  "list rows are not a multiple of 16 entries per lane group)", (long long)n);
+        return -6;
+    }
+    PersistArgs ps;
+    ps.pos[0] = (float4 *)d_pos_a;
+    ps.pos[1] = (float4 *)d_pos_b;
+    ps.gate[0] = gate_a_word;
+    ps.gate[1] = gate_b_word;
+    ps.n_steps = n_steps;
+    ps.barrier = d_barrier;
+    cudaStream_t s = as_stream(stream);
+    if ((rc = check_cuda(cudaMemsetAsync(d_barrier, 0, sizeof(uint32_t), s), "barrier reset")))
+        return rc;
+    void *args[] = {(void *)&n, (void *)&a, (void *)&d_nbr, (void *)&d_counts, (void *)&pitch,
+                    (void *)&d_boundary, (void *)&d_status, (void *)&adv, (void *)&ps};
+    const void *fn = ntypes == 1 ? persistent_kernel<false>(sub) : persistent_kernel<true>(sub);
+    return check_cuda(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kForceThreads), args, 0, s),
+                      "b2md_steps_persistent");
 }
 
 B2MD_EXPORT int b2md_force_lj_pairs_advance(

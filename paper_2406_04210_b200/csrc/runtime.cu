@@ -84,7 +84,10 @@ Set buffer_set(const b2md_runner *r, int k) {
 Set live(const b2md_runner *r) { return buffer_set(r, r->current); }
 Set spare(const b2md_runner *r) { return buffer_set(r, 1 - r->current); }
 
-int stride_rows(const b2md_runner *r) { return (r->cfg.stride + 15) / 16 * 16; }
+int stride_rows(const b2md_runner *r) {
+    const int m = r->cfg.list_row_multiple > 0 ? r->cfg.list_row_multiple : 16;
+    return (r->cfg.stride + m - 1) / m * m;
+}
 
 __global__ void k_graph_gate(cudaGraphConditionalHandle handle, const b2md_status *status) {
     const bool go = !status->frozen && status->rebuild_flag != 0;
@@ -613,6 +616,76 @@ int advance_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_inter, int64_t
     return 0;
 }
 
+bool can_persist(const b2md_runner *r) {
+    const b2md_runner_config &c = r->cfg;
+    return c.persistent_steps > 0 && c.pair_rows == 0 && c.barrier != nullptr && can_advance(r);
+}
+
+// Up to `n_inter` intermediate steps in ONE cooperative launch (b2md_steps_persistent): the
+// device loops over the steps behind grid barriers, stops before a step whose positions need
+// a new list and counts the steps it took.  Requires r->ahead.  *stop = 1 on overflow /
+// singular.  A launch that cannot be made (grid not co-resident) switches the mode off.
+int persistent_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_inter, int64_t before,
+                     int *stop) {
+    b2md_runner_config &c = r->cfg;
+    int rc;
+    *stop = 0;
+    const int m = (int)(n_inter < c.persistent_steps ? n_inter : c.persistent_steps);
+    Set a = live(r);
+    void *in = r->pos_cur ? r->pos_cur : a.pos_hi;
+    void *other = in == a.pos_hi ? c.pos_hi_alt : a.pos_hi;
+    const int gate_other = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+    rc = b2md_steps_persistent(in, other, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt, c.ref_pos,
+                               r->half_skin2, c.nbr, c.counts, c.pitch, stride_rows(r), c.boundary,
+                               r->table.data(), c.ntypes, r->gate_in, gate_other, m, c.barrier,
+                               c.status, r->stream);
+    if (rc == -6) {                      // not co-resident on this device: per-step launches
+        c.persistent_steps = 0;
+        return 0;
+    }
+    if (rc) return rc;
+    r->launches += 1;
+    if ((rc = read_status(r))) return rc;
+    if (r->h_status->frozen) {
+        set_error("b2md_runner_run: a grid barrier of the persistent step kernel timed out");
+        return -7;
+    }
+    const int32_t *words = reinterpret_cast<const int32_t *>(r->h_status);
+    int ran = words[kWordAdvanceCount] - r->count_seen;
+    if (ran < 0) ran = 0;
+    if (ran > m) ran = m;
+    r->count_seen += ran;
+    for (int q = 0; q < ran; ++q) toggle_advance_state(r);
+    rep->steps_done += ran;
+    rep->max_disp2 = (double)__builtin_bit_cast(float, r->h_status->max_disp2_bits);
+    r->last_disp2 = rep->max_disp2;
+    if (r->h_status->singular != ~0ull) {
+        if ((rc = canonicalize(r))) return rc;
+        if ((rc = read_status(r))) return rc;
+        rep->singular = r->h_status->singular;
+        rep->reason = B2MD_RUN_SINGULAR;
+        finish_report(r, rep, before);
+        *stop = 1;
+        return 0;
+    }
+    if (ran < m) {
+        // the positions reached after `ran` steps need a new list
+        if ((rc = canonicalize(r))) return rc;
+        if ((rc = rebuild(r, rep))) return rc;
+        r->gate_in = kWordRebuildFlag;
+        r->last_disp2 = 0.0;
+        if (!r->list_valid) {
+            r->mid_step = true;
+            r->ahead = false;
+            rep->reason = B2MD_RUN_OVERFLOW;
+            finish_report(r, rep, before);
+            *stop = 1;
+            return 0;
+        }
+    }
+    return 0;
+}
+
 // A batch of graphed steps.  *stop = 1 on overflow / singular.
 int graph_batch(b2md_runner *r, b2md_run_report *rep, int64_t n_batch, int64_t before, int *stop) {
     const b2md_runner_config &c = r->cfg;
@@ -877,6 +950,8 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
         // graphed steps need the fused kick and must not be the observable last step
         if (c.use_graph && r->pending_kick && left > 1) {
             if ((rc = graph_batch(r, rep, left - 1, before, &stop))) return rc;
+        } else if (r->ahead && left > 1 && can_persist(r)) {
+            if ((rc = persistent_batch(r, rep, left - 1, before, &stop))) return rc;
         } else if (c.queue_depth > 1 && r->ahead && left > 1 && can_advance(r)) {
             if ((rc = advance_batch(r, rep, left - 1, before, &stop))) return rc;
         } else {

@@ -230,7 +230,8 @@ def build_neighbor_list(state: ParticleState, grid: CellGrid, r_list: float, str
     dev = state.device_state()
     n = dev.n
     pitch = _round_up(n, 32)
-    rows = _round_up(stride, 16)
+    # small systems: 64-row granules, so that the row kernels may put 16 lanes on a particle
+    rows = _round_up(stride, 64 if n < 200_000 else 16)
     reuse = (_recycle and prev is not None and not prev._consumed and
              prev.d_nbr.shape == (rows, pitch) and prev._dev is dev)
     if reuse:

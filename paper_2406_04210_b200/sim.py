@@ -51,6 +51,9 @@ STRIDE_GROWTH_LIMIT = 10
 #: below this size the thread-per-particle kernel also advances the particles it has
 #: evaluated (one launch per step); from PAIR_ROWS_MIN_PARTICLES up the pair kernel does
 ADVANCE_ROWS_MAX_PARTICLES = 60_000
+#: ... and up to this size (148 SMs x 1024 resident threads, one lane per particle) the
+#: intermediate steps run in batches inside one cooperative launch (b2md_steps_persistent)
+PERSISTENT_MAX_PARTICLES = 148 * 1024
 
 _REORDER_MODES = {None: 0, "none": 0, "hilbert": 1, "cell": 2}
 
@@ -69,7 +72,7 @@ class Simulation:
                  reorder_every: int = 1, native: bool | None = None,
                  stride_policy: str = "fit", graph: int | bool = False,
                  pair_rows: bool | None = None, advance: bool | None = None,
-                 queue_depth: int | None = None):
+                 queue_depth: int | None = None, persistent_steps: int | None = None):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -103,12 +106,16 @@ class Simulation:
         if advance is None:
             env = os.environ.get("B2MD_ADVANCE")
             advance = (env != "0") if env in ("0", "1") else \
-                (self.pair_rows or state.n < ADVANCE_ROWS_MAX_PARTICLES)
+                (self.pair_rows or state.n < PERSISTENT_MAX_PARTICLES)
         self.advance = bool(advance) and not thermostatted
         # one-launch steps queued per status read-back (small systems: a step is shorter
         # than a host round trip)
         self.queue_depth = int(os.environ.get("B2MD_QUEUE_DEPTH", "1")) if queue_depth is None \
             else int(queue_depth)
+        # systems without pair rows: MD steps per launch of the persistent step kernel
+        # (b2md_steps_persistent; 0 = one gated launch per step).  Bit-identical trajectories.
+        self.persistent_steps = int(os.environ.get("B2MD_PERSISTENT_STEPS", "256")) \
+            if persistent_steps is None else int(persistent_steps)
         self.graph_steps = 0
         # (a thermostatted native loop launches integrate / force / finalize / thermostat
         # separately: the thermostat is the reference's second finalize slot, sim.py:86-87)
@@ -232,14 +239,19 @@ class Simulation:
     def _alloc_list(self, dev: DeviceState):
         torch = _torch()
         pitch = _round_up(dev.n, 32)
-        rows = _round_up(self._stride, 16)
+        # (64-row granules let the persistent step kernel of small systems put 16 lanes on a
+        # particle: a trip of it reads 4 x 16 entries of a row)
+        rows = _round_up(self._stride, self._row_multiple())
         # zero-filled: padding entries must stay valid row indices
         return torch.zeros((rows, pitch), dtype=torch.int32, device=dev.device), pitch
+
+    def _row_multiple(self) -> int:
+        return 64 if self.state.n < 200_000 else 16
 
     def _alloc_pair_list(self, dev: DeviceState):
         """Pair-row buffer: 2 * rows entries per pair, so a merge never overflows."""
         torch = _torch()
-        rows = _round_up(self._stride, 16)
+        rows = _round_up(self._stride, self._row_multiple())
         pair_pitch = _round_up((dev.n + 1) // 2, 32)
         return (torch.zeros((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
                             device=dev.device), pair_pitch, 2 * rows)
@@ -310,6 +322,12 @@ class Simulation:
             k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
             cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
             cfg.queue_depth = max(self.queue_depth, 1)
+        cfg.list_row_multiple = self._row_multiple()
+        if self.advance and not self.graph and not self.pair_rows and self.persistent_steps > 0:
+            # small systems: intermediate steps in batches inside one cooperative launch
+            k["barrier"] = torch.zeros(4, dtype=torch.int32, **d)
+            cfg.barrier = k["barrier"].data_ptr()
+            cfg.persistent_steps = self.persistent_steps
         if self.pair_rows:
             k["pair_nbr"], cfg.pair_pitch, cfg.pair_rows = self._alloc_pair_list(dev)
             # pair counts, then the block schedule of the pair kernel (b2md_pair_schedule)

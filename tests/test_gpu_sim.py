@@ -137,8 +137,34 @@ def test_nve_energy_conservation_n4096():
     assert 15 <= sim.rebuild_count <= 40      # reference: 24 per 1000 steps
     p = np.array(sim.samples[-1].total_momentum)
     assert np.max(np.abs(p)) <= 1e-2
-    assert sim.kernel_launches >= 1000      # >= one launch per step (two without pair rows)
+    # small systems run their intermediate steps in batches inside ONE cooperative launch
+    # (b2md_steps_persistent): far fewer launches than steps
+    assert sim.persistent_steps > 0 and 100 <= sim.kernel_launches < 1000
     sim.close()
+
+
+def test_persistent_step_kernel_is_bit_identical_to_one_launch_per_step():
+    """b2md_steps_persistent (up to 256 MD steps per cooperative launch, grid barriers between
+    them, 16 / 4 / 2 / 1 lanes per particle by size) against the gated one-launch steps and the
+    separate integrate / force launches: same trajectories, energies, image counters and rebuild
+    schedule bit for bit, for every lane count, across rebuilds and sample steps."""
+    for n in (2048, 20_000, 50_000):
+        out = []
+        for kw in (dict(persistent_steps=0, advance=False), dict(persistent_steps=0, advance=True),
+                   dict(persistent_steps=256), dict(persistent_steps=7)):
+            sim = lattice_sim(n, True, every=37, dt=0.002, **kw)
+            sim.run(150)
+            sim.run(63)
+            out.append((series(sim), np.array(sim.state.positions.acquire_read(b2.HOST)),
+                        np.array(sim.state.velocities.acquire_read(b2.HOST)),
+                        np.array(sim.state.images.acquire_read(b2.HOST)), sim.rebuild_count,
+                        sim.kernel_launches))
+            sim.close()
+        for other in out[1:]:
+            for a, b in zip(out[0][:5], other[:5]):
+                assert np.array_equal(a, b), n
+        assert out[0][4] >= 3
+        assert out[2][5] < out[1][5] < out[0][5]          # launches: batches < one per step < two
 
 
 def test_stride_growth_recovers_from_overflow():
