@@ -209,13 +209,14 @@ int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
  * other buffer; gate_a_word / gate_b_word are the status words holding the rebuild flag of
  * the positions in d_pos_a / d_pos_b.  The loop stops before a step whose input positions
  * need a new list; every completed step adds one to status word 13 (the advance counter), so
- * the caller learns how many steps ran and which buffer is live.  d_barrier: 4 bytes of
- * device scratch.  stride (allocated rows of the list) must be a multiple of 16 entries per
+ * the caller learns how many steps ran and which buffer is live.  d_barrier:
+ * B2MD_BARRIER_BYTES of device scratch, 128-byte aligned.  stride (allocated rows of the list) must be a multiple of 16 entries per
  * lane group: b2md_steps_persistent_lanes(n, stride, ntypes) returns the lanes per particle
  * the launch would use on the current device (16 or 4), 0 when the grid cannot be
  * co-resident -- b2md_steps_persistent then fails with -6 and launches nothing.
  * status->frozen != 0 afterwards: a barrier timed out (never expected; the launch is
  * cooperative) and the loop was abandoned. */
+#define B2MD_BARRIER_BYTES 4096
 int b2md_steps_persistent_lanes(int64_t n, int32_t stride, int32_t ntypes);
 int b2md_steps_persistent(void *d_pos_a, void *d_pos_b, void *d_pos_lo, void *d_vel,
                           void *d_image_i4, int64_t n, const b2md_box *box, double dt,
@@ -505,7 +506,7 @@ typedef struct b2md_runner_config {
                                     list_row_multiple = 64); 0: one launch per step */
     int32_t list_row_multiple;   /* nbr holds round_up(stride, this) rows; 0 = 16 (64 lets the
                                     persistent kernel use 16 lanes per particle) */
-    uint32_t *barrier;           /* 4 bytes of device scratch (persistent_steps > 0) */
+    uint32_t *barrier;           /* B2MD_BARRIER_BYTES of device scratch, 128-byte aligned */
     /* Optional caller-owned resources (NULL = the runner creates and destroys its own).
      * Page-locking memory and creating streams are the expensive parts of creating a
      * runner (1-7 ms measured on B200); a caller that builds many short-lived simulations

@@ -234,21 +234,38 @@ __device__ __forceinline__ void compute4(RowAcc &acc, const float4 pi, int cnt, 
 // PIPE = true additionally keeps the NEXT trip's four position gathers in flight
 // while the current trip is being computed (deeper memory-level parallelism at
 // the price of 16 more registers).
-template <int SUB, int PIPEK, int AXES, bool TABLE, bool THERMO, bool NC = true>
+// The index entries of the first two trips of a row (what row_loop loads before its loop):
+// the persistent kernel loads them once per launch instead of once per step.
+template <int SUB>
+__device__ __forceinline__ void row_first_indices(int (&ja)[4], int (&jb)[4], int kmax,
+                                                  const int32_t *__restrict__ col, int64_t pitch) {
+    constexpr int kTrip = 4 * SUB;
+    const int64_t step = (int64_t)SUB * pitch;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        ja[u] = (0 < kmax) ? __ldcs(col + u * step) : 0;
+        jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
+    }
+}
+
+template <int SUB, int PIPEK, int AXES, bool TABLE, bool THERMO, bool NC = true,
+          bool PRELOADED = false>
 __device__ __forceinline__ void row_loop(RowAcc &acc, const float4 pi, int cnt, int k0, int kmin,
                                          int kmax, const int32_t *__restrict__ col,
                                          int64_t pitch, const float4 *pos,
                                          const ForceArgs &a,
                                          const float4 *s_tab_a, const float2 *s_tab_b,
-                                         int ti_row) {
+                                         int ti_row, const int *ja0 = nullptr,
+                                         const int *jb0 = nullptr) {
     constexpr bool PIPE = (PIPEK == 1);
     constexpr int kTrip = 4 * SUB;            // entries of one particle consumed per trip
     const int64_t step = (int64_t)SUB * pitch;
     int ja[4], jb[4];
+    if (PRELOADED) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        ja[u] = (0 < kmax) ? __ldcs(col + u * step) : 0;
-        jb[u] = (kTrip < kmax) ? __ldcs(col + (4 + u) * step) : 0;
+        for (int u = 0; u < 4; ++u) { ja[u] = ja0[u]; jb[u] = jb0[u]; }
+    } else {
+        row_first_indices<SUB>(ja, jb, kmax, col, pitch);
     }
     float4 pa[4], pb[4];
     if (PIPE) gather4<NC>(pa, ja, pos);
@@ -454,42 +471,60 @@ struct PersistArgs {
     float4 *pos[2];           // step s reads pos[s & 1], writes pos[(s & 1) ^ 1]
     int gate[2];              // status word holding the rebuild flag of pos[0] / pos[1]
     int n_steps;
-    unsigned *barrier;        // zeroed by the host before the launch
-};
+    unsigned long long *barrier;   // B2MD_BARRIER_BYTES, zeroed before the launch: per counter,
+};                                 // arrivals in the low word, flagged arrivals in the high word
 
 constexpr long long kBarrierTimeout = 4000000000ll;      // ~2 s at 1.97 GHz
+#ifndef B2MD_PERSIST_THREADS
+#define B2MD_PERSIST_THREADS 256
+#endif
+// threads per block of the persistent kernel: the grid barrier costs one atomic and one
+// polling thread per BLOCK, so fewer, larger blocks make it cheaper (128 ... 512 measured
+// within 10 % of each other, 1024 slower)
+constexpr int kPersistThreads = B2MD_PERSIST_THREADS;
 
-__device__ __forceinline__ bool grid_barrier(unsigned *counter, unsigned target, b2md_status *status) {
-    __shared__ int s_ok;
+// Grid-wide barrier; thread 0 of every block arrives with `flagged` (this block saw a
+// displacement beyond the threshold).  Returns -1 if the barrier timed out, else how many
+// arrivals carried a flag so far -- the rebuild decision travels with the barrier, no second
+// round trip.  The counter only grows: step s waits for (s + 1) x gridDim.x arrivals.  (A
+// two-level version -- 16 group counters on their own cache lines, last arrival of a group
+// arrives on the top counter -- was measured slower, 10.3 against 9.4 us per step at N = 4096:
+// the extra dependent atomic costs more than 256 same-address atomics.)
+__device__ __forceinline__ int grid_barrier(unsigned long long *counter, unsigned step,
+                                            bool flagged, b2md_status *status) {
+    __shared__ int s_flags;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();                                   // release: my block's stores
-        atomicAdd(counter, 1u);
+        atomicAdd(counter, 1ull | (flagged ? (1ull << 32) : 0ull));
+        const unsigned target = gridDim.x * (step + 1u);
         const long long t0 = clock64();
-        int ok = 1;
-        while (*(volatile unsigned *)counter < target) {
+        unsigned long long v;
+        int out = 0;
+        while ((unsigned)(v = *(volatile unsigned long long *)counter) < target) {
             if (clock64() - t0 > kBarrierTimeout || *(volatile int *)&status->frozen) {
                 status->frozen = 1;
-                ok = 0;
+                out = -1;
                 break;
             }
         }
+        if (out == 0) out = (int)(v >> 32);
         __threadfence();                                   // acquire: everybody else's stores
-        s_ok = ok;
+        s_flags = out;
     }
     __syncthreads();
-    return s_ok != 0;
+    return s_flags;
 }
 
 template <int SUB, bool TABLE>
-__global__ void __launch_bounds__(kForceThreads, 8)
+__global__ void __launch_bounds__(kPersistThreads, 1024 / kPersistThreads)
 k_steps_persistent(int64_t n, const __grid_constant__ ForceArgs a,
                    const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
                    int64_t pitch, const uint8_t *__restrict__ boundary, b2md_status *status,
                    const __grid_constant__ AdvanceArgs adv, const __grid_constant__ PersistArgs ps) {
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
-    __shared__ float s_max[kForceThreads / 32];
+    __shared__ float s_max[kPersistThreads / 32];
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
@@ -497,30 +532,47 @@ k_steps_persistent(int64_t n, const __grid_constant__ ForceArgs a,
         }
         __syncthreads();
     }
-    constexpr int kPerBlock = kForceThreads / SUB;
+    // grid-uniform: the flag of the initial positions was written by an earlier launch
+    if (((volatile int *)status)[ps.gate[0]]) return;
+    constexpr int kPerBlock = kPersistThreads / SUB;
     const int sub = threadIdx.x % SUB;
     const int64_t i_raw = blockIdx.x * (int64_t)kPerBlock + threadIdx.x / SUB;
     const bool active = i_raw < n;
     const int64_t i = active ? i_raw : n - 1;
-    // the list does not change during the launch
+    const bool owner = active && sub == 0;
+    // what does not change during the launch stays in registers: the list (row length, the
+    // index entries of the first two trips), and -- in the particle's owner lane -- the state
+    // no other thread touches: low words, velocity, snapshot, the high words just written
     const int cnt = active ? counts[i] : 0;
     const int kmax = __reduce_max_sync(0xffffffffu, cnt);
     const int kmin = __reduce_min_sync(0xffffffffu, active ? cnt : 0x7fffffff);
     const int axes = boundary ? (__reduce_or_sync(0xffffffffu, active ? (int)boundary[i] : 0) & 7) : 7;
     const int32_t *col = nbr + (int64_t)sub * pitch + i;
-    const int ti_row = TABLE ? __float_as_int(ld_coherent_f4(ps.pos[0] + i).w) * a.ntypes : 0;
+    int ja0[4], jb0[4];
+    row_first_indices<SUB>(ja0, jb0, kmax, col, pitch);
+    float4 h = ld_coherent_f4(ps.pos[0] + i);
+    float4 l = owner ? adv.pos_lo[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 v = owner ? adv.vel[i] : make_float4(0.f, 0.f, 0.f, 1.f);
+    float4 r = owner ? adv.ref_pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int ti_row = TABLE ? __float_as_int(h.w) * a.ntypes : 0;
 
-    for (int s = 0; s < ps.n_steps; ++s) {
-        const int w_in = ps.gate[s & 1], w_out = ps.gate[(s & 1) ^ 1];
-        // grid-uniform: written before the previous barrier (or by an earlier launch)
-        if (((volatile int *)status)[w_in]) break;
+    int s = 0;
+    for (; s < ps.n_steps; ++s) {
+        const int w_out = ps.gate[(s & 1) ^ 1];
         const float4 *pos = ps.pos[s & 1];
         float4 *pos_out = ps.pos[(s & 1) ^ 1];
-        const float4 pi = ld_coherent_f4(pos + i);
+        // the particle's own position: from its owner lane
+        float4 pi = h;
+        if (SUB > 1) {
+            const int src = (threadIdx.x & 31) & ~(SUB - 1);
+            pi.x = __shfl_sync(0xffffffffu, h.x, src);
+            pi.y = __shfl_sync(0xffffffffu, h.y, src);
+            pi.z = __shfl_sync(0xffffffffu, h.z, src);
+        }
         RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
-#define B2MD_ROW_LOOP(AXES)                                                                 \
-    row_loop<SUB, 0, AXES, TABLE, false, false>(acc, pi, cnt, sub, kmin, kmax, col, pitch, pos, \
-                                                a, s_tab_a, s_tab_b, ti_row)
+#define B2MD_ROW_LOOP(AXES)                                                                     \
+    row_loop<SUB, 0, AXES, TABLE, false, false, true>(acc, pi, cnt, sub, kmin, kmax, col, pitch, \
+                                                      pos, a, s_tab_a, s_tab_b, ti_row, ja0, jb0)
         switch (axes) {                 // warp-uniform
             case 0: B2MD_ROW_LOOP(0); break;
             case 1: B2MD_ROW_LOOP(1); break;
@@ -536,7 +588,7 @@ k_steps_persistent(int64_t n, const __grid_constant__ ForceArgs a,
             acc.fz += __shfl_xor_sync(0xffffffffu, acc.fz, o);
         }
         float d2 = 0.0f;
-        if (active && sub == 0) {
+        if (owner) {
             float fx, fy, fz;
             if (TABLE) {
                 fx = acc.fx; fy = acc.fy; fz = acc.fz;
@@ -544,27 +596,37 @@ k_steps_persistent(int64_t n, const __grid_constant__ ForceArgs a,
                 const PairParams &p = a.single;
                 fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
             }
-            float4 h = pi;
-            d2 = advance_particle<2>(i, h, make_float4(fx, fy, fz, 0.0f), adv.pos_lo, adv.vel,
-                                     adv.image, adv.step, adv.ref_pos);
+            const float4 before = h;
+            d2 = advance_regs<2>(i, h, l, v, r, true, make_float4(fx, fy, fz, 0.0f), adv.image,
+                                 adv.step);
             pos_out[i] = h;
             if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-                report_singular((int)i, pi, cnt, nbr + i, pitch, pos, a.box, status);
+                report_singular((int)i, before, cnt, nbr + i, pitch, pos, a.box, status);
         }
         // displacement maximum of the block -> status; the flag of the new positions
         d2 = warp_max(d2);
         if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
         __syncthreads();
+        bool flagged = false;
         if (threadIdx.x < 32) {
-            float m = threadIdx.x < kForceThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+            float m = threadIdx.x < kPersistThreads / 32 ? s_max[threadIdx.x] : 0.0f;
             m = warp_max(m);
             if (threadIdx.x == 0 && m > 0.0f) {
                 atomicMax(&status->max_disp2_bits, __float_as_uint(m));
-                if (m > adv.step.half_skin2) ((int *)status)[w_out] = 1;
+                if (m > adv.step.half_skin2) {
+                    ((int *)status)[w_out] = 1;
+                    flagged = true;
+                }
             }
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&((int *)status)[kWordAdvanceCount], 1);
-        if (!grid_barrier(ps.barrier, gridDim.x * (unsigned)(s + 1), status)) break;
+        const int flags = grid_barrier(ps.barrier, (unsigned)s, flagged, status);
+        if (flags != 0) break;           // the new positions need a list (or the barrier failed)
+    }
+    if (owner) {                         // the state this launch kept in registers
+        adv.pos_lo[i] = l;
+        adv.vel[i] = v;
+        adv.ref_pos[i] = r;
     }
 }
 
@@ -749,6 +811,9 @@ __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, 
 #ifndef B2MD_PAIR_TILE_ROTATE
 #define B2MD_PAIR_TILE_ROTATE 0
 #endif
+#ifndef B2MD_PAIR_HALF_TILE
+#define B2MD_PAIR_HALF_TILE 0
+#endif
 
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
@@ -784,6 +849,25 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
         // loop that runs at the register cap); the rotation happens at the bottom
         const int ev[4] = {e0.x, e0.y, e0.z, e0.w};
 #endif
+#if B2MD_PAIR_HALF_TILE
+        // two gathers in flight at a time (eight registers less in a loop at the register cap)
+#pragma unroll
+        for (int h = 0; h < 4; h += 2) {
+            float4 pj[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) pj[u] = __ldg(pos + ((unsigned)ev[h + u] >> 2));
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (TABLE)
+                    pair_entry_packed_table<AXES, THERMO>(acc, ax, ay, az, cx, cy, cz, ev[h + u],
+                                                          pj[u], a, s_tab_a, s_tab_b, ta_row,
+                                                          tb_row);
+                else
+                    pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, cx, cy, cz, ev[h + u],
+                                                          pj[u], a);
+            }
+        }
+#else
         float4 pj[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) pj[u] = __ldg(pos + ((unsigned)ev[u] >> 2));
@@ -796,6 +880,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
                 pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, cx, cy, cz, ev[u], pj[u],
                                                       a);
         }
+#endif
 #if B2MD_PAIR_TILE_ROTATE != 0
         e0 = e1;
         if (q + 2 < tiles) e1 = __ldcs(col);            // warp-uniform; a stale e1 is never used
@@ -1014,21 +1099,38 @@ k_pair_schedule(const int32_t *__restrict__ flags, int n_blocks, int32_t *__rest
     }
 }
 
-// ---- all pairs, shared-memory tiles of 128 positions ------------------------
+// ---- all pairs (reference _all_to_all_chunk, forces.py:29-69) --------------------
+// The paper's primary benchmark is N = 2000: one thread per particle is 16 blocks on 148 SMs.
+// A thread-block CLUSTER of kAllPairsSplit blocks therefore shares one block of 128 particles
+// i: block r of the cluster walks the j tiles r, r + S, r + 2S, ... (positions staged through
+// shared memory, 128 at a time), and the partial sums of the S blocks are combined through
+// distributed shared memory by block 0 of the cluster in the fixed order r = 0 .. S-1 -- no
+// atomics, no scratch buffer, bitwise reproducible.
+constexpr int kAllPairsSplit = 8;           // portable cluster size
+
+struct AllPairsPartial {
+    float fx, fy, fz, u, w;
+    int cnt;
+    long long first_bad;
+};
+
 template <bool TABLE>
-__global__ void __launch_bounds__(kForceThreads)
+__global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(kForceThreads)
 k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                   float4 *__restrict__ force, float *__restrict__ virial, b2md_status *status) {
     __shared__ float4 tile[kForceThreads];
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ AllPairsPartial s_part[kForceThreads];
     if (TABLE) {
         for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
             s_tab_a[t] = a.tab_a[t];
             s_tab_b[t] = a.tab_b[t];
         }
     }
-    const int64_t i_raw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned rank;                                   // block rank inside the cluster
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int64_t i_raw = (blockIdx.x / kAllPairsSplit) * (int64_t)blockDim.x + threadIdx.x;
     const bool active = i_raw < n;
     const int64_t i = active ? i_raw : n - 1;
     const float4 pi = pos[i];
@@ -1036,7 +1138,8 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
     const BoxF &b = a.box;
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     long long first_bad = -1;
-    for (int64_t base = 0; base < n; base += kForceThreads) {
+    for (int64_t base = (int64_t)rank * kForceThreads; base < n;
+         base += (int64_t)kAllPairsSplit * kForceThreads) {
         __syncthreads();
         const int64_t jl = base + threadIdx.x;
         tile[threadIdx.x] = pos[jl < n ? jl : n - 1];
@@ -1060,21 +1163,49 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
             }
         }
     }
-    if (!active) return;
-    float fx, fy, fz, u, w;
-    if (TABLE) {
-        fx = acc.fx; fy = acc.fy; fz = acc.fz; u = acc.u; w = acc.w;
-    } else {
-        const PairParams &p = a.single;
-        fx = p.c_f * acc.fx; fy = p.c_f * acc.fy; fz = p.c_f * acc.fz;
-        u = fmaf(p.c_u, acc.u, p.half_shift * (float)acc.cnt);
-        w = p.c_w * acc.w;
+    AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, first_bad};
+    s_part[threadIdx.x] = mine;
+    // cluster barrier (release / acquire): every block's partial sums are in its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank == 0 && active) {
+        RowAcc sum = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+        long long bad = -1;
+        const unsigned local = (unsigned)__cvta_generic_to_shared(&s_part[threadIdx.x]);
+#pragma unroll
+        for (unsigned r = 0; r < (unsigned)kAllPairsSplit; ++r) {      // fixed order
+            unsigned remote;
+            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+            float fx, fy, fz, u, w;
+            int cnt;
+            long long fb;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(fx) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+4];" : "=f"(fy) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+8];" : "=f"(fz) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+12];" : "=f"(u) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+16];" : "=f"(w) : "r"(remote));
+            asm volatile("ld.shared::cluster.s32 %0, [%1+20];" : "=r"(cnt) : "r"(remote));
+            asm volatile("ld.shared::cluster.s64 %0, [%1+24];" : "=l"(fb) : "r"(remote));
+            sum.fx += fx; sum.fy += fy; sum.fz += fz; sum.u += u; sum.w += w; sum.cnt += cnt;
+            // tiles are dealt round-robin: the smallest index over all blocks is the first j
+            if (fb >= 0 && (bad < 0 || fb < bad)) bad = fb;
+        }
+        float fx, fy, fz, u, w;
+        if (TABLE) {
+            fx = sum.fx; fy = sum.fy; fz = sum.fz; u = sum.u; w = sum.w;
+        } else {
+            const PairParams &p = a.single;
+            fx = p.c_f * sum.fx; fy = p.c_f * sum.fy; fz = p.c_f * sum.fz;
+            u = fmaf(p.c_u, sum.u, p.half_shift * (float)sum.cnt);
+            w = p.c_w * sum.w;
+        }
+        force[i] = make_float4(fx, fy, fz, u);
+        if (virial) virial[i] = w;
+        if (bad >= 0)
+            atomicMin((unsigned long long *)&status->singular,
+                      ((unsigned long long)(unsigned)i << 32) | (unsigned)bad);
     }
-    force[i] = make_float4(fx, fy, fz, u);
-    if (virial) virial[i] = w;
-    if (first_bad >= 0)
-        atomicMin((unsigned long long *)&status->singular,
-                  ((unsigned long long)(unsigned)i << 32) | (unsigned)first_bad);
+    // nobody leaves while block 0 may still read its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int ntypes) {
@@ -1169,7 +1300,7 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     ForceArgs a;
     int rc = fill_args(a, box, table, ntypes);
     if (rc) return rc;
-    const unsigned blocks = blocks_for(n, kForceThreads);
+    const unsigned blocks = blocks_for(n, kForceThreads) * kAllPairsSplit;   // clusters of 8
     cudaStream_t s = as_stream(stream);
     if (ntypes == 1)
         k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(
@@ -1384,9 +1515,9 @@ int persistent_lanes(int64_t n, int32_t rows, int *blocks_out) {
     const int sub = lanes_for(n, rows);
     int per_sm = 0;
     const void *fn = persistent_kernel<TABLE>(sub);
-    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kForceThreads, 0);
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, 0);
     if (err != cudaSuccess) { cudaGetLastError(); return 0; }
-    const int64_t blocks = (n + kForceThreads / sub - 1) / (kForceThreads / sub);
+    const int64_t blocks = (n + kPersistThreads / sub - 1) / (kPersistThreads / sub);
     if (blocks > (int64_t)per_sm * sms) return 0;
     *blocks_out = (int)blocks;
     return sub;
@@ -1432,14 +1563,14 @@ B2MD_EXPORT int b2md_steps_persistent(
     ps.gate[0] = gate_a_word;
     ps.gate[1] = gate_b_word;
     ps.n_steps = n_steps;
-    ps.barrier = d_barrier;
+    ps.barrier = reinterpret_cast<unsigned long long *>(d_barrier);
     cudaStream_t s = as_stream(stream);
-    if ((rc = check_cuda(cudaMemsetAsync(d_barrier, 0, sizeof(uint32_t), s), "barrier reset")))
+    if ((rc = check_cuda(cudaMemsetAsync(d_barrier, 0, B2MD_BARRIER_BYTES, s), "barrier reset")))
         return rc;
     void *args[] = {(void *)&n, (void *)&a, (void *)&d_nbr, (void *)&d_counts, (void *)&pitch,
                     (void *)&d_boundary, (void *)&d_status, (void *)&adv, (void *)&ps};
     const void *fn = ntypes == 1 ? persistent_kernel<false>(sub) : persistent_kernel<true>(sub);
-    return check_cuda(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kForceThreads), args, 0, s),
+    return check_cuda(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kPersistThreads), args, 0, s),
                       "b2md_steps_persistent");
 }
 

@@ -84,6 +84,42 @@ inline StepConst make_step(const b2md_box *box, double dt, double half_skin2) {
     return c;
 }
 
+// KICKS half-kicks with force f, drift, wrap, image counters, displacement from the list
+// snapshot, on a particle held in registers: h / l = position high / low words, v = velocity
+// (w = mass), r = the snapshot's high words.  Image counters are touched in memory, and only on
+// a face crossing.  Returns the squared displacement (0 when !have_ref).
+template <int KICKS>
+__device__ __forceinline__ float advance_regs(int64_t i, float4 &h, float4 &l, float4 &v, float4 &r,
+                                              bool have_ref, const float4 f,
+                                              int4 *__restrict__ image, const StepConst &c) {
+#pragma unroll
+    for (int k = 0; k < KICKS; ++k) kick(v, f, c.half_dt);
+    drift(h.x, l.x, v.x, c.dt_hi, c.dt_lo);
+    drift(h.y, l.y, v.y, c.dt_hi, c.dt_lo);
+    drift(h.z, l.z, v.z, c.dt_hi, c.dt_lo);
+    const int kx = wrap_ds(h.x, l.x, c.L_hi[0], c.L_lo[0], c.invL[0]);
+    const int ky = wrap_ds(h.y, l.y, c.L_hi[1], c.L_lo[1], c.invL[1]);
+    const int kz = wrap_ds(h.z, l.z, c.L_hi[2], c.L_lo[2], c.invL[2]);
+    const bool wrapped = (kx | ky | kz) != 0;
+    if (wrapped) {
+        int4 im = image[i];
+        im.x += kx; im.y += ky; im.z += kz;
+        image[i] = im;
+    }
+    float d2 = 0.0f;
+    if (have_ref) {
+        if (wrapped) {
+            // keep (hi - ref) equal to the unwrapped displacement
+            r.x = fmaf(-(float)kx, c.L_hi[0], r.x);
+            r.y = fmaf(-(float)ky, c.L_hi[1], r.y);
+            r.z = fmaf(-(float)kz, c.L_hi[2], r.z);
+        }
+        const float dx = h.x - r.x, dy = h.y - r.y, dz = h.z - r.z;
+        d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    }
+    return d2;
+}
+
 // KICKS half-kicks with force f, drift, wrap, image counters, displacement from the
 // list snapshot: one particle of k_integrate.  h (position high words) comes in and
 // goes out through registers; returns the squared displacement (0 without ref_pos).

@@ -55,6 +55,11 @@ struct b2md_runner {
     int steps_per_graph;
     int64_t graph_launch_kernels;   // kernels per step in the always-executed part
     int64_t graph_rebuild_kernels;  // kernels inside one conditional body
+    // The host-launched rebuild sequence (~25 small kernels) as one graph launch per live-set
+    // parity: at N <= 10^5 the sequence is launch-bound (250 us of launches for 60 us of work)
+    cudaGraphExec_t rebuild_exec[2];
+    int64_t rebuild_exec_kernels[2];
+    int rebuild_seen[2];            // host-launched rebuilds per parity (a graph pays from the 2nd on)
     // one-launch steps (b2md_force_lj_pairs_advance)
     void *pos_cur;            // where the live position high words are (canonical or alt)
     bool ahead;               // positions already advanced to the step about to be processed
@@ -281,8 +286,39 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
     int rc = check_cuda(cudaEventRecord(ev0, r->stream), "rebuild timer");
     if (rc) return rc;
     // graph mode keeps the live pointers fixed (they are baked into the step graph)
-    rc = enqueue_rebuild(r, do_reorder, c.use_graph != 0, &r->launches);
-    if (rc) return rc;
+    // (instantiating a graph costs about as much as launching the sequence once: the first
+    // rebuild of each parity is launched directly, so that short runs do not pay for it)
+    const bool as_graph = c.use_graph == 0 && (c.reorder_mode == 0 || c.reorder_every == 1) &&
+                          r->rebuild_seen[r->current]++ > 0 &&
+                          env_choice("B2MD_REBUILD_GRAPH", 1) != 0;
+    if (as_graph) {
+        // one captured sequence per parity of the live set (a reorder flips the sets, so the
+        // pointers differ); replayed with a single launch from then on
+        const int parity = r->current;
+        if (!r->rebuild_exec[parity]) {
+            cudaGraph_t graph = nullptr;
+            int64_t kernels = 0;
+            if ((rc = check_cuda(cudaStreamBeginCapture(r->stream, cudaStreamCaptureModeRelaxed),
+                                 "rebuild capture"))) return rc;
+            const int rc_enq = enqueue_rebuild(r, do_reorder, false, &kernels);
+            const int rc_end = check_cuda(cudaStreamEndCapture(r->stream, &graph), "rebuild capture end");
+            r->current = parity;                       // the capture only recorded: undo the flip
+            if (rc_enq) { if (graph) cudaGraphDestroy(graph); return rc_enq; }
+            if (rc_end) return rc_end;
+            rc = check_cuda(cudaGraphInstantiate(&r->rebuild_exec[parity], graph, 0),
+                            "rebuild graph instantiate");
+            cudaGraphDestroy(graph);
+            if (rc) return rc;
+            r->rebuild_exec_kernels[parity] = kernels;
+        }
+        if ((rc = check_cuda(cudaGraphLaunch(r->rebuild_exec[parity], r->stream), "rebuild graph")))
+            return rc;
+        r->launches += r->rebuild_exec_kernels[parity];
+        if (do_reorder) r->current = 1 - r->current;
+    } else {
+        rc = enqueue_rebuild(r, do_reorder, c.use_graph != 0, &r->launches);
+        if (rc) return rc;
+    }
     if ((rc = check_cuda(cudaEventRecord(ev1, r->stream), "rebuild timer"))) return rc;
     r->rebuild_events_used += 2;
     if (do_reorder) rep->reorders += 1;
@@ -298,6 +334,11 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
 }
 
 void destroy_graph(b2md_runner *r) {
+    for (int g = 0; g < 2; ++g) {
+        if (r->rebuild_exec[g]) cudaGraphExecDestroy(r->rebuild_exec[g]);
+        r->rebuild_exec[g] = nullptr;
+        r->rebuild_seen[g] = 0;
+    }
     for (int g = 0; g < 2; ++g) {
         if (r->graph_exec[g]) cudaGraphExecDestroy(r->graph_exec[g]);
         if (r->graph[g]) cudaGraphDestroy(r->graph[g]);
@@ -777,6 +818,9 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->last_disp2 = 0.0;
     r->graph[0] = r->graph[1] = nullptr;
     r->graph_exec[0] = r->graph_exec[1] = nullptr;
+    r->rebuild_exec[0] = r->rebuild_exec[1] = nullptr;
+    r->rebuild_exec_kernels[0] = r->rebuild_exec_kernels[1] = 0;
+    r->rebuild_seen[0] = r->rebuild_seen[1] = 0;
     r->steps_per_graph = cfg->use_graph > 1 ? cfg->use_graph : 1;
     r->pos_cur = nullptr;
     r->ahead = false;

@@ -325,7 +325,7 @@ class Simulation:
         cfg.list_row_multiple = self._row_multiple()
         if self.advance and not self.graph and not self.pair_rows and self.persistent_steps > 0:
             # small systems: intermediate steps in batches inside one cooperative launch
-            k["barrier"] = torch.zeros(4, dtype=torch.int32, **d)
+            k["barrier"] = torch.zeros(1024, dtype=torch.int32, **d)      # B2MD_BARRIER_BYTES
             cfg.barrier = k["barrier"].data_ptr()
             cfg.persistent_steps = self.persistent_steps
         if self.pair_rows:

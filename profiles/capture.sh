@@ -20,3 +20,5 @@ ncu --set full --clock-control none --import-source on -k regex:k_pair_rows -s 1
 for k in force integrate nlist pairrows; do python profiles/ncu_summary.py gpurun_out/$k.ncu-rep > gpurun_out/ncu_$k.txt 2>&1; done
 python profiles/launch_table.py gpurun_out/launches_bench.csv 30 > gpurun_out/launch_table_bench.txt 2>&1
 tail -c 2500 gpurun_out/bench.json; cat gpurun_out/bench_reference.json
+# the reports themselves exceed what gpurun copies back (64 MiB): keep the summaries
+rm -f gpurun_out/*.ncu-rep

@@ -11,3 +11,5 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
 tail -2 gpurun_out/prof_allkernels.log
 python profiles/kernel_roofline.py gpurun_out/allkernels.ncu-rep > gpurun_out/kernel_roofline.txt 2>&1
 cat gpurun_out/kernel_roofline.txt
+# the reports themselves exceed what gpurun copies back (64 MiB): keep the summaries
+rm -f gpurun_out/*.ncu-rep
