@@ -333,7 +333,7 @@ class Simulation:
             # pair counts, then the block schedule of the pair kernel (b2md_pair_schedule)
             k["pair_counts"] = torch.zeros(
                 cfg.pair_pitch + int(lib.b2md_pair_schedule_len(n)), dtype=torch.int32, **d)
-            cfg.pair_schedule = 1
+            cfg.pair_schedule = 0 if os.environ.get("B2MD_PAIR_SCHEDULE") == "0" else 1
             cfg.pair_nbr = k["pair_nbr"].data_ptr()
             cfg.pair_counts = k["pair_counts"].data_ptr()
         # page-locked status mirror and the runner's two streams come from torch's caching
