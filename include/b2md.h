@@ -158,6 +158,25 @@ int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                         uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
                         int32_t flags, b2md_status *d_status, void *stream);
 
+/* The list build of the native step loop (sim.py:131-139 -> neighbor.py:185-240) when the
+ * force kernel reads PAIR ROWS (b2md_pair_rows below): list build and pair rows in one call.
+ * With B2MD_LIST_ANY_PREFIX and a cell-contiguous particle order (after b2md_gather_rows by
+ * Hilbert / cell keys) the list kernel emits the merged rows of particles 2t, 2t+1 straight
+ * from its per-cell decision masks, and only the pairs whose two particles sit in different
+ * cells go through the plain rows and the merge -- d_nbr then holds valid rows for THOSE
+ * particles only (d_counts, d_boundary and the status words are complete).  Otherwise it is
+ * b2md_build_nlist_ex followed by b2md_pair_rows.  The pair rows are bit-identical either way.
+ * list_rows: allocated rows of d_nbr (>= stride); pair_rows >= 2 * list_rows. */
+int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                         const b2md_box *box, const b2md_grid *grid,
+                         const int32_t *d_cell_of, const int32_t *d_cell_start,
+                         const int32_t *d_cell_particles, double r_list,
+                         int32_t stride, int64_t pitch, int32_t *d_nbr, int32_t *d_counts,
+                         uint8_t *d_boundary, double boundary_margin, int64_t n_rows,
+                         int32_t flags, int32_t list_rows, int32_t *d_pair_nbr,
+                         int32_t *d_pair_counts, int64_t pair_pitch, int32_t pair_rows,
+                         b2md_status *d_status, void *stream);
+
 /* Snapshot of the unwrapped positions a list was built from
  * (neighbor.py:238, core.py:216-219): exact fp64 rows (n,3) and the fp32
  * reference copy used by the in-loop displacement check. */

@@ -120,6 +120,9 @@ _SIGNATURES = {
     "b2md_build_nlist_ex": (c_int32, [_P, _P, c_int64, POINTER(Box), POINTER(Grid), _P, _P, _P,
                                       c_double, c_int32, c_int64, _P, _P, _P, c_double, c_int64,
                                       c_int32, _P, _P]),
+    "b2md_build_pair_list": (c_int32, [_P, _P, c_int64, POINTER(Box), POINTER(Grid), _P, _P, _P,
+                                       c_double, c_int32, c_int64, _P, _P, _P, c_double, c_int64,
+                                       c_int32, c_int32, _P, _P, c_int64, c_int32, _P, _P]),
     "b2md_slab_classify": (c_int32, [_P, _P, c_int64, c_double, c_double, c_double, c_double,
                                      _P, _P, _P]),
     "b2md_compact_scratch_bytes": (c_int64, [c_int64]),

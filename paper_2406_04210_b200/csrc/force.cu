@@ -311,6 +311,30 @@ __device__ __noinline__ void report_singular(int i, const float4 pi, int cnt,
     }
 }
 
+// The same over a pair row (entries j << 2 | flags, int4 tiles, see k_pair_rows): the pair
+// kernels never look at the plain rows -- the step loop's list build writes them only for
+// pairs that straddle two cells (b2md_build_pair_list).  which = 0: particle 2t, 1: 2t+1.
+__device__ __noinline__ void report_singular_pair(int i, int which, const float4 pi, int cnt,
+                                                  const int4 *__restrict__ col,
+                                                  int64_t pair_pitch,
+                                                  const float4 *__restrict__ pos, const BoxF &b,
+                                                  b2md_status *status) {
+    for (int k = 0; k < cnt; ++k) {
+        const int e = reinterpret_cast<const int *>(col + (int64_t)(k >> 2) * pair_pitch)[k & 3];
+        if (!((e >> which) & 1)) continue;
+        const int j = (int)((unsigned)e >> 2);
+        const float4 pj = pos[j];
+        const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) == 0.0f) {
+            atomicMin((unsigned long long *)&status->singular,
+                      ((unsigned long long)(unsigned)i << 32) | (unsigned)j);
+            return;
+        }
+    }
+}
+
 // ADVANCE (both list kernels): the kernel also applies what the step loop does between two force
 // evaluations -- both half-kicks with the forces it has just computed, the drift, the
 // wrap and the displacement check (= k_integrate<2>) -- so the intermediate steps of
@@ -916,6 +940,9 @@ __device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const 
 #ifndef B2MD_PAIR_MIN_BLOCKS
 #define B2MD_PAIR_MIN_BLOCKS (1024 / kPairThreads)
 #endif
+#ifndef B2MD_PAIR_INTERIOR_FACE
+#define B2MD_PAIR_INTERIOR_FACE 0
+#endif
 #ifndef B2MD_PAIR_OUTLINE
 #define B2MD_PAIR_OUTLINE 0      // 0: nothing, 1: fallback 7, 2: + multi-axis face variants, 3: all but 0
 #endif                           // (measured, profiles/README.md: 0 is the fastest build)
@@ -988,6 +1015,15 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     // mid-plane on each flagged axis
     const bool face_ok = (axes & ~clear) == 0;
     int variant = face_ok ? (axes << 3) : (axes ? 7 : 0);
+#if B2MD_PAIR_INTERIOR_FACE
+    // Experiment knob (off): interior warps whose particles are all clear of the x mid-plane run
+    // the x face-frame loop (same bits: every image number is 0 there and the correction terms
+    // cancel exactly).  With the knob off, "all warps on variant 8" measured 106.9 us against
+    // 113.4 us for variant 0 -- three packed operations MORE per entry, yet faster; with the knob
+    // on, ptxas assigned the registers of every loop differently and both took 115 us.  The
+    // +-10 % of this kernel are register-allocation luck (profiles/README.md).
+    if (variant == 0 && (clear & 1)) variant = 8;
+#endif
     if ((gated >> 2) & 0x3fff) {                     // timing experiments only (profiles/exp)
         const int v = ((gated >> 2) & 0x3fff) - 1;
         // 64: flagged warps run a second copy of the no-shift loop (instruction-cache probe)
@@ -1043,8 +1079,8 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 if (THERMO && virial) virial[i] = w;
             }
             if (!(isfinite(fx) && isfinite(fy) && isfinite(fz)))
-                report_singular((int)i, reload_f4(pos + i), counts[i], nbr + i, pitch, pos, a.box,
-                                status);
+                report_singular_pair((int)i, which, reload_f4(pos + i), cnt, col, pair_pitch, pos,
+                                     a.box, status);
         }
     }
     if (ADVANCE) advance_publish_disp<kPairThreads>(d2, s_max, status, adv);

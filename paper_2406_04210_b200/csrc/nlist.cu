@@ -540,14 +540,50 @@ __device__ __forceinline__ unsigned long long nl_fma2(unsigned long long a, unsi
 #define B2MD_LIST_MIN_BLOCKS 4
 #endif
 
-template <int WARPS>
+// Position of combined rank R in the bit stream (ma[x] | mb[x]), x = 0 .. n_chunks-1: word w and
+// that word with its lower-ranked bits cleared.  (R beyond the stream: word 0, harmless.)
+__device__ __forceinline__ void seek_rank(const uint32_t *ma, const uint32_t *mb, int n_chunks,
+                                          int R, int &w, uint32_t &um) {
+    int cum = 0, w0 = 0, r0 = 0;
+    for (int x = 0; x < n_chunks; ++x) {
+        const int c = __popc(ma[x] | mb[x]);
+        const bool here = R >= cum && R < cum + c;
+        w0 = here ? x : w0;
+        r0 = here ? R - cum : r0;
+        cum += c;
+    }
+    w = w0;
+    um = ma[w0] | mb[w0];
+    for (int k = 0; k < r0; ++k) um &= um - 1u;
+}
+
+// PAIRS (b2md_build_pair_list): the kernel emits the force kernel's PAIR ROWS (see k_pair_rows
+// below for the layout) straight from the ballot masks instead of the plain rows.  Rows 2t and
+// 2t+1 that sit next to each other in a pass share one candidate stream, so their merged row is
+// the set bits of (mask of 2t | mask of 2t+1) in stream order, each entry flagged with the two
+// mask bits -- no merge, and the 4 c B per particle of plain rows are never written or read back.
+// The pairs of a pass share the warp: each gets 32 / pairs lanes, and the lanes of a pair split
+// its merged row by RANK into runs of whole int4 tiles (a lane seeks to its first entry through
+// the population counts of the mask words), so they are balanced and tile-aligned by
+// construction.  Rows whose partner lives in another cell or pass ("single" rows) are dealt to
+// the lanes the same way and stored as plain rows; k_pair_rows<true> merges those afterwards
+// and pads every pair row to the longest row of its force-kernel warp.
+struct PairOut {
+    int4 *pair_nbr;
+    int32_t *pair_counts;
+    int64_t pair_pitch;
+    int pair_tiles;
+};
+
+template <int WARPS, bool PAIRS>
 __global__ void __launch_bounds__(WARPS * 32, B2MD_LIST_MIN_BLOCKS)
 k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict__ pos_lo,
                     int64_t n, int64_t n_rows, const __grid_constant__ ListGeom g,
                     int64_t n_cells, const int32_t *__restrict__ cell_start,
                     const int32_t *__restrict__ cell_particles, int stride, int64_t pitch,
                     int32_t *__restrict__ nbr, int32_t *__restrict__ counts,
-                    uint8_t *__restrict__ boundary, b2md_status *status, int exact_prefix) {
+                    uint8_t *__restrict__ boundary, b2md_status *status, int exact_prefix,
+                    const __grid_constant__ PairOut po) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char *base = smem_raw + warp * ballot_warp_bytes();
@@ -621,6 +657,32 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
         const int i = active ? i_raw : -1;
         const float4 hi_i = active ? pos_hi[i] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
         int found = 0;
+        // PAIRS: lanes per pair / per single row of the pass (see the kernel comment)
+        int a_L = 32, a_sub = 0, a_row = 0, a_i = 0, a_done = 0;
+        int b_L = 32, b_sub = 0, b_row = 0, b_i = 0, b_done = 0;
+        bool a_has = false, b_has = false;
+        int e1 = 0, e2 = 0, e3 = 0;
+        if (PAIRS) {
+            const int i_next = __shfl_down_sync(0xffffffffu, i_raw, 1);
+            const int i_prev = __shfl_up_sync(0xffffffffu, i_raw, 1);
+            const bool lo_ok = ascending && active && !(i & 1) && lane + 1 < ni &&
+                               i_next == i + 1 && i + 1 < n_rows;
+            const bool hi_ok = ascending && active && (i & 1) && lane >= 1 && i_prev == i - 1;
+            const unsigned lo_mask = __ballot_sync(0xffffffffu, lo_ok);
+            const unsigned sg_mask = __ballot_sync(0xffffffffu, active && !lo_ok && !hi_ok);
+            const int n_a = __popc(lo_mask), n_b = __popc(sg_mask);
+            a_L = n_a ? 32 / n_a : 32;
+            b_L = n_b ? 32 / n_b : 32;
+            const int ua = lane / a_L, ub = lane / b_L;
+            a_sub = lane - ua * a_L;
+            b_sub = lane - ub * b_L;
+            a_has = ua < n_a;
+            b_has = ub < n_b;
+            a_row = a_has ? (int)__fns(lo_mask, 0, ua + 1) : 0;
+            b_row = b_has ? (int)__fns(sg_mask, 0, ub + 1) : 0;
+            a_i = __shfl_sync(0xffffffffu, i_raw, a_row);
+            b_i = __shfl_sync(0xffffffffu, i_raw, b_row);
+        }
         {
             __syncwarp();
             if (lane < kPassRows) {
@@ -718,6 +780,123 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                     if (lane < ni && self >= 0 && self < total)
                         s_mask[lane * kMaskPitch + (self >> 5)] &= ~(1u << (self & 31));
                 }
+                if (PAIRS) {
+                    // rows of this batch counted from their masks (counts[], overflow)
+                    if (active) {
+                        const uint32_t *mr = s_mask + lane * kMaskPitch;
+                        for (int w = 0; w < n_chunks; ++w) found += __popc(mr[w]);
+                    }
+                    // ---- pairs: merged row = set bits of (mask A | mask B) in stream order
+                    {
+                        const uint32_t *ma = s_mask + a_row * kMaskPitch;
+                        const uint32_t *mb = ma + kMaskPitch;
+                        int T = 0;
+                        if (a_has)
+                            for (int w = 0; w < n_chunks; ++w) T += __popc(ma[w] | mb[w]);
+                        // entries carried in sub-lane 0's registers from the previous batch
+                        // (unfinished tile): that lane then takes the whole batch
+                        const int carry = a_done & 3;
+                        const int full = T >> 2;
+                        int t0 = full * a_sub / a_L, t1 = full * (a_sub + 1) / a_L;
+                        int left = 4 * (t1 - t0) + (a_sub == a_L - 1 ? (T & 3) : 0);
+                        if (carry) { t0 = 0; left = a_sub == 0 ? T : 0; }
+                        if (!a_has) left = 0;
+                        int tile = (a_done >> 2) + t0;
+                        int w = 0;
+                        uint32_t um = 0u;
+                        seek_rank(ma, mb, n_chunks, 4 * t0, w, um);
+                        uint32_t aw = ma[w], bw = mb[w];
+                        const int32_t *ps = s_stream + w * 32;
+                        int4 *pt = po.pair_nbr + (a_i >> 1) + (int64_t)tile * po.pair_pitch;
+                        int e0 = 0;
+#define B2MD_NEXT_ENTRY()                                                                         \
+    {                                                                                             \
+        while (um == 0u && left > 0) {       /* (1 % of the words are empty) */                   \
+            ++w;                                                                                  \
+            aw = ma[w];                                                                           \
+            bw = mb[w];                                                                           \
+            um = aw | bw;                                                                         \
+            ps += 32;                                                                             \
+        }                                                                                         \
+        const bool has = left > 0 && um != 0u;                                                    \
+        const int bit = (__ffs(um) - 1) & 31;                                                     \
+        um &= um - 1u;                                                                            \
+        const int j = ps[bit] & 0x03ffffff;                                                       \
+        const int e = (j << 2) | (int)((aw >> bit) & 1u) | (int)(((bw >> bit) & 1u) << 1);        \
+        if (has) { e0 = e1; e1 = e2; e2 = e3; e3 = e; }                                           \
+        left -= has ? 1 : 0;                                                                      \
+    }
+                        if (carry && a_sub == 0 && a_has) {
+                            // finish the carried tile first (rare: cells with several batches)
+                            int fill = carry;
+                            while (fill < 4 && left > 0) {
+                                const int before = left;
+                                B2MD_NEXT_ENTRY();
+                                fill += before - left;
+                            }
+                            if (fill == 4) {
+                                if (tile < po.pair_tiles) *pt = make_int4(e0, e1, e2, e3);
+                                pt += po.pair_pitch;
+                                ++tile;
+                            }
+                        }
+                        // Branch-free tile loop: four entries, one 16-byte store.  (The lanes of
+                        // a warp are at different words and tiles; every divergent branch would
+                        // be executed once per path.)
+                        while (__any_sync(0xffffffffu, left > 0)) {
+                            const bool whole = left >= 4;
+#pragma unroll
+                            for (int rep = 0; rep < 4; ++rep) B2MD_NEXT_ENTRY();
+                            if (whole && tile < po.pair_tiles) *pt = make_int4(e0, e1, e2, e3);
+                            pt += po.pair_pitch;
+                            ++tile;
+                        }
+#undef B2MD_NEXT_ENTRY
+                        // the unfinished tile sits in the last lane of the pair (or in sub-lane
+                        // 0 when that one took the whole batch): hand it to sub-lane 0, which
+                        // continues it in the next batch or flushes it
+                        const int src = carry ? lane : lane - a_sub + a_L - 1;
+                        const int t1e = __shfl_sync(0xffffffffu, e1, src & 31);
+                        const int t2e = __shfl_sync(0xffffffffu, e2, src & 31);
+                        const int t3e = __shfl_sync(0xffffffffu, e3, src & 31);
+                        if (a_sub == 0) { e1 = t1e; e2 = t2e; e3 = t3e; }
+                        a_done += T;
+                    }
+                    // ---- single rows: plain-row entries at their rank
+                    if (__any_sync(0xffffffffu, b_has)) {
+                        const uint32_t *mr = s_mask + b_row * kMaskPitch;
+                        int T = 0;
+                        if (b_has)
+                            for (int w = 0; w < n_chunks; ++w) T += __popc(mr[w]);
+                        const int k0 = T * b_sub / b_L, k1 = T * (b_sub + 1) / b_L;
+                        int left = b_has ? k1 - k0 : 0;
+                        unsigned rank = (unsigned)(b_done + k0);
+                        int w = 0;
+                        uint32_t um = 0u;
+                        seek_rank(mr, mr, n_chunks, k0, w, um);
+                        const int32_t *ps = s_stream + w * 32;
+                        int32_t *pr = nbr + (int64_t)rank * pitch + b_i;
+                        while (__any_sync(0xffffffffu, left > 0)) {
+#pragma unroll
+                            for (int rep = 0; rep < 2; ++rep) {
+                                if (um == 0u && left > 0) {
+                                    ++w;
+                                    um = mr[w];
+                                    ps += 32;
+                                }
+                                const bool has = left > 0 && um != 0u;
+                                const int bit = (__ffs(um) - 1) & 31;
+                                um &= um - 1u;
+                                const int j = ps[bit] & 0x03ffffff;
+                                if (has && rank < (unsigned)stride) *pr = j;
+                                pr += has ? pitch : 0;
+                                rank += has ? 1u : 0u;
+                                left -= has ? 1 : 0;
+                            }
+                        }
+                        b_done += T;
+                    }
+                } else
                 // ---- phase 2: lane r walks the set bits of row r in stream order
                 // (= ascending j) and stores entry k of its row; all rows are at the
                 // same k, so the column-major stores coalesce across the cell's particles
@@ -766,10 +945,22 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                 }
             }
         }
+        if (PAIRS && a_has && a_sub == 0) {
+            // flush the unfinished tile (entries first, then flag-less padding)
+            int fill = a_done & 3;
+            if (fill) {
+                int e0 = 0;
+                for (; fill < 4; ++fill) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; }
+                if ((a_done >> 2) < po.pair_tiles)
+                    po.pair_nbr[(int64_t)(a_done >> 2) * po.pair_pitch + (a_i >> 1)] =
+                        make_int4(e0, e1, e2, e3);
+            }
+            po.pair_counts[a_i >> 1] = a_done;
+        }
         // slow path: some row wants more than `stride` entries, so the reference's scan
         // order decides which ones are kept (skipped when the caller is going to grow
         // the stride and rebuild anyway)
-        if (exact_prefix && __any_sync(0xffffffffu, found > stride)) {
+        if (!PAIRS && exact_prefix && __any_sync(0xffffffffu, found > stride)) {
             found = 0;
             if (active)
                 found = scan_row_reference_order(pos_hi, pos_lo, g, cx, cy, cz, cell_start,
@@ -883,6 +1074,10 @@ __global__ void k_max_disp(const float4 *__restrict__ pos_hi, const float4 *__re
 // and trip fetches four entries and a warp reads 512 contiguous bytes.  Rows are
 // padded with flag-less entries (j = 0) up to the longest row of the warp, so the
 // force kernel needs no per-entry bound check.
+// FIXUP (after k_list_cells_ballot<.., PAIRS>): only the pairs that kernel left marked
+// (pair_counts[t] < 0: the two rows were not neighbours in one pass of one cell and went to the
+// plain list) are merged; every row is then padded to the longest row of its warp.
+template <bool FIXUP>
 __global__ void __launch_bounds__(128)
 k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
             int64_t n_rows, int4 *__restrict__ pair_nbr, int32_t *__restrict__ pair_counts,
@@ -890,53 +1085,67 @@ k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t n_pairs = (n_rows + 1) >> 1;
     const bool active = t < n_pairs;
-    const int64_t a = 2 * t, b = 2 * t + 1;
-    const int ca = active ? counts[a] : 0;
-    const int cb = (active && b < n_rows) ? counts[b] : 0;
-    const int32_t *ra = nbr + a, *rb = nbr + b;
-    constexpr int kEnd = 0x7fffffff;
-    int ia = 0, ib = 0;
-    int va = ca > 0 ? ra[0] : kEnd;
-    int vb = cb > 0 ? rb[0] : kEnd;
-    int e0 = 0, e1 = 0, e2 = 0, e3 = 0, k = 0;
     int4 *out = pair_nbr + t;
-    const int cap = pair_tiles * 4;
-    while (va != kEnd || vb != kEnd) {
-        const int m = min(va, vb);
-        const bool from_a = va == m, from_b = vb == m;
-        const int e = (m << 2) | (from_a ? 1 : 0) | (from_b ? 2 : 0);
-        if (from_a) { ++ia; va = ia < ca ? ra[(int64_t)ia * pitch] : kEnd; }
-        if (from_b) { ++ib; vb = ib < cb ? rb[(int64_t)ib * pitch] : kEnd; }
-        e0 = e1; e1 = e2; e2 = e3; e3 = e;
-        ++k;
-        if ((k & 3) == 0 && k <= cap)
+    int total = 0, k = 0;
+    bool merge = active;
+    if (FIXUP && active) {
+        total = pair_counts[t];
+        merge = total < 0;
+        k = (total + 3) & ~3;
+    }
+    if (merge) {
+        const int64_t a = 2 * t, b = 2 * t + 1;
+        const int ca = counts[a];
+        const int cb = b < n_rows ? counts[b] : 0;
+        const int32_t *ra = nbr + a, *rb = nbr + b;
+        constexpr int kEnd = 0x7fffffff;
+        int ia = 0, ib = 0;
+        int va = ca > 0 ? ra[0] : kEnd;
+        int vb = cb > 0 ? rb[0] : kEnd;
+        int e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+        k = 0;
+        const int cap = pair_tiles * 4;
+        while (va != kEnd || vb != kEnd) {
+            const int m = min(va, vb);
+            const bool from_a = va == m, from_b = vb == m;
+            const int e = (m << 2) | (from_a ? 1 : 0) | (from_b ? 2 : 0);
+            if (from_a) { ++ia; va = ia < ca ? ra[(int64_t)ia * pitch] : kEnd; }
+            if (from_b) { ++ib; vb = ib < cb ? rb[(int64_t)ib * pitch] : kEnd; }
+            e0 = e1; e1 = e2; e2 = e3; e3 = e;
+            ++k;
+            if ((k & 3) == 0 && k <= cap)
+                out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
+        }
+        total = k;                             // <= ca + cb <= capacity by construction
+        // flush the partial tile (flag-less padding entries)
+        while (k & 3) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; ++k; }
+        if (k > total && k <= cap)
             out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
     }
-    const int total = k;                       // <= ca + cb <= capacity by construction
-    // flush the partial tile, then pad to the warp's longest row (flag-less entries)
-    while (k & 3) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; ++k; }
-    if (k > total && k <= cap)
-        out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
+    // pad to the warp's longest row
     const int tiles = k >> 2;
-    const int warp_tiles = __reduce_max_sync(0xffffffffu, tiles);
+    const int warp_tiles = min(__reduce_max_sync(0xffffffffu, tiles), pair_tiles);
     if (t < pair_pitch)
         for (int q = tiles; q < warp_tiles; ++q)
             out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
-    if (t < pair_pitch) pair_counts[t] = active ? total : 0;
+    if (t < pair_pitch && (!FIXUP || merge || !active)) pair_counts[t] = active ? total : 0;
 }
 
 }  // namespace b2md
 
 using namespace b2md;
 
-B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
-                                    const b2md_box *box, const b2md_grid *grid,
-                                    const int32_t *d_cell_of, const int32_t *d_cell_start,
-                                    const int32_t *d_cell_particles, double r_list,
-                                    int32_t stride, int64_t pitch, int32_t *d_nbr,
-                                    int32_t *d_counts, uint8_t *d_boundary,
-                                    double boundary_margin, int64_t n_rows, int32_t flags,
-                                    b2md_status *d_status, void *stream) {
+namespace {
+
+// pairs != nullptr: pair rows are wanted as well (b2md_build_pair_list); *pairs_done says
+// whether the list kernel emitted them itself (the plain rows are then incomplete).
+int build_list(const void *d_pos_hi, const void *d_pos_lo, int64_t n, const b2md_box *box,
+               const b2md_grid *grid, const int32_t *d_cell_of, const int32_t *d_cell_start,
+               const int32_t *d_cell_particles, double r_list, int32_t stride, int64_t pitch,
+               int32_t *d_nbr, int32_t *d_counts, uint8_t *d_boundary, double boundary_margin,
+               int64_t n_rows, int32_t flags, b2md_status *d_status, void *stream,
+               const PairOut *pairs, bool *pairs_done) {
+    if (pairs_done) *pairs_done = false;
     if (n <= 0 || !box || !grid || !d_status) { set_error("b2md_build_nlist: bad arguments"); return -1; }
     if (stride < 1) { set_error("b2md_build_nlist: stride must be >= 1"); return -2; }
     if (pitch < n) { set_error("b2md_build_nlist: pitch < n"); return -3; }
@@ -994,12 +1203,26 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
         constexpr int kBallotWarps = 8;
         const int64_t nc = grid->n_cells;
         const size_t smem = ballot_warp_bytes() * kBallotWarps;
-        cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_list_cells_ballot<kBallotWarps><<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
-            (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc, d_cell_start,
-            d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary, d_status,
-            (flags & B2MD_LIST_ANY_PREFIX) ? 0 : 1);
+        if (pairs && (flags & B2MD_LIST_ANY_PREFIX) && env_choice("B2MD_LIST_PAIRS", 1) != 0) {
+            cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            // every pair starts out marked "merge from the plain rows"
+            cudaMemsetAsync(pairs->pair_counts, 0xff, sizeof(int32_t) * (size_t)pairs->pair_pitch, s);
+            k_list_cells_ballot<kBallotWarps, true>
+                <<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
+                    (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc,
+                    d_cell_start, d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary,
+                    d_status, 0, *pairs);
+            *pairs_done = true;
+        } else {
+            cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_list_cells_ballot<kBallotWarps, false>
+                <<<blocks_for(nc, kBallotWarps), kBallotWarps * 32, smem, s>>>(
+                    (const float4 *)d_pos_hi, (const float4 *)d_pos_lo, n, n_rows, g, nc,
+                    d_cell_start, d_cell_particles, stride, pitch, d_nbr, d_counts, d_boundary,
+                    d_status, (flags & B2MD_LIST_ANY_PREFIX) ? 0 : 1, PairOut{});
+        }
     } else if (prefilter && warp_smem * 2 <= 200 * 1024) {
         // warp-per-cell kernel; fewer warps per CTA when rows are long
         const int64_t nc = grid->n_cells;
@@ -1030,6 +1253,57 @@ B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, 
     if (d_boundary)
         k_count_boundary<<<blocks_for(n_rows, 256), 256, 0, s>>>(d_boundary, n_rows, d_status);
     B2MD_CHECK_LAUNCH("b2md_build_nlist");
+    return 0;
+}
+
+}  // namespace
+
+B2MD_EXPORT int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                    const b2md_box *box, const b2md_grid *grid,
+                                    const int32_t *d_cell_of, const int32_t *d_cell_start,
+                                    const int32_t *d_cell_particles, double r_list,
+                                    int32_t stride, int64_t pitch, int32_t *d_nbr,
+                                    int32_t *d_counts, uint8_t *d_boundary,
+                                    double boundary_margin, int64_t n_rows, int32_t flags,
+                                    b2md_status *d_status, void *stream) {
+    return build_list(d_pos_hi, d_pos_lo, n, box, grid, d_cell_of, d_cell_start, d_cell_particles,
+                      r_list, stride, pitch, d_nbr, d_counts, d_boundary, boundary_margin, n_rows,
+                      flags, d_status, stream, nullptr, nullptr);
+}
+
+B2MD_EXPORT int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
+                                     const b2md_box *box, const b2md_grid *grid,
+                                     const int32_t *d_cell_of, const int32_t *d_cell_start,
+                                     const int32_t *d_cell_particles, double r_list,
+                                     int32_t stride, int64_t pitch, int32_t *d_nbr,
+                                     int32_t *d_counts, uint8_t *d_boundary,
+                                     double boundary_margin, int64_t n_rows, int32_t flags,
+                                     int32_t list_rows, int32_t *d_pair_nbr,
+                                     int32_t *d_pair_counts, int64_t pair_pitch,
+                                     int32_t pair_rows, b2md_status *d_status, void *stream) {
+    const int64_t n_pairs = (n_rows + 1) / 2;
+    if (!d_pair_nbr || !d_pair_counts || pair_pitch < n_pairs || pair_pitch % 32 != 0 ||
+        pair_rows % 4 != 0 || pair_rows < 2 * list_rows || list_rows < stride) {
+        set_error("b2md_build_pair_list: pair_pitch must be a multiple of 32 >= ceil(n_rows/2), "
+                  "pair_rows a multiple of 4 >= 2 * list_rows, list_rows >= stride");
+        return -6;
+    }
+    const PairOut po = {(int4 *)d_pair_nbr, d_pair_counts, pair_pitch, pair_rows / 4};
+    bool pairs_done = false;
+    int rc = build_list(d_pos_hi, d_pos_lo, n, box, grid, d_cell_of, d_cell_start,
+                        d_cell_particles, r_list, stride, pitch, d_nbr, d_counts, d_boundary,
+                        boundary_margin, n_rows, flags, d_status, stream, &po, &pairs_done);
+    if (rc) return rc;
+    const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
+    if (pairs_done)
+        k_pair_rows<true><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+                                                                 po.pair_nbr, d_pair_counts,
+                                                                 pair_pitch, po.pair_tiles);
+    else
+        k_pair_rows<false><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+                                                                  po.pair_nbr, d_pair_counts,
+                                                                  pair_pitch, po.pair_tiles);
+    B2MD_CHECK_LAUNCH("b2md_build_pair_list");
     return 0;
 }
 
@@ -1084,9 +1358,9 @@ B2MD_EXPORT int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, in
     }
     // whole warps only: the padding loop uses a warp reduction
     const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
-    k_pair_rows<<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
-                                                       (int4 *)d_pair_nbr, d_pair_counts,
-                                                       pair_pitch, pair_rows / 4);
+    k_pair_rows<false><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+                                                              (int4 *)d_pair_nbr, d_pair_counts,
+                                                              pair_pitch, pair_rows / 4);
     B2MD_CHECK_LAUNCH("b2md_pair_rows");
     return 0;
 }

@@ -247,17 +247,25 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
     if ((rc = b2md_bin(a.pos_hi, a.pos_lo, c.n, &r->grid, c.cell_of, c.cell_start,
                        c.cell_particles, c.bin_scratch, s))) return rc;
     // an overflowed list is never used here: the caller grows the stride and rebuilds
-    if ((rc = b2md_build_nlist_ex(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
-                                  c.cell_start, c.cell_particles, r->r_list, c.stride, c.pitch,
-                                  c.nbr, c.counts, c.boundary, r->r_list + c.skin, c.n,
-                                  B2MD_LIST_ANY_PREFIX, c.status, s)))
+    if (c.pair_rows > 0) {
+        // list and pair rows in one go (the plain rows are written only where a pair straddles
+        // two cells)
+        if ((rc = b2md_build_pair_list(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
+                                       c.cell_start, c.cell_particles, r->r_list, c.stride,
+                                       c.pitch, c.nbr, c.counts, c.boundary, r->r_list + c.skin,
+                                       c.n, B2MD_LIST_ANY_PREFIX, stride_rows(r), c.pair_nbr,
+                                       c.pair_counts, c.pair_pitch, c.pair_rows, c.status, s)))
+            return rc;
+    } else if ((rc = b2md_build_nlist_ex(a.pos_hi, a.pos_lo, c.n, &c.box, &r->grid, c.cell_of,
+                                         c.cell_start, c.cell_particles, r->r_list, c.stride,
+                                         c.pitch, c.nbr, c.counts, c.boundary, r->r_list + c.skin,
+                                         c.n, B2MD_LIST_ANY_PREFIX, c.status, s))) {
         return rc;
+    }
     if ((rc = b2md_snapshot(a.pos_hi, a.pos_lo, a.image, c.n, &c.box, c.at_build, c.ref_pos, s)))
         return rc;
     *kernels += 1 + 3 + scan_launches(r->grid.n_cells) + 2 + 1;
     if (c.pair_rows > 0) {
-        if ((rc = b2md_pair_rows(c.nbr, c.counts, c.pitch, stride_rows(r), c.n, c.pair_nbr,
-                                 c.pair_counts, c.pair_pitch, c.pair_rows, s))) return rc;
         *kernels += 1;
         if (c.pair_schedule) {
             if ((rc = b2md_pair_schedule(c.boundary, c.n, c.pair_counts, c.pair_pitch, s)))
