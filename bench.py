@@ -412,6 +412,68 @@ def run_gpu_arm(args):
                   k["boundary"].data_ptr(), tab_ptr, 1, _lib.FORCE_SKIP_THERMO | sched,
                   dev.force.data_ptr(), dev.virial.data_ptr(), dev.status.data_ptr(), dev.stream)
 
+    extra_kernels = {}
+    if sim.pair_rows:
+        # The step loop's list build (b2md_build_pair_list) writes plain rows only for the pairs
+        # that straddle two cells.  The per-kernel timings below want the complete per-particle
+        # list next to the pair rows made from it: bin and build both here, on the positions the
+        # timed run ended on -- the two-stage path the fused build replaces, timed beside it.
+        cfg = k["cfg"]
+        r_list = R_CUT + SKIN
+        grid = _lib.Grid()
+        _lib.call("b2md_grid_shape", box.c_box(), r_list, ctypes.byref(grid))
+        pair_rows_alt = torch.zeros_like(k["pair_nbr"])
+        pair_counts_alt = torch.zeros_like(k["pair_counts"])
+
+        def rebin():
+            _lib.call("b2md_status_reset_list", dev.status.data_ptr(), dev.stream)
+            _lib.call("b2md_bin", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(), n,
+                      ctypes.byref(grid), k["cell_of"].data_ptr(), k["cell_start"].data_ptr(),
+                      k["cell_particles"].data_ptr(), k["bin_scratch"].data_ptr(), dev.stream)
+
+        def launch_list_plain():
+            _lib.call("b2md_build_nlist_ex", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(), n,
+                      box.c_box(), ctypes.byref(grid), k["cell_of"].data_ptr(),
+                      k["cell_start"].data_ptr(), k["cell_particles"].data_ptr(), r_list,
+                      cfg.stride, k["pitch"], k["nbr"].data_ptr(), k["counts"].data_ptr(),
+                      k["boundary"].data_ptr(), r_list + SKIN, n, 1, dev.status.data_ptr(),
+                      dev.stream)
+
+        def launch_list_fused():
+            _lib.call("b2md_build_pair_list", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(), n,
+                      box.c_box(), ctypes.byref(grid), k["cell_of"].data_ptr(),
+                      k["cell_start"].data_ptr(), k["cell_particles"].data_ptr(), r_list,
+                      cfg.stride, k["pitch"], k["nbr"].data_ptr(), k["counts"].data_ptr(),
+                      k["boundary"].data_ptr(), r_list + SKIN, n, 1, rows,
+                      pair_rows_alt.data_ptr(), pair_counts_alt.data_ptr(), cfg.pair_pitch,
+                      cfg.pair_rows, dev.status.data_ptr(), dev.stream)
+
+        def launch_merge():
+            _lib.call("b2md_pair_rows", k["nbr"].data_ptr(), k["counts"].data_ptr(), k["pitch"],
+                      rows, n, k["pair_nbr"].data_ptr(), k["pair_counts"].data_ptr(),
+                      cfg.pair_pitch, cfg.pair_rows, dev.stream)
+
+        rebin()
+        fused_ms = time_kernel(launch_list_fused, 5, torch, stream)
+        plain_ms = time_kernel(launch_list_plain, 5, torch, stream)      # leaves complete rows
+        merge_ms = time_kernel(launch_merge, 5, torch, stream)
+        if cfg.pair_schedule:
+            _lib.call("b2md_pair_schedule", k["boundary"].data_ptr(), n,
+                      k["pair_counts"].data_ptr(), cfg.pair_pitch, dev.stream)
+        torch.cuda.synchronize()
+        same_pairs = bool(torch.equal(pair_rows_alt, k["pair_nbr"]) and
+                          torch.equal(pair_counts_alt[:cfg.pair_pitch],
+                                      k["pair_counts"][:cfg.pair_pitch]))
+        cbar = float(k["counts"][:n].float().mean().item())
+        extra_kernels["b2md_build_pair_list (list + pair rows, once per rebuild: "
+                      "k_list_cells_ballot<PAIRS> + k_pair_fixup)"] = {
+            "launch_ms": fused_ms, "algorithmic_bytes_per_launch": n * (32.0 + 4.0 * cbar),
+            "achieved": n * (32.0 + 4.0 * cbar) / (fused_ms * 1e-3) / 1e9,
+            "pair_rows_identical_to_two_stage_build": same_pairs}
+        extra_kernels["two-stage build it replaces (k_list_cells_ballot + k_pair_rows)"] = {
+            "launch_ms": plain_ms + merge_ms, "list_ms": plain_ms, "merge_ms": merge_ms}
+        del pair_rows_alt, pair_counts_alt
+
     # the kernel the step loop launches (pair rows for systems this large)
     force_kernel = "k_force_lj_pair" if sim.pair_rows else "k_force_lj"
     force_ms = time_kernel(launch_force_pairs if sim.pair_rows else launch_force_rows, 50, torch,
@@ -419,21 +481,12 @@ def run_gpu_arm(args):
     pair_entries = (float(k["pair_counts"][:k["cfg"].pair_pitch].float().sum().item()) / n
                     if sim.pair_rows else None)
 
-    extra_kernels = {}
     if sim.pair_rows:
-        # for comparison: the thread-per-particle kernel on the same list, and the merge
+        # for comparison: the thread-per-particle kernel on the same list
         rows_ms = time_kernel(launch_force_rows, 20, torch, stream)
         extra_kernels["k_force_lj (thread per particle, same list)"] = {
             "launch_ms": rows_ms,
             "achieved": n * (32.0 + 4.0 * cbar) / (rows_ms * 1e-3) / 1e9}
-        cfg = k["cfg"]
-
-        def launch_merge():
-            _lib.call("b2md_pair_rows", k["nbr"].data_ptr(), k["counts"].data_ptr(), k["pitch"],
-                      rows, n, k["pair_nbr"].data_ptr(), k["pair_counts"].data_ptr(),
-                      cfg.pair_pitch, cfg.pair_rows, dev.stream)
-        extra_kernels["k_pair_rows (once per rebuild)"] = {
-            "launch_ms": time_kernel(launch_merge, 10, torch, stream)}
     force_bytes = n * (32.0 + 4.0 * cbar)          # pos 16 + idx 4*c + force 16 (no-thermo variant)
     peak, peak_src = measured_peak()
     achieved = force_bytes / (force_ms * 1e-3) / 1e9

@@ -310,6 +310,39 @@ int b2md_force_lj_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *
  * launch anyway (the all-reduce of the rebuild flag) orders the stores before the
  * neighbour's next launch.  A launch whose gate is closed stores nothing.  Null slot
  * arrays = no halo on that side; all four null = b2md_force_lj_pairs_advance. */
+/* One-launch step over PRUNED pair rows (dynamic pruning of the Verlet list; the reference has
+ * one list, neighbor.py:185-240, and evaluates every listed pair every step, forces.py:72-110).
+ * The full ("outer") rows d_pair_nbr hold every pair inside r_cut + skin at the last list build;
+ * only the pairs inside r_cut now contribute (forces.py:92).  A launch with prune_mode
+ * B2MD_PRUNE_NOW walks the outer rows and also writes the "inner" rows: the entries either
+ * particle of the pair has inside r_cut_max + delta now, same order, same layout (d_inner_nbr,
+ * d_inner_counts, pair_rows entries per row), and records every particle's displacement from
+ * the list snapshot in the spare word of d_ref_pos_f4.  Launches with B2MD_PRUNE_INNER walk the
+ * inner rows (fewer entries; the dropped ones would have contributed exact zeros, so the forces
+ * are bit-identical) and are valid while no particle has moved more than delta / 2 since the
+ * prune; B2MD_PRUNE_OUTER walks the outer rows (when the inner ones are stale and a prune is
+ * not legal any more).  Every launch publishes three flag bits about the positions it WRITES in
+ * status word gate_out_word: 1 = they need a new list (as b2md_force_lj_pairs_advance), 2 = the
+ * inner rows have expired for them, 4 = a prune is no longer legal for them (a particle is
+ * further than (skin - delta) / 2 from the list snapshot, so the outer rows are not complete
+ * to r_cut_max + delta).  A launch whose gate_in_word says it must not run (bit 1; bit 2 for
+ * B2MD_PRUNE_INNER; bit 4 for B2MD_PRUNE_NOW) returns at once and copies the word to
+ * gate_out_word.  The flag bits do not clear themselves: three status words rotate, and
+ * every launch zeroes gate_clear_word (the word the next launch will write).  Status word 15
+ * collects the largest squared displacement since the prune. */
+#define B2MD_PRUNE_INNER 1
+#define B2MD_PRUNE_NOW 2
+#define B2MD_PRUNE_OUTER 3
+int b2md_force_lj_pairs_advance_pruned(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
+    int32_t gate_out_word, int32_t gate_clear_word, int32_t prune_mode, int32_t *d_inner_nbr,
+    int32_t *d_inner_counts, int32_t pair_rows, double r_cut_max, double skin, double delta,
+    b2md_status *d_status, void *stream);
+
 int b2md_force_lj_pairs_advance_halo(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
                                      void *d_vel, void *d_image_i4, int64_t n,
                                      const b2md_box *box, double dt, void *d_ref_pos_f4,
@@ -534,6 +567,13 @@ typedef struct b2md_runner_config {
     void *h_status;              /* >= 64 bytes of page-locked host memory */
     void *run_stream;            /* cudaStream_t for the step loop (must not be `stream`) */
     void *copy_stream;           /* cudaStream_t for the status read-backs */
+    /* Pruned ("inner") pair rows: with prune_delta > 0 (and pair rows, pos_hi_alt, queue_depth
+     * 1) the one-launch steps walk rows pruned to r_cut + prune_delta, re-pruned from the full
+     * rows whenever a particle has moved prune_delta / 2 since the last prune -- see
+     * b2md_force_lj_pairs_advance_pruned.  Same shapes as pair_nbr / pair_counts. */
+    int32_t *pair_nbr_inner;
+    int32_t *pair_counts_inner;
+    double prune_delta;
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };
@@ -582,6 +622,11 @@ int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finalize_at_end,
  * call.  probability = min(rate * dt, 1); 0 switches the thermostat off.  A thermostatted
  * runner launches integrate / force / finalize / thermostat separately (the thermostat
  * sits between the two half-kicks that the fused kernels merge). */
+/* After a stride growth: the new inner pair rows (same shape as the new pair rows). */
+int b2md_runner_set_inner_pair_list(b2md_runner *runner, int32_t *d_pair_nbr_inner);
+/* Prune launches so far; *outer_steps (may be NULL) = one-launch steps that had to walk the
+ * full rows because the inner ones had expired and a prune was no longer legal. */
+int64_t b2md_runner_prune_count(const b2md_runner *runner, int64_t *outer_steps);
 int b2md_runner_set_thermostat(b2md_runner *r, double probability, double temperature,
                                uint64_t seed);
 /* Step counter (SignalEngine.step_count) of the first step of the next b2md_runner_run. */

@@ -72,6 +72,7 @@ class RunnerConfig(Structure):
         ("pos_hi_alt", c_void_p), ("queue_depth", c_int32), ("pair_schedule", c_int32),
         ("persistent_steps", c_int32), ("list_row_multiple", c_int32), ("barrier", c_void_p),
         ("h_status", c_void_p), ("run_stream", c_void_p), ("copy_stream", c_void_p),
+        ("pair_nbr_inner", c_void_p), ("pair_counts_inner", c_void_p), ("prune_delta", c_double),
     ]
 
 
@@ -152,6 +153,12 @@ _SIGNATURES = {
                                               _P, c_double, _P, _P, c_int64, _P, _P, c_int64, _P,
                                               POINTER(c_double), c_int32, c_int32, c_int32,
                                               c_int32, _P, _P]),
+    "b2md_force_lj_pairs_advance_pruned": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box),
+                                                     c_double, _P, c_double, _P, _P, c_int64, _P,
+                                                     _P, c_int64, _P, POINTER(c_double), c_int32,
+                                                     c_int32, c_int32, c_int32, c_int32, c_int32,
+                                                     _P, _P, c_int32, c_double, c_double,
+                                                     c_double, _P, _P]),
     "b2md_force_lj_pairs_advance_halo": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box),
                                                    c_double, _P, c_double, _P, _P, c_int64, _P, _P,
                                                    c_int64, _P, POINTER(c_double), c_int32,
@@ -187,6 +194,8 @@ _SIGNATURES = {
     "b2md_runner_set_pair_list": (c_int32, [c_void_p, _P, c_int32]),
     "b2md_runner_prepare": (c_int32, [c_void_p, POINTER(RunReport)]),
     "b2md_runner_run": (c_int32, [c_void_p, c_int64, c_int32, POINTER(RunReport)]),
+    "b2md_runner_set_inner_pair_list": (c_int32, [c_void_p, _P]),
+    "b2md_runner_prune_count": (c_int64, [c_void_p, POINTER(c_int64)]),
     "b2md_runner_set_thermostat": (c_int32, [c_void_p, c_double, c_double, c_uint64]),
     "b2md_runner_set_step": (c_int32, [c_void_p, c_int64]),
 }

@@ -358,13 +358,40 @@ struct AdvanceArgs {
     // (peer memory over NVLink).  Null = no halo on that side.
     const int32_t *halo_dst[2];
     float4 *halo_out[2];
+    // Pruned ("inner") pair rows, b2md_force_lj_pairs_advance_pruned: prune_mode 0 = none,
+    // kPruneInner = walk the inner rows, kPruneNow = walk the outer rows and write the inner ones
+    // (entries with r < r_cut + delta, the prune snapshot into ref_pos.w), kPruneOuter = walk the
+    // outer rows but keep publishing the inner flags.  Flag bits of the gate words: 1 = the
+    // positions need a new list, 2 = the inner rows have expired for them (some particle moved
+    // more than delta / 2 since the prune), 4 = a prune is no longer legal for them (some
+    // particle is further than (skin - delta) / 2 from the list snapshot, so the outer rows are
+    // not complete to r_cut + delta any more).  gate_clear: the third word of the rotation,
+    // zeroed by this launch for the next one to write.
+    int prune_mode, gate_clear;
+    int4 *inner_nbr;
+    int32_t *inner_counts;
+    float inner_rl2, inner_half2, prune_limit2;
+    int inner_tiles;
 };
+constexpr int kPruneInner = 1, kPruneNow = 2, kPruneOuter = 3;
+constexpr int kWordInnerDisp = 15;         // b2md_status::reserved[3]: max inner displacement^2
 
 // Gate of an ADVANCE launch (see AdvanceArgs): true = this launch must not run.
 __device__ __forceinline__ bool advance_gate_closed(b2md_status *status, const AdvanceArgs &adv) {
     // a launch that must not run hands the flag on, so that launches queued behind it
     // do not run either; one that runs counts itself (the host may have several queued)
-    if (((volatile int *)status)[adv.gate_in]) {
+    const int w = ((volatile int *)status)[adv.gate_in];
+    if (adv.prune_mode) {
+        // three gate words in rotation (flag bits do not clear themselves as the rebuild flag
+        // does): nobody reads or writes gate_clear during this launch
+        if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_clear] = 0;
+        const bool closed = (w & 1) || (adv.prune_mode == kPruneInner && (w & 2)) ||
+                            (adv.prune_mode == kPruneNow && (w & 4));
+        if (closed) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_out] = w;
+            return true;
+        }
+    } else if (w) {
         if (blockIdx.x == 0 && threadIdx.x == 0) ((int *)status)[adv.gate_out] = 1;
         return true;
     }
@@ -384,7 +411,30 @@ __device__ __forceinline__ void advance_publish_disp(float d2, float *s_max, b2m
         m = warp_max(m);
         if (threadIdx.x == 0 && m > 0.0f) {
             atomicMax(&status->max_disp2_bits, __float_as_uint(m));
-            if (m > adv.step.half_skin2) ((int *)status)[adv.gate_out] = 1;
+            if (adv.prune_mode) {
+                const int bits = (m > adv.step.half_skin2 ? 1 : 0) | (m > adv.prune_limit2 ? 4 : 0);
+                if (bits) atomicOr(&((int *)status)[adv.gate_out], bits);
+            } else if (m > adv.step.half_skin2) {
+                ((int *)status)[adv.gate_out] = 1;
+            }
+        }
+    }
+}
+
+// The same for the displacement since the last prune (flag bit 2 of the gate word).
+template <int THREADS>
+__device__ __forceinline__ void advance_publish_inner(float d2, float *s_max, b2md_status *status,
+                                                      const AdvanceArgs &adv) {
+    d2 = warp_max(d2);
+    __syncthreads();                       // s_max is reused
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < THREADS / 32 ? s_max[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0 && m > 0.0f) {
+            atomicMax(&((unsigned *)status)[kWordInnerDisp], __float_as_uint(m));
+            if (m > adv.inner_half2) atomicOr(&((int *)status)[adv.gate_out], 2);
         }
     }
 }
@@ -762,12 +812,38 @@ struct PackAcc {
     int cnt_a, cnt_b;
 };
 
+// PRUNE launches (AdvanceArgs::prune_mode == kPruneNow) also write the "inner" pair row: the
+// entries either particle of the pair still has inside r_cut + delta, ownership flags narrowed
+// to the particles that do, in the same (ascending) order and the same int4 tile layout.
+struct PruneOut {
+    int o0, o1, o2, o3, cnt, cap;
+    unsigned oq, pitch;             // element offset of the tile being filled; tiles are pitch apart
+    int4 *ocol;
+    float rl2;
+};
+// Branch-free (the lanes of a warp keep different entries; 80 % are kept): four selects shift
+// the entry in, one predicated 16-byte store per fourth kept entry.
+__device__ __forceinline__ void prune_keep(PruneOut &P, int e, float r2a, float r2b) {
+    const bool ka = (e & 1) && r2a < P.rl2, kb = (e & 2) && r2b < P.rl2;
+    const bool keep = ka || kb;
+    const int ne = (e & ~3) | (ka ? 1 : 0) | (kb ? 2 : 0);
+    P.o0 = keep ? P.o1 : P.o0;
+    P.o1 = keep ? P.o2 : P.o1;
+    P.o2 = keep ? P.o3 : P.o2;
+    P.o3 = keep ? ne : P.o3;
+    P.cnt += keep ? 1 : 0;
+    const bool st = keep && (P.cnt & 3) == 0;
+    if (st && P.cnt <= P.cap) P.ocol[P.oq] = make_int4(P.o0, P.o1, P.o2, P.o3);
+    P.oq += st ? P.pitch : 0u;
+}
+
 // SIG1: sigma^2 == 1.0f, so s2 = sigma^2 * ir2 is ir2 itself (x * 1.0f is exact: same bits,
 // one packed multiply less on the FMA pipe that bounds this kernel).
-template <int AXES, bool THERMO, bool SIG1>
+template <int AXES, bool THERMO, bool SIG1, bool PRUNE = false>
 __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 ay, f32x2 az,
                                                   f32x2 cx, f32x2 cy, f32x2 cz,
-                                                  int e, const float4 pj, const ForceArgs &a) {
+                                                  int e, const float4 pj, const ForceArgs &a,
+                                                  PruneOut *P = nullptr) {
     const BoxF &b = a.box;
     const PairParams &p = a.single;
     const f32x2 dx = delta2m<AxisMode<AXES, 0>::value>(ax, cx, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0], b.half[0]);
@@ -776,6 +852,7 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
     const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
     float r2a, r2b;
     upk(r2, r2a, r2b);
+    if (PRUNE) prune_keep(*P, e, r2a, r2b);
     const float ia = masked_rcp(r2a, p.rc2, e, 1), ib = masked_rcp(r2b, p.rc2, e, 2);
     const f32x2 ir2 = pk(ia, ib);
     const f32x2 s2 = SIG1 ? ir2 : mul2(pk1(p.sig2), ir2);
@@ -797,14 +874,14 @@ __device__ __forceinline__ void pair_entry_packed(PackAcc &acc, f32x2 ax, f32x2 
 // parameters of (type of 2t, type of j) and (type of 2t+1, type of j) in the two
 // halves.  Operation order per half is lj_pair_table's, so the sums stay bit-identical
 // to the row kernel's.
-template <int AXES, bool THERMO>
+template <int AXES, bool THERMO, bool PRUNE = false>
 __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, f32x2 ay,
                                                         f32x2 az, f32x2 cx, f32x2 cy, f32x2 cz,
                                                         int e, const float4 pj,
                                                         const ForceArgs &a,
                                                         const float4 *s_tab_a,
                                                         const float2 *s_tab_b, int ta_row,
-                                                        int tb_row) {
+                                                        int tb_row, PruneOut *P = nullptr) {
     const BoxF &b = a.box;
     const int tj = __float_as_int(pj.w);
     const float4 qa = s_tab_a[ta_row + tj], qb = s_tab_a[tb_row + tj];
@@ -814,6 +891,7 @@ __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, 
     const f32x2 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
     float r2a, r2b;
     upk(r2, r2a, r2b);
+    if (PRUNE) prune_keep(*P, e, r2a, r2b);
     const float ia = masked_rcp(r2a, qa.y, e, 1), ib = masked_rcp(r2b, qb.y, e, 2);
     const f32x2 ir2 = pk(ia, ib);
     const f32x2 s2 = mul2(pk(qa.x, qb.x), ir2);
@@ -841,13 +919,13 @@ __device__ __forceinline__ void pair_entry_packed_table(PackAcc &acc, f32x2 ax, 
 
 // `tiles` = longest row of the warp in int4 tiles (rows are padded that far with
 // flag-less entries); the index tiles of the next two trips are kept in flight.
-template <int AXES, bool TABLE, bool THERMO, bool SIG1>
+template <int AXES, bool TABLE, bool THERMO, bool SIG1, bool PRUNE = false>
 __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4 pa,
                                               const float4 pb, int tiles,
                                               const int4 *__restrict__ col, int64_t pair_pitch,
                                               const float4 *__restrict__ pos, const ForceArgs &a,
                                               const float4 *s_tab_a, const float2 *s_tab_b,
-                                              int ta_row, int tb_row) {
+                                              int ta_row, int tb_row, PruneOut *P = nullptr) {
     // The loop body is kept to one trip: unrolling it further (to rotate the tile
     // registers without moves) made instruction fetch the limiter -- 30 % of the
     // stall samples were "no instruction".
@@ -898,11 +976,12 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (TABLE)
-                pair_entry_packed_table<AXES, THERMO>(acc, ax, ay, az, cx, cy, cz, ev[u], pj[u],
-                                                      a, s_tab_a, s_tab_b, ta_row, tb_row);
+                pair_entry_packed_table<AXES, THERMO, PRUNE>(acc, ax, ay, az, cx, cy, cz, ev[u],
+                                                             pj[u], a, s_tab_a, s_tab_b, ta_row,
+                                                             tb_row, P);
             else
-                pair_entry_packed<AXES, THERMO, SIG1>(acc, ax, ay, az, cx, cy, cz, ev[u], pj[u],
-                                                      a);
+                pair_entry_packed<AXES, THERMO, SIG1, PRUNE>(acc, ax, ay, az, cx, cy, cz, ev[u],
+                                                             pj[u], a, P);
         }
 #endif
 #if B2MD_PAIR_TILE_ROTATE != 0
@@ -924,7 +1003,7 @@ __device__ __forceinline__ void pair_row_loop(RowAcc &A, RowAcc &B, const float4
 // harness, B2MD_PAIR_OUTLINE -- see the dispatch.  ptxas' register assignment inside the
 // 64-register loop decides +-10 % of this kernel (identical instruction mix, different
 // operand banks), and any change elsewhere in the kernel reshuffles it.
-template <int AXES, bool TABLE, bool THERMO, bool SIG1>
+template <int AXES, bool TABLE, bool THERMO, bool SIG1, bool PRUNE = false>
 __device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const float4 pa,
                                                     const float4 pb, int tiles,
                                                     const int4 *__restrict__ col,
@@ -932,9 +1011,9 @@ __device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const 
                                                     const float4 *__restrict__ pos,
                                                     const ForceArgs &a, const float4 *s_tab_a,
                                                     const float2 *s_tab_b, int ta_row,
-                                                    int tb_row) {
-    pair_row_loop<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch, pos, a, s_tab_a,
-                                             s_tab_b, ta_row, tb_row);
+                                                    int tb_row, PruneOut *P = nullptr) {
+    pair_row_loop<AXES, TABLE, THERMO, SIG1, PRUNE>(A, B, pa, pb, tiles, col, pair_pitch, pos, a,
+                                                    s_tab_a, s_tab_b, ta_row, tb_row, P);
 }
 
 #ifndef B2MD_PAIR_MIN_BLOCKS
@@ -949,8 +1028,8 @@ __device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const 
 
 // ADVANCE: 0 = forces only, 1 = one-launch step, 2 = one-launch step that also stores the
 // slab halo into the neighbour ranks' ghost rows (AdvanceArgs::halo_*)
-template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE>
-__global__ void __launch_bounds__(kPairThreads, B2MD_PAIR_MIN_BLOCKS)
+template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE, bool PRUNE = false>
+__global__ void __launch_bounds__(kPairThreads, PRUNE ? 6 : B2MD_PAIR_MIN_BLOCKS)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
                 int64_t pair_pitch, const int32_t *__restrict__ nbr,
@@ -983,7 +1062,9 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     const bool has_b = ia + 1 < n;
     const int64_t ib = has_b ? ia + 1 : ia;
     const float4 pa = pos[ia], pb = pos[ib];
-    const int cnt = active ? pair_counts[t] : 0;
+    // pruned step loop: the rows walked are the inner ones unless this launch prunes / falls back
+    const bool inner = ADVANCE == 1 && !PRUNE && adv.prune_mode == kPruneInner;
+    const int cnt = active ? (inner ? adv.inner_counts : pair_counts)[t] : 0;
     int tiles = __reduce_max_sync(0xffffffffu, (cnt + 3) >> 2);
     if (gated >> 16) tiles = tiles * ((gated >> 16) - 1) / 100;   // timing experiment: shorter rows
     // boundary flags of the warp's particles (nlist.cu, boundary_flag): bits 0-2 OR-ed = axes
@@ -998,17 +1079,26 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     }
     const int axes = (gated & 2) ? 0 : __reduce_or_sync(0xffffffffu, near);
     clear = __reduce_and_sync(0xffffffffu, clear);
-    const int4 *col = pair_nbr + t;
+    const int4 *col = (inner ? (const int4 *)adv.inner_nbr : pair_nbr) + t;
+    PruneOut P = {0, 0, 0, 0, 0, 0, 0u, (unsigned)pair_pitch, nullptr, 0.0f};
+    if (PRUNE) {
+        P.cap = active ? adv.inner_tiles * 4 : 0;
+        P.ocol = adv.inner_nbr + t;
+        P.rl2 = adv.inner_rl2;
+    }
     const int ta_row = TABLE ? __float_as_int(pa.w) * a.ntypes : 0;
     const int tb_row = TABLE ? __float_as_int(pb.w) * a.ntypes : 0;
 
     RowAcc A = {0.f, 0.f, 0.f, 0.f, 0.f, 0}, B = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
 #define B2MD_PAIR_LOOP(AXES)                                                                  \
-    pair_row_loop<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch, pos, a,    \
-                                             s_tab_a, s_tab_b, ta_row, tb_row)
+    pair_row_loop<AXES, TABLE, THERMO, SIG1, PRUNE>(A, B, pa, pb, tiles, col, pair_pitch, pos,  \
+                                                    a, s_tab_a, s_tab_b, ta_row, tb_row,      \
+                                                    PRUNE ? &P : nullptr)
 #define B2MD_PAIR_LOOP_OUT(AXES)                                                              \
-    pair_row_loop_outlined<AXES, TABLE, THERMO, SIG1>(A, B, pa, pb, tiles, col, pair_pitch,   \
-                                                      pos, a, s_tab_a, s_tab_b, ta_row, tb_row)
+    pair_row_loop_outlined<AXES, TABLE, THERMO, SIG1, PRUNE>(A, B, pa, pb, tiles, col,        \
+                                                             pair_pitch, pos, a, s_tab_a,     \
+                                                             s_tab_b, ta_row, tb_row,         \
+                                                             PRUNE ? &P : nullptr)
 #define B2MD_PAIR_LOOP_LVL(AXES, LVL)                                                         \
     do { if (B2MD_PAIR_OUTLINE >= LVL) B2MD_PAIR_LOOP_OUT(AXES); else B2MD_PAIR_LOOP(AXES); } while (0)
     // face frame (see face_frame): legal when every particle of the warp is clear of the
@@ -1043,7 +1133,23 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
 #undef B2MD_PAIR_LOOP
 #undef B2MD_PAIR_LOOP_OUT
 #undef B2MD_PAIR_LOOP_LVL
-    float d2 = 0.0f;
+    if (PRUNE) {
+        // flush the unfinished tile, pad to the warp's longest inner row (flag-less entries),
+        // store the inner count -- the layout k_pair_rows produces
+        const int kept = P.cnt;
+        int k = kept;
+        while (k & 3) { P.o0 = P.o1; P.o1 = P.o2; P.o2 = P.o3; P.o3 = 0; ++k; }
+        if (k > kept && k <= P.cap) P.ocol[P.oq] = make_int4(P.o0, P.o1, P.o2, P.o3);
+        const int my_tiles = active ? k >> 2 : 0;
+        const int warp_tiles = min(__reduce_max_sync(0xffffffffu, my_tiles), adv.inner_tiles);
+        if (t_raw < pair_pitch) {
+            int4 *oc = adv.inner_nbr + t_raw;
+            for (int q = my_tiles; q < warp_tiles; ++q)
+                oc[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
+            adv.inner_counts[t_raw] = active ? kept : 0;
+        }
+    }
+    float d2 = 0.0f, d2_inner = 0.0f;
     if (active) {
 #pragma unroll
         for (int which = 0; which < 2; ++which) {
@@ -1063,8 +1169,17 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
                 // the particle's own position is read again (an L1 / L2 hit) instead of being
                 // kept in registers across the row loop: 8 registers of slack there
                 float4 h = reload_f4(pos + i);
-                d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo,
-                                                   adv.vel, adv.image, adv.step, adv.ref_pos));
+                if (ADVANCE == 1 && adv.prune_mode) {                    // kernel-uniform
+                    float di;
+                    d2 = fmaxf(d2, advance_particle_pruned<2>(i, h, make_float4(fx, fy, fz, u),
+                                                              adv.pos_lo, adv.vel, adv.image,
+                                                              adv.step, adv.ref_pos, PRUNE, di));
+                    d2_inner = fmaxf(d2_inner, di);
+                } else {
+                    d2 = fmaxf(d2, advance_particle<2>(i, h, make_float4(fx, fy, fz, u),
+                                                       adv.pos_lo, adv.vel, adv.image, adv.step,
+                                                       adv.ref_pos));
+                }
                 adv.pos_out[i] = h;
                 if (ADVANCE == 2) {
 #pragma unroll
@@ -1084,6 +1199,8 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
         }
     }
     if (ADVANCE) advance_publish_disp<kPairThreads>(d2, s_max, status, adv);
+    if (ADVANCE == 1 && adv.prune_mode)
+        advance_publish_inner<kPairThreads>(d2_inner, s_max, status, adv);
 }
 
 // ---- block schedule of the pair kernel ---------------------------------------
@@ -1394,6 +1511,19 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
         } else {
             B2MD_LAUNCH_PAIR(true, false, false, 2);
         }
+    } else if (advance && adv.prune_mode == kPruneNow) {
+#define B2MD_LAUNCH_PRUNE(TABLE, SIG1)                                                        \
+    k_force_lj_pair<TABLE, false, SIG1, 1, true><<<blocks, kPairThreads, 0, s>>>(             \
+        (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
+        d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
+        ((flags & B2MD_FORCE_GATED) ? 1 : 0) | exp_bits, adv)
+        if (ntypes == 1) {
+            if (sig1) B2MD_LAUNCH_PRUNE(false, true);
+            else B2MD_LAUNCH_PRUNE(false, false);
+        } else {
+            B2MD_LAUNCH_PRUNE(true, false);
+        }
+#undef B2MD_LAUNCH_PRUNE
     } else if (advance) {
         if (ntypes == 1) {
             if (sig1) B2MD_LAUNCH_PAIR(false, false, true, 1);
@@ -1474,6 +1604,12 @@ int fill_advance(AdvanceArgs &adv, const void *d_pos_hi, void *d_pos_hi_out, voi
     adv.gate_out = gate_out_word;
     adv.halo_dst[0] = adv.halo_dst[1] = nullptr;
     adv.halo_out[0] = adv.halo_out[1] = nullptr;
+    adv.prune_mode = 0;
+    adv.gate_clear = 0;
+    adv.inner_nbr = nullptr;
+    adv.inner_counts = nullptr;
+    adv.inner_rl2 = adv.inner_half2 = adv.prune_limit2 = 0.0f;
+    adv.inner_tiles = 0;
     return 0;
 }
 
@@ -1621,6 +1757,48 @@ B2MD_EXPORT int b2md_force_lj_pairs_advance(
         d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, n, box, dt, d_ref_pos_f4, half_skin2,
         d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts, pitch, d_boundary, table, ntypes,
         flags, gate_in_word, gate_out_word, nullptr, nullptr, nullptr, nullptr, d_status, stream);
+}
+
+B2MD_EXPORT int b2md_force_lj_pairs_advance_pruned(
+    const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo, void *d_vel, void *d_image_i4,
+    int64_t n, const b2md_box *box, double dt, void *d_ref_pos_f4, double half_skin2,
+    const int32_t *d_pair_nbr, const int32_t *d_pair_counts, int64_t pair_pitch,
+    const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, const uint8_t *d_boundary,
+    const double *table, int32_t ntypes, int32_t flags, int32_t gate_in_word,
+    int32_t gate_out_word, int32_t gate_clear_word, int32_t prune_mode, int32_t *d_inner_nbr,
+    int32_t *d_inner_counts, int32_t pair_rows, double r_cut_max, double skin, double delta,
+    b2md_status *d_status, void *stream) {
+    AdvanceArgs adv;
+    int rc = fill_advance(adv, d_pos_hi, d_pos_hi_out, d_pos_lo, d_vel, d_image_i4, box, dt,
+                          d_ref_pos_f4, half_skin2, gate_in_word, gate_out_word,
+                          "b2md_force_lj_pairs_advance_pruned");
+    if (rc) return rc;
+    if (prune_mode < kPruneInner || prune_mode > kPruneOuter || !d_inner_nbr || !d_inner_counts ||
+        pair_rows < 4 || pair_rows % 4 != 0 || !(delta > 0.0) || !(delta < skin) ||
+        (uint64_t)(pair_rows / 4) * (uint64_t)pair_pitch >= 0xffffffffull ||
+        0.5 * (skin - delta) > 0.99 * kPruneRange || gate_clear_word == gate_in_word ||
+        gate_clear_word == gate_out_word || gate_clear_word < 0 || gate_clear_word >= 16 ||
+        gate_clear_word == kWordAdvanceCount || gate_clear_word == kWordInnerDisp ||
+        gate_in_word == kWordInnerDisp || gate_out_word == kWordInnerDisp) {
+        set_error("b2md_force_lj_pairs_advance_pruned: bad arguments (need 0 < delta < skin, "
+                  "(skin - delta) / 2 <= 0.126, three distinct gate words)");
+        return -1;
+    }
+    adv.prune_mode = prune_mode;
+    adv.gate_clear = gate_clear_word;
+    adv.inner_nbr = (int4 *)d_inner_nbr;
+    adv.inner_counts = d_inner_counts;
+    adv.inner_tiles = pair_rows / 4;
+    // keep what is inside r_cut + delta now (fp32 distance of the high words: a little wider)
+    adv.inner_rl2 = (float)((r_cut_max + delta) * (r_cut_max + delta) * (1.0 + 1e-5));
+    // expiry: some particle moved more than delta / 2 since the prune; the packed prune
+    // snapshot is off by up to kPruneStep / 2 per component
+    adv.inner_half2 = shaved_bound2(box, 0.5 * delta, 0.51 * kPruneStep);
+    // a prune is legal while the outer rows are complete to r_cut + delta
+    adv.prune_limit2 = shaved_bound2(box, 0.5 * (skin - delta), 0.0);
+    return launch_pairs(d_pos_hi, n, box, d_pair_nbr, d_pair_counts, pair_pitch, d_nbr, d_counts,
+                        pitch, d_boundary, table, ntypes, flags | B2MD_FORCE_SKIP_THERMO, nullptr,
+                        nullptr, d_status, &adv, stream, "b2md_force_lj_pairs_advance_pruned");
 }
 
 B2MD_EXPORT int b2md_force_lj_pairs_advance_halo(

@@ -4,6 +4,8 @@
 // (core.py:72-93), vv_finalize (integrate.py:73-79).
 #pragma once
 
+#include <string.h>
+
 #include "common.cuh"
 
 namespace b2md {
@@ -161,6 +163,97 @@ __device__ __forceinline__ float advance_particle(int64_t i, float4 &h, const fl
         d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
     }
     return d2;
+}
+
+// ---- pruned ("inner") pair rows of the step loop -------------------------------------------
+// The list snapshot's spare word (ref_pos.w) holds the particle's displacement from the list
+// snapshot AT THE LAST PRUNE, three 10-bit fixed-point components: the step kernel then knows
+// the displacement since the prune, (h - r) - u_prune, without a second snapshot array.
+// Range +-kPruneRange per component (a prune is only legal while every particle is within
+// (skin - delta) / 2 <= kPruneRange of its snapshot); the rounding error, <= kPruneStep / 2 per
+// component, comes off the expiry threshold (make_prune).
+constexpr float kPruneRange = 0.128f;
+constexpr float kPruneStep = kPruneRange / 511.0f;
+
+__device__ __forceinline__ float pack_disp(float ux, float uy, float uz) {
+    const float inv = 1.0f / kPruneStep;
+    const int qx = max(-511, min(511, __float2int_rn(ux * inv))) + 512;
+    const int qy = max(-511, min(511, __float2int_rn(uy * inv))) + 512;
+    const int qz = max(-511, min(511, __float2int_rn(uz * inv))) + 512;
+    return __int_as_float(qx | (qy << 10) | (qz << 20));
+}
+__device__ __forceinline__ void unpack_disp(float w, float &ux, float &uy, float &uz) {
+    const int b = __float_as_int(w);
+    ux = (float)((b & 1023) - 512) * kPruneStep;
+    uy = (float)(((b >> 10) & 1023) - 512) * kPruneStep;
+    uz = (float)(((b >> 20) & 1023) - 512) * kPruneStep;
+}
+inline float pack_disp_zero_host() {
+    const int b = 512 | (512 << 10) | (512 << 20);
+    float f;
+    memcpy(&f, &b, sizeof f);
+    return f;
+}
+
+// advance_particle for a step loop with pruned pair rows.  snapshot_now: this launch prunes --
+// the displacement of the INPUT position (h on entry) becomes the prune snapshot.  d2_inner
+// receives the squared displacement of the advanced position since the last prune.
+template <int KICKS>
+__device__ __forceinline__ float advance_particle_pruned(int64_t i, float4 &h, const float4 f,
+                                                         float4 *__restrict__ pos_lo,
+                                                         float4 *__restrict__ vel,
+                                                         int4 *__restrict__ image,
+                                                         const StepConst &c,
+                                                         float4 *__restrict__ ref_pos,
+                                                         bool snapshot_now, float &d2_inner) {
+    float4 r = ref_pos[i];
+    bool store_ref = false;
+    if (snapshot_now) {
+        r.w = pack_disp(h.x - r.x, h.y - r.y, h.z - r.z);
+        store_ref = true;
+    }
+    float4 v = vel[i];
+#pragma unroll
+    for (int k = 0; k < KICKS; ++k) kick(v, f, c.half_dt);
+    vel[i] = v;
+    float4 l = pos_lo[i];
+    drift(h.x, l.x, v.x, c.dt_hi, c.dt_lo);
+    drift(h.y, l.y, v.y, c.dt_hi, c.dt_lo);
+    drift(h.z, l.z, v.z, c.dt_hi, c.dt_lo);
+    const int kx = wrap_ds(h.x, l.x, c.L_hi[0], c.L_lo[0], c.invL[0]);
+    const int ky = wrap_ds(h.y, l.y, c.L_hi[1], c.L_lo[1], c.invL[1]);
+    const int kz = wrap_ds(h.z, l.z, c.L_hi[2], c.L_lo[2], c.invL[2]);
+    pos_lo[i] = l;
+    if ((kx | ky | kz) != 0) {
+        int4 im = image[i];
+        im.x += kx; im.y += ky; im.z += kz;
+        image[i] = im;
+        // keep (hi - ref) equal to the unwrapped displacement
+        r.x = fmaf(-(float)kx, c.L_hi[0], r.x);
+        r.y = fmaf(-(float)ky, c.L_hi[1], r.y);
+        r.z = fmaf(-(float)kz, c.L_hi[2], r.z);
+        store_ref = true;
+    }
+    if (store_ref) ref_pos[i] = r;
+    const float dx = h.x - r.x, dy = h.y - r.y, dz = h.z - r.z;
+    float ux, uy, uz;
+    unpack_disp(r.w, ux, uy, uz);
+    const float ex = dx - ux, ey = dy - uy, ez = dz - uz;
+    d2_inner = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+    return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+// The same never-fire-late shave as make_step's half_skin2, for an arbitrary displacement bound
+// `d` (plus `extra` of known error on the displacement itself).
+inline float shaved_bound2(const b2md_box *box, double d, double extra) {
+    double lmax = 0.0;
+    for (int a = 0; a < 3; ++a) lmax = box->edge[a] > lmax ? box->edge[a] : lmax;
+    int e = 0;
+    frexp(lmax, &e);
+    const double delta = 2.5 * ldexp(1.0, e - 24) + extra;
+    double shaved = d * d - (2.0 * 1.7320508075688772 * d * delta + 3.0 * delta * delta);
+    shaved *= 1.0 - 1e-6;
+    return shaved > 0.0 ? (float)shaved : 0.0f;
 }
 
 }  // namespace b2md

@@ -1028,7 +1028,9 @@ __global__ void k_snapshot(const float4 *__restrict__ pos_hi, const float4 *__re
         at_build[3 * i + 1] = __dadd_rn(ds_to_double(h.y, l.y), __dmul_rn((double)im.y, box.L[1]));
         at_build[3 * i + 2] = __dadd_rn(ds_to_double(h.z, l.z), __dmul_rn((double)im.z, box.L[2]));
     }
-    if (ref_pos) ref_pos[i] = make_float4(h.x, h.y, h.z, 0.f);
+    // w: "no displacement at the last prune" in the packing of integrate.cuh (pack_disp)
+    if (ref_pos)
+        ref_pos[i] = make_float4(h.x, h.y, h.z, __int_as_float(512 | (512 << 10) | (512 << 20)));
 }
 
 // Exact fp64 displacement maximum (neighbor.py:251-253).
@@ -1129,6 +1131,104 @@ k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
         for (int q = tiles; q < warp_tiles; ++q)
             out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
     if (t < pair_pitch && (!FIXUP || merge || !active)) pair_counts[t] = active ? total : 0;
+}
+
+// The marked pairs after k_list_cells_ballot<.., PAIRS> (pair_counts[t] < 0: rows 2t and 2t+1
+// sit in different cells or passes and went to the plain list), merged by a whole warp each:
+// k_pair_rows<true> walks the two rows entry by entry -- a chain of ~90 dependent loads that only
+// 6 % of the threads execute, 134 us at N = 1 M.  Here a warp takes 32 consecutive pairs and,
+// for every marked one, stages both rows in shared memory (independent loads), finds the merged
+// position of every element by binary search in the other row (an element of both rows is
+// emitted once, by row A, with both flags), and stores the entries; then all 32 rows are padded
+// to the warp's longest, exactly as k_pair_rows does.  Same bits.
+constexpr int kFixupWarps = 4;
+
+__global__ void __launch_bounds__(kFixupWarps * 32)
+k_pair_fixup(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
+             int list_rows, int64_t n_rows, int4 *__restrict__ pair_nbr,
+             int32_t *__restrict__ pair_counts, int64_t pair_pitch, int pair_tiles) {
+    extern __shared__ int32_t s_fix[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t *sa = s_fix + warp * (3 * list_rows + 1);      // row A, row B, duplicate prefix of A
+    int32_t *sb = sa + list_rows;
+    int32_t *sp = sb + list_rows;
+    const int64_t t0 = ((int64_t)blockIdx.x * kFixupWarps + warp) * 32;
+    const int64_t n_pairs = (n_rows + 1) >> 1;
+    if (t0 >= pair_pitch) return;
+    const int64_t t = t0 + lane;
+    const bool active = t < n_pairs;
+    int total = active ? pair_counts[t] : 0;
+    const unsigned marked = __ballot_sync(0xffffffffu, active && total < 0);
+    int32_t *flat = reinterpret_cast<int32_t *>(pair_nbr);
+    const int cap = pair_tiles * 4;
+    for (unsigned left = marked; left; left &= left - 1u) {
+        const int m_lane = __ffs(left) - 1;
+        const int64_t m = t0 + m_lane;
+        const int64_t a = 2 * m, b = 2 * m + 1;
+        const int ca = counts[a];
+        const int cb = b < n_rows ? counts[b] : 0;
+        __syncwarp();
+        for (int k = lane; k < ca; k += 32) sa[k] = nbr[(int64_t)k * pitch + a];
+        for (int k = lane; k < cb; k += 32) sb[k] = nbr[(int64_t)k * pitch + b];
+        __syncwarp();
+        // row A: position = k + (elements of B below x) - (common elements below x)
+        int dups = 0;
+        for (int k0 = 0; k0 < ca; k0 += 32) {                 // warp-uniform trip count
+            const int k = k0 + lane;
+            const bool in = k < ca;
+            const int x = in ? sa[k] : 0x7fffffff;
+            int lo = 0, hi = cb;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sb[mid] < x) lo = mid + 1; else hi = mid;
+            }
+            const bool dup = in && lo < cb && sb[lo] == x;
+            const unsigned dm = __ballot_sync(0xffffffffu, dup);
+            const int before = dups + __popc(dm & ((1u << lane) - 1u));
+            if (in) {
+                sp[k] = before;
+                const int pos = k + lo - before;
+                if (pos < cap)
+                    flat[((int64_t)(pos >> 2) * pair_pitch + m) * 4 + (pos & 3)] =
+                        (x << 2) | 1 | (dup ? 2 : 0);
+            }
+            dups += __popc(dm);
+        }
+        if (lane == 0) sp[ca] = dups;
+        __syncwarp();
+        // row B: elements that are not in A
+        for (int k0 = 0; k0 < cb; k0 += 32) {
+            const int k = k0 + lane;
+            const bool in = k < cb;
+            const int y = in ? sb[k] : 0x7fffffff;
+            int lo = 0, hi = ca;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sa[mid] < y) lo = mid + 1; else hi = mid;
+            }
+            const bool dup = in && lo < ca && sa[lo] == y;
+            if (in && !dup) {
+                const int pos = lo + k - sp[lo];
+                if (pos < cap)
+                    flat[((int64_t)(pos >> 2) * pair_pitch + m) * 4 + (pos & 3)] = (y << 2) | 2;
+            }
+        }
+        const int merged = ca + cb - dups;
+        // flag-less padding of the last tile
+        if (lane < ((4 - (merged & 3)) & 3)) {
+            const int pos = merged + lane;
+            if (pos < cap) flat[((int64_t)(pos >> 2) * pair_pitch + m) * 4 + (pos & 3)] = 0;
+        }
+        if (lane == m_lane) total = merged;
+    }
+    // pad to the warp's longest row
+    const int tiles = (total + 3) >> 2;
+    const int warp_tiles = min(__reduce_max_sync(0xffffffffu, tiles), pair_tiles);
+    int4 *out = pair_nbr + t;
+    if (t < pair_pitch) {
+        for (int q = tiles; q < warp_tiles; ++q) out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
+        if (!active || ((marked >> lane) & 1u)) pair_counts[t] = total;
+    }
 }
 
 }  // namespace b2md
@@ -1295,7 +1395,12 @@ B2MD_EXPORT int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo,
                         boundary_margin, n_rows, flags, d_status, stream, &po, &pairs_done);
     if (rc) return rc;
     const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
-    if (pairs_done)
+    const size_t fix_smem = (size_t)kFixupWarps * (3 * (size_t)list_rows + 1) * sizeof(int32_t);
+    if (pairs_done && fix_smem <= 48 * 1024 && env_choice("B2MD_PAIR_FIXUP", 1) != 0)
+        k_pair_fixup<<<blocks_for(pair_pitch / 32, kFixupWarps), kFixupWarps * 32, fix_smem,
+                       as_stream(stream)>>>(d_nbr, d_counts, pitch, list_rows, n_rows, po.pair_nbr,
+                                            d_pair_counts, pair_pitch, po.pair_tiles);
+    else if (pairs_done)
         k_pair_rows<true><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
                                                                  po.pair_nbr, d_pair_counts,
                                                                  pair_pitch, po.pair_tiles);

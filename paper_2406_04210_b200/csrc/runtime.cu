@@ -65,6 +65,13 @@ struct b2md_runner {
     bool ahead;               // positions already advanced to the step about to be processed
     int gate_in;              // status word holding the rebuild flag of those positions
     int count_seen;           // advance launches counted by the device so far (word 13)
+    // pruned pair rows (cfg.prune_delta > 0): what the next one-launch step may walk
+    bool prune_on;
+    int inner_state;          // kInnerNeedPrune / kInnerValid / kInnerOuterOnly
+    bool after_integrate;     // positions came from k_integrate: inner flags unknown for them
+    int steps_since_prune;
+    bool refreshed;           // the late refresh of this list's inner rows has been tried
+    int64_t prunes_total, outer_steps_total;
     // Andersen thermostat (second finalize slot of the reference, sim.py:86-87)
     double thermo_p, thermo_t;
     uint64_t thermo_seed;
@@ -141,6 +148,15 @@ int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
 constexpr int kWordRebuildFlag = 5;   // b2md_status::rebuild_flag
 constexpr int kWordAltFlag = 12;      // b2md_status::reserved[0]
 constexpr int kWordAdvanceCount = 13; // b2md_status::reserved[1]
+constexpr int kWordThirdFlag = 14;    // b2md_status::reserved[2]: pruned loops rotate three words
+constexpr int kInnerNeedPrune = 0, kInnerValid = 1, kInnerOuterOnly = 2;
+
+// Gate word after `w`: two words alternate in the plain loop; with pruned pair rows the flag
+// bits do not clear themselves, so three words rotate (b2md_force_lj_pairs_advance_pruned).
+int next_gate(const b2md_runner *r, int w) {
+    if (!r->prune_on) return w == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+    return w == kWordRebuildFlag ? kWordAltFlag : (w == kWordAltFlag ? kWordThirdFlag : kWordRebuildFlag);
+}
 
 bool thermostatted(const b2md_runner *r) { return r->thermo_p > 0.0; }
 
@@ -161,13 +177,20 @@ int canonicalize(b2md_runner *r) {
 
 // force(s) + finalize(s) + integrate(s+1) in one launch, gated on the rebuild flag of
 // the positions it reads; the advanced high words go to the other buffer.
-int launch_advance(b2md_runner *r) {
+int launch_advance(b2md_runner *r, int prune_mode = 0) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     void *in = r->pos_cur ? r->pos_cur : a.pos_hi;
     void *out = in == a.pos_hi ? c.pos_hi_alt : a.pos_hi;
-    const int gate_out = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+    const int gate_out = next_gate(r, r->gate_in);
     r->launches += 1;
+    if (prune_mode)
+        return b2md_force_lj_pairs_advance_pruned(
+            in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt, c.ref_pos, r->half_skin2,
+            c.pair_nbr, c.pair_counts, c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
+            r->table.data(), c.ntypes, c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0, r->gate_in,
+            gate_out, next_gate(r, gate_out), prune_mode, c.pair_nbr_inner, c.pair_counts_inner,
+            c.pair_rows, c.r_cut, c.skin, c.prune_delta, c.status, r->stream);
     if (c.pair_rows <= 0)
         return b2md_force_lj_advance(in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt,
                                      c.ref_pos, r->half_skin2, c.nbr, c.counts, c.pitch,
@@ -338,6 +361,9 @@ int rebuild(b2md_runner *r, b2md_run_report *rep) {
     r->list_valid = r->h_status->overflow == 0;
     r->pos_cur = live(r).pos_hi;      // callers hand over canonical positions; sets may swap
     r->count_seen = 0;                // the status reset of the rebuild cleared the counter
+    r->inner_state = kInnerNeedPrune; // new outer rows: the inner ones are void
+    r->after_integrate = false;       // (the list snapshot is these positions)
+    r->refreshed = false;
     return 0;
 }
 
@@ -493,6 +519,15 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     if (!r->ahead) {
         // positions of this step: integrate in place (canonical buffer)
         if ((rc = canonicalize(r))) return rc;
+        if (r->prune_on) {
+            // the gate rotation restarts at the rebuild-flag word: all three words clean
+            int32_t *w = reinterpret_cast<int32_t *>(c.status);
+            const int words[3] = {kWordRebuildFlag, kWordAltFlag, kWordThirdFlag};
+            for (int k = 0; k < 3; ++k)
+                if ((rc = check_cuda(cudaMemsetAsync(w + words[k], 0, sizeof(int32_t), s),
+                                     "gate reset"))) return rc;
+            r->after_integrate = true;
+        }
         if (r->pending_kick)
             rc = b2md_vv_finalize_integrate(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n,
                                             &c.box, c.dt, c.ref_pos, r->half_skin2, c.status, s);
@@ -521,7 +556,20 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     // already close to the threshold one step ago (a rebuild is likely and waiting a few
     // microseconds beats discarding a force evaluation).
     const bool speculate = fuse || r->last_disp2 < 0.85 * r->half_skin2;
-    if (fuse) rc = launch_advance(r);
+    int mode = 0;
+    if (fuse && r->prune_on) {
+        const double legal = 0.5 * (c.skin - c.prune_delta);
+        if (r->after_integrate || r->inner_state == kInnerOuterOnly) mode = B2MD_PRUNE_OUTER;
+        else if (r->inner_state == kInnerNeedPrune) mode = B2MD_PRUNE_NOW;
+        // refresh the inner rows while that is still legal: the last prune of a list's life
+        // should come as late as the outer rows allow
+        else if (!r->refreshed && r->steps_since_prune >= 3 &&
+                 r->last_disp2 > 0.78 * legal * legal && r->last_disp2 < 0.98 * legal * legal) {
+            mode = B2MD_PRUNE_NOW;
+            r->refreshed = true;
+        } else mode = B2MD_PRUNE_INNER;
+    }
+    if (fuse) rc = launch_advance(r, mode);
     else if (speculate) rc = launch_force(r, thermo);
     if (rc) return rc;
     if ((rc = check_cuda(cudaEventSynchronize(r->ev), "event sync"))) return rc;
@@ -555,7 +603,9 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
         *stop = 1;
         return 0;
     }
-    const bool need_rebuild = reinterpret_cast<const int32_t *>(r->h_status)[r->gate_in] != 0;
+    const int gate_word = reinterpret_cast<const int32_t *>(r->h_status)[r->gate_in];
+    // (pruned loops: bits 2 and 4 of the word are about the inner rows, see launch_advance)
+    const bool need_rebuild = r->prune_on ? (gate_word & 1) != 0 : gate_word != 0;
     if (need_rebuild) {
         if (!fuse && speculate) rep->wasted_force_launches += 1;   // (a gated launch did nothing)
         if ((rc = canonicalize(r))) return rc;
@@ -571,11 +621,39 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
             *stop = 1;
             return 0;
         }
-        if (fuse) rc = launch_advance(r);
-        else rc = launch_force(r, thermo);
+        if (fuse) {
+            mode = r->prune_on ? B2MD_PRUNE_NOW : 0;
+            rc = launch_advance(r, mode);
+        } else {
+            rc = launch_force(r, thermo);
+        }
         if (rc) return rc;
     } else if (!speculate) {
         if ((rc = launch_force(r, thermo))) return rc;
+    } else if (fuse && mode && ((mode == B2MD_PRUNE_INNER && (gate_word & 2)) ||
+                                (mode == B2MD_PRUNE_NOW && (gate_word & 4)))) {
+        // the launch found its rows stale (or the prune illegal), returned at once and copied
+        // the flags to its output word: clean that word and launch what the flags allow
+        if (mode == B2MD_PRUNE_NOW && !(gate_word & 2) && r->inner_state == kInnerValid)
+            mode = B2MD_PRUNE_INNER;                        // the refresh came too late: carry on
+        else if (!(gate_word & 4)) mode = B2MD_PRUNE_NOW;
+        else { mode = B2MD_PRUNE_OUTER; r->inner_state = kInnerOuterOnly; }
+        if ((rc = check_cuda(cudaMemsetAsync(reinterpret_cast<int32_t *>(c.status) +
+                                                 next_gate(r, r->gate_in), 0, sizeof(int32_t), s),
+                             "gate clean"))) return rc;
+        r->launches -= 1;                                   // (the gated launch did nothing)
+        if ((rc = launch_advance(r, mode))) return rc;
+    }
+    if (fuse && mode) {
+        if (mode == B2MD_PRUNE_NOW) {
+            r->inner_state = kInnerValid;
+            r->steps_since_prune = 0;
+            r->prunes_total += 1;
+        } else {
+            r->steps_since_prune += 1;
+            if (mode == B2MD_PRUNE_OUTER) r->outer_steps_total += 1;
+        }
+        r->after_integrate = false;
     }
     if (fuse) {
         // the launch advanced the particles to the next step: its output buffer and its
@@ -583,7 +661,7 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
         Set now = live(r);
         void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
         r->pos_cur = in == now.pos_hi ? c.pos_hi_alt : now.pos_hi;
-        r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+        r->gate_in = next_gate(r, r->gate_in);
         r->ahead = true;
         r->pending_kick = false;
         r->count_seen += 1;               // exactly one of this step's launches ran
@@ -601,7 +679,7 @@ void toggle_advance_state(b2md_runner *r) {
     Set now = live(r);
     void *in = r->pos_cur ? r->pos_cur : now.pos_hi;
     r->pos_cur = in == now.pos_hi ? r->cfg.pos_hi_alt : now.pos_hi;
-    r->gate_in = r->gate_in == kWordRebuildFlag ? kWordAltFlag : kWordRebuildFlag;
+    r->gate_in = next_gate(r, r->gate_in);
 }
 
 // Up to `n_inter` intermediate steps as queued one-launch steps, several per status
@@ -835,6 +913,15 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->gate_in = kWordRebuildFlag;
     r->count_seen = 0;
     if (r->cfg.queue_depth < 1) r->cfg.queue_depth = 1;
+    r->prune_on = cfg->prune_delta > 0.0 && cfg->prune_delta < cfg->skin &&
+                  0.5 * (cfg->skin - cfg->prune_delta) <= 0.125 && cfg->pair_rows > 0 &&
+                  cfg->pair_nbr_inner && cfg->pair_counts_inner && cfg->pos_hi_alt &&
+                  cfg->use_graph == 0 && r->cfg.queue_depth == 1;
+    r->inner_state = kInnerNeedPrune;
+    r->after_integrate = false;
+    r->steps_since_prune = 0;
+    r->refreshed = false;
+    r->prunes_total = r->outer_steps_total = 0;
     r->own_h_status = r->own_stream = r->own_copy_stream = true;
     r->thermo_p = 0.0;
     r->thermo_t = 1.0;
@@ -911,6 +998,23 @@ B2MD_EXPORT int b2md_runner_set_pair_list(b2md_runner *r, int32_t *pair_nbr, int
     r->list_valid = false;
     destroy_graph(r);
     return 0;
+}
+
+B2MD_EXPORT int b2md_runner_set_inner_pair_list(b2md_runner *r, int32_t *pair_nbr_inner) {
+    if (!r || (r->prune_on && !pair_nbr_inner)) {
+        set_error("b2md_runner_set_inner_pair_list: bad arguments");
+        return -1;
+    }
+    r->cfg.pair_nbr_inner = pair_nbr_inner;
+    r->inner_state = kInnerNeedPrune;
+    r->list_valid = false;
+    return 0;
+}
+
+B2MD_EXPORT int64_t b2md_runner_prune_count(const b2md_runner *r, int64_t *outer_steps) {
+    if (!r) return -1;
+    if (outer_steps) *outer_steps = r->outer_steps_total;
+    return r->prunes_total;
 }
 
 B2MD_EXPORT int b2md_runner_set_thermostat(b2md_runner *r, double probability,

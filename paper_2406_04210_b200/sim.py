@@ -72,7 +72,8 @@ class Simulation:
                  reorder_every: int = 1, native: bool | None = None,
                  stride_policy: str = "fit", graph: int | bool = False,
                  pair_rows: bool | None = None, advance: bool | None = None,
-                 queue_depth: int | None = None, persistent_steps: int | None = None):
+                 queue_depth: int | None = None, persistent_steps: int | None = None,
+                 prune_delta: float | None = None):
         if force_mode not in FORCE_MODES:
             raise ConfigError(f"unknown force_mode {force_mode!r}")
         if force_mode == TRUNCATED and not lj.truncated:
@@ -116,6 +117,20 @@ class Simulation:
         # (b2md_steps_persistent; 0 = one gated launch per step).  Bit-identical trajectories.
         self.persistent_steps = int(os.environ.get("B2MD_PERSISTENT_STEPS", "256")) \
             if persistent_steps is None else int(persistent_steps)
+        # Pruned pair rows for the one-launch steps: rows cut to r_cut + prune_delta, re-pruned
+        # from the full list rows whenever a particle has moved prune_delta / 2 (the full rows
+        # keep the reference's rebuild schedule, neighbor.py:243-254; dropped entries would
+        # have contributed exact zeros, so trajectories are bit-identical).  Off by default
+        # (None / 0): measured at N = 1 M, skin 0.3, delta 0.1, a step over the inner rows takes
+        # 97 us instead of 109, but each of the three prune launches per list costs 209 us (the
+        # per-entry compaction doubles the instructions of the issue-bound loop) -- 0.1418 against
+        # 0.1425 ms per step, inside the noise (profiles/README.md).
+        if prune_delta is None:
+            env = os.environ.get("B2MD_PRUNE_DELTA")
+            prune_delta = float(env) if env not in (None, "") else 0.0
+        # (legal prunes need every particle within (skin - delta) / 2 <= 0.125 of the snapshot)
+        self.prune_delta = float(prune_delta) if (0.0 < prune_delta < self.skin and
+                                                  0.5 * (self.skin - prune_delta) <= 0.125) else 0.0
         self.graph_steps = 0
         # (a thermostatted native loop launches integrate / force / finalize / thermostat
         # separately: the thermostat is the reference's second finalize slot, sim.py:86-87)
@@ -336,6 +351,14 @@ class Simulation:
             cfg.pair_schedule = 0 if os.environ.get("B2MD_PAIR_SCHEDULE") == "0" else 1
             cfg.pair_nbr = k["pair_nbr"].data_ptr()
             cfg.pair_counts = k["pair_counts"].data_ptr()
+            if self.prune_delta > 0.0 and self.advance and not self.graph and \
+                    max(self.queue_depth, 1) == 1:
+                # pruned ("inner") pair rows for the one-launch steps
+                k["pair_nbr_inner"] = torch.zeros_like(k["pair_nbr"])
+                k["pair_counts_inner"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
+                cfg.pair_nbr_inner = k["pair_nbr_inner"].data_ptr()
+                cfg.pair_counts_inner = k["pair_counts_inner"].data_ptr()
+                cfg.prune_delta = self.prune_delta
         # page-locked status mirror and the runner's two streams come from torch's caching
         # host allocator / stream pool: creating them per runner costs 1-7 ms of driver calls
         k["h_status"] = torch.empty(16, dtype=torch.int32).pin_memory()
@@ -401,6 +424,10 @@ class Simulation:
                     _lib.call("b2md_runner_set_pair_list", self._runner,
                               self._keep["pair_nbr"].data_ptr(), rows2)
                     self._keep["cfg"].pair_rows = rows2
+                    if "pair_nbr_inner" in self._keep:
+                        self._keep["pair_nbr_inner"] = _torch().zeros_like(self._keep["pair_nbr"])
+                        _lib.call("b2md_runner_set_inner_pair_list", self._runner,
+                                  self._keep["pair_nbr_inner"].data_ptr())
                 continue
             return
 
@@ -468,6 +495,14 @@ class Simulation:
             pressure=t.pressure(self.box.volume),
             com_velocity=t.com_velocity,
         )
+
+    def prune_stats(self):
+        """(prune launches, one-launch steps that walked the full rows) of the native loop."""
+        if not self.native or not getattr(self, "_runner", None):
+            return 0, 0
+        outer = ctypes.c_int64(0)
+        prunes = _lib.load().b2md_runner_prune_count(self._runner, ctypes.byref(outer))
+        return int(prunes), int(outer.value)
 
     def reset_counters(self):
         """Zero phase timers, overflow events and the rebuild baseline."""
