@@ -163,9 +163,10 @@ int b2md_build_nlist_ex(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
  * With B2MD_LIST_ANY_PREFIX and a cell-contiguous particle order (after b2md_gather_rows by
  * Hilbert / cell keys) the list kernel emits the merged rows of particles 2t, 2t+1 straight
  * from its per-cell decision masks, and only the pairs whose two particles sit in different
- * cells go through the plain rows and the merge -- d_nbr then holds valid rows for THOSE
- * particles only (d_counts, d_boundary and the status words are complete).  Otherwise it is
- * b2md_build_nlist_ex followed by b2md_pair_rows.  The pair rows are bit-identical either way.
+ * cells go through plain rows and a merge -- d_nbr is then SCRATCH (it holds the rows of those
+ * particles only, row-major: row i at d_nbr + i * list_rows); d_counts, d_boundary and the
+ * status words are complete.  Otherwise it is b2md_build_nlist_ex followed by b2md_pair_rows
+ * (and d_nbr holds the full column-major list).  The pair rows are bit-identical either way.
  * list_rows: allocated rows of d_nbr (>= stride); pair_rows >= 2 * list_rows. */
 int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo, int64_t n,
                          const b2md_box *box, const b2md_grid *grid,

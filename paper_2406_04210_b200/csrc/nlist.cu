@@ -466,19 +466,22 @@ __host__ __device__ inline size_t ballot_warp_bytes() {
 
 // Ascending order of one row of the column-major list, in place (neighbor.py:152);
 // insertion sort: the callers' rows are nearly sorted.
-__device__ __forceinline__ void sort_row_in_list(int32_t *__restrict__ nbr, int64_t pitch, int i,
-                                                 int kept) {
+__device__ __forceinline__ void sort_row_strided(int32_t *__restrict__ row, int64_t step, int kept) {
     for (int a = 1; a < kept; ++a) {
-        const int v = nbr[(int64_t)a * pitch + i];
+        const int v = row[(int64_t)a * step];
         int b = a - 1;
         while (b >= 0) {
-            const int w = nbr[(int64_t)b * pitch + i];
+            const int w = row[(int64_t)b * step];
             if (w <= v) break;
-            nbr[(int64_t)(b + 1) * pitch + i] = w;
+            row[(int64_t)(b + 1) * step] = w;
             --b;
         }
-        if (b + 1 != a) nbr[(int64_t)(b + 1) * pitch + i] = v;
+        if (b + 1 != a) row[(int64_t)(b + 1) * step] = v;
     }
+}
+__device__ __forceinline__ void sort_row_in_list(int32_t *__restrict__ nbr, int64_t pitch, int i,
+                                                 int kept) {
+    sort_row_strided(nbr + i, pitch, kept);
 }
 
 // One particle's row straight into the column-major list in the reference's scan
@@ -566,13 +569,16 @@ __device__ __forceinline__ void seek_rank(const uint32_t *ma, const uint32_t *mb
 // its merged row by RANK into runs of whole int4 tiles (a lane seeks to its first entry through
 // the population counts of the mask words), so they are balanced and tile-aligned by
 // construction.  Rows whose partner lives in another cell or pass ("single" rows) are dealt to
-// the lanes the same way and stored as plain rows; k_pair_rows<true> merges those afterwards
-// and pads every pair row to the longest row of its force-kernel warp.
+// the lanes the same way and stored as plain rows -- ROW-major in this mode (row i at nbr +
+// i * list_rows: 6 % of the rows, scattered over the whole list, would otherwise be one DRAM
+// sector per entry for the merge that follows); k_pair_fixup merges those afterwards and pads
+// every pair row to the longest row of its force-kernel warp.
 struct PairOut {
     int4 *pair_nbr;
     int32_t *pair_counts;
     int64_t pair_pitch;
     int pair_tiles;
+    int list_rows;      // PAIRS: single rows are stored ROW-major, row i at nbr + i * list_rows
 };
 
 template <int WARPS, bool PAIRS>
@@ -781,6 +787,8 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                         s_mask[lane * kMaskPitch + (self >> 5)] &= ~(1u << (self & 31));
                 }
                 if (PAIRS) {
+                    __syncwarp();      // the masks are read by other lanes than the row's own
+
                     // rows of this batch counted from their masks (counts[], overflow)
                     if (active) {
                         const uint32_t *mr = s_mask + lane * kMaskPitch;
@@ -875,7 +883,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                         uint32_t um = 0u;
                         seek_rank(mr, mr, n_chunks, k0, w, um);
                         const int32_t *ps = s_stream + w * 32;
-                        int32_t *pr = nbr + (int64_t)rank * pitch + b_i;
+                        int32_t *pr = nbr + (int64_t)b_i * po.list_rows + rank;
                         while (__any_sync(0xffffffffu, left > 0)) {
 #pragma unroll
                             for (int rep = 0; rep < 2; ++rep) {
@@ -889,7 +897,7 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
                                 um &= um - 1u;
                                 const int j = ps[bit] & 0x03ffffff;
                                 if (has && rank < (unsigned)stride) *pr = j;
-                                pr += has ? pitch : 0;
+                                pr += has ? 1 : 0;
                                 rank += has ? 1u : 0u;
                                 left -= has ? 1 : 0;
                             }
@@ -969,7 +977,8 @@ k_list_cells_ballot(const float4 *__restrict__ pos_hi, const float4 *__restrict_
             // particle order not cell-contiguous (never after a reorder; ghost rows of a
             // slab are appended unsorted): rows came out in stream order -- ascending
             // inside every cell, cells by first occupant -- so they are nearly sorted
-            sort_row_in_list(nbr, pitch, i, min(found, stride));
+            if (PAIRS) sort_row_strided(nbr + (int64_t)i * po.list_rows, 1, min(found, stride));
+            else sort_row_in_list(nbr, pitch, i, min(found, stride));
         }
         if (active) {
             counts[i] = min(found, stride);
@@ -1076,10 +1085,6 @@ __global__ void k_max_disp(const float4 *__restrict__ pos_hi, const float4 *__re
 // and trip fetches four entries and a warp reads 512 contiguous bytes.  Rows are
 // padded with flag-less entries (j = 0) up to the longest row of the warp, so the
 // force kernel needs no per-entry bound check.
-// FIXUP (after k_list_cells_ballot<.., PAIRS>): only the pairs that kernel left marked
-// (pair_counts[t] < 0: the two rows were not neighbours in one pass of one cell and went to the
-// plain list) are merged; every row is then padded to the longest row of its warp.
-template <bool FIXUP>
 __global__ void __launch_bounds__(128)
 k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts, int64_t pitch,
             int64_t n_rows, int4 *__restrict__ pair_nbr, int32_t *__restrict__ pair_counts,
@@ -1087,60 +1092,50 @@ k_pair_rows(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts,
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t n_pairs = (n_rows + 1) >> 1;
     const bool active = t < n_pairs;
+    const int64_t a = 2 * t, b = 2 * t + 1;
+    const int ca = active ? counts[a] : 0;
+    const int cb = (active && b < n_rows) ? counts[b] : 0;
+    const int32_t *ra = nbr + a, *rb = nbr + b;
+    constexpr int kEnd = 0x7fffffff;
+    int ia = 0, ib = 0;
+    int va = ca > 0 ? ra[0] : kEnd;
+    int vb = cb > 0 ? rb[0] : kEnd;
+    int e0 = 0, e1 = 0, e2 = 0, e3 = 0, k = 0;
     int4 *out = pair_nbr + t;
-    int total = 0, k = 0;
-    bool merge = active;
-    if (FIXUP && active) {
-        total = pair_counts[t];
-        merge = total < 0;
-        k = (total + 3) & ~3;
-    }
-    if (merge) {
-        const int64_t a = 2 * t, b = 2 * t + 1;
-        const int ca = counts[a];
-        const int cb = b < n_rows ? counts[b] : 0;
-        const int32_t *ra = nbr + a, *rb = nbr + b;
-        constexpr int kEnd = 0x7fffffff;
-        int ia = 0, ib = 0;
-        int va = ca > 0 ? ra[0] : kEnd;
-        int vb = cb > 0 ? rb[0] : kEnd;
-        int e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-        k = 0;
-        const int cap = pair_tiles * 4;
-        while (va != kEnd || vb != kEnd) {
-            const int m = min(va, vb);
-            const bool from_a = va == m, from_b = vb == m;
-            const int e = (m << 2) | (from_a ? 1 : 0) | (from_b ? 2 : 0);
-            if (from_a) { ++ia; va = ia < ca ? ra[(int64_t)ia * pitch] : kEnd; }
-            if (from_b) { ++ib; vb = ib < cb ? rb[(int64_t)ib * pitch] : kEnd; }
-            e0 = e1; e1 = e2; e2 = e3; e3 = e;
-            ++k;
-            if ((k & 3) == 0 && k <= cap)
-                out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
-        }
-        total = k;                             // <= ca + cb <= capacity by construction
-        // flush the partial tile (flag-less padding entries)
-        while (k & 3) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; ++k; }
-        if (k > total && k <= cap)
+    const int cap = pair_tiles * 4;
+    while (va != kEnd || vb != kEnd) {
+        const int m = min(va, vb);
+        const bool from_a = va == m, from_b = vb == m;
+        const int e = (m << 2) | (from_a ? 1 : 0) | (from_b ? 2 : 0);
+        if (from_a) { ++ia; va = ia < ca ? ra[(int64_t)ia * pitch] : kEnd; }
+        if (from_b) { ++ib; vb = ib < cb ? rb[(int64_t)ib * pitch] : kEnd; }
+        e0 = e1; e1 = e2; e2 = e3; e3 = e;
+        ++k;
+        if ((k & 3) == 0 && k <= cap)
             out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
     }
-    // pad to the warp's longest row
+    const int total = k;                       // <= ca + cb <= capacity by construction
+    // flush the partial tile, then pad to the warp's longest row (flag-less entries)
+    while (k & 3) { e0 = e1; e1 = e2; e2 = e3; e3 = 0; ++k; }
+    if (k > total && k <= cap)
+        out[(int64_t)((k >> 2) - 1) * pair_pitch] = make_int4(e0, e1, e2, e3);
     const int tiles = k >> 2;
-    const int warp_tiles = min(__reduce_max_sync(0xffffffffu, tiles), pair_tiles);
+    const int warp_tiles = __reduce_max_sync(0xffffffffu, tiles);
     if (t < pair_pitch)
         for (int q = tiles; q < warp_tiles; ++q)
             out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
-    if (t < pair_pitch && (!FIXUP || merge || !active)) pair_counts[t] = active ? total : 0;
+    if (t < pair_pitch) pair_counts[t] = active ? total : 0;
 }
 
 // The marked pairs after k_list_cells_ballot<.., PAIRS> (pair_counts[t] < 0: rows 2t and 2t+1
-// sit in different cells or passes and went to the plain list), merged by a whole warp each:
-// k_pair_rows<true> walks the two rows entry by entry -- a chain of ~90 dependent loads that only
-// 6 % of the threads execute, 134 us at N = 1 M.  Here a warp takes 32 consecutive pairs and,
-// for every marked one, stages both rows in shared memory (independent loads), finds the merged
-// position of every element by binary search in the other row (an element of both rows is
-// emitted once, by row A, with both flags), and stores the entries; then all 32 rows are padded
-// to the warp's longest, exactly as k_pair_rows does.  Same bits.
+// sit in different cells or passes and went to the plain list, row-major), merged by a whole
+// warp each.  (One thread per pair walking the two rows entry by entry, as k_pair_rows does, is
+// a chain of ~90 dependent loads that only 6 % of the threads execute: 134 us at N = 1 M.)
+// A warp takes 32 consecutive pairs and, for every marked one, stages both rows in shared
+// memory (coalesced loads), finds the merged position of every element by binary search in the
+// other row (an element of both rows is emitted once, by row A, with both flags), and stores
+// the entries; then all 32 rows are padded to the warp's longest, exactly as k_pair_rows does.
+// Same bits.
 constexpr int kFixupWarps = 4;
 
 __global__ void __launch_bounds__(kFixupWarps * 32)
@@ -1168,8 +1163,8 @@ k_pair_fixup(const int32_t *__restrict__ nbr, const int32_t *__restrict__ counts
         const int ca = counts[a];
         const int cb = b < n_rows ? counts[b] : 0;
         __syncwarp();
-        for (int k = lane; k < ca; k += 32) sa[k] = nbr[(int64_t)k * pitch + a];
-        for (int k = lane; k < cb; k += 32) sb[k] = nbr[(int64_t)k * pitch + b];
+        for (int k = lane; k < ca; k += 32) sa[k] = nbr[a * list_rows + k];      // row-major
+        for (int k = lane; k < cb; k += 32) sb[k] = nbr[b * list_rows + k];
         __syncwarp();
         // row A: position = k + (elements of B below x) - (common elements below x)
         int dups = 0;
@@ -1303,7 +1298,8 @@ int build_list(const void *d_pos_hi, const void *d_pos_lo, int64_t n, const b2md
         constexpr int kBallotWarps = 8;
         const int64_t nc = grid->n_cells;
         const size_t smem = ballot_warp_bytes() * kBallotWarps;
-        if (pairs && (flags & B2MD_LIST_ANY_PREFIX) && env_choice("B2MD_LIST_PAIRS", 1) != 0) {
+        if (pairs && (flags & B2MD_LIST_ANY_PREFIX) && env_choice("B2MD_LIST_PAIRS", 1) != 0 &&
+            (size_t)kFixupWarps * (3 * (size_t)pairs->list_rows + 1) * sizeof(int32_t) <= 48 * 1024) {
             cudaFuncSetAttribute(k_list_cells_ballot<kBallotWarps, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             // every pair starts out marked "merge from the plain rows"
@@ -1388,7 +1384,7 @@ B2MD_EXPORT int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo,
                   "pair_rows a multiple of 4 >= 2 * list_rows, list_rows >= stride");
         return -6;
     }
-    const PairOut po = {(int4 *)d_pair_nbr, d_pair_counts, pair_pitch, pair_rows / 4};
+    const PairOut po = {(int4 *)d_pair_nbr, d_pair_counts, pair_pitch, pair_rows / 4, list_rows};
     bool pairs_done = false;
     int rc = build_list(d_pos_hi, d_pos_lo, n, box, grid, d_cell_of, d_cell_start,
                         d_cell_particles, r_list, stride, pitch, d_nbr, d_counts, d_boundary,
@@ -1396,16 +1392,12 @@ B2MD_EXPORT int b2md_build_pair_list(const void *d_pos_hi, const void *d_pos_lo,
     if (rc) return rc;
     const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
     const size_t fix_smem = (size_t)kFixupWarps * (3 * (size_t)list_rows + 1) * sizeof(int32_t);
-    if (pairs_done && fix_smem <= 48 * 1024 && env_choice("B2MD_PAIR_FIXUP", 1) != 0)
+    if (pairs_done)
         k_pair_fixup<<<blocks_for(pair_pitch / 32, kFixupWarps), kFixupWarps * 32, fix_smem,
                        as_stream(stream)>>>(d_nbr, d_counts, pitch, list_rows, n_rows, po.pair_nbr,
                                             d_pair_counts, pair_pitch, po.pair_tiles);
-    else if (pairs_done)
-        k_pair_rows<true><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
-                                                                 po.pair_nbr, d_pair_counts,
-                                                                 pair_pitch, po.pair_tiles);
     else
-        k_pair_rows<false><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+        k_pair_rows<<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
                                                                   po.pair_nbr, d_pair_counts,
                                                                   pair_pitch, po.pair_tiles);
     B2MD_CHECK_LAUNCH("b2md_build_pair_list");
@@ -1463,7 +1455,7 @@ B2MD_EXPORT int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, in
     }
     // whole warps only: the padding loop uses a warp reduction
     const unsigned blocks = blocks_for((n_pairs + 31) / 32 * 32, 128);
-    k_pair_rows<false><<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
+    k_pair_rows<<<blocks, 128, 0, as_stream(stream)>>>(d_nbr, d_counts, pitch, n_rows,
                                                               (int4 *)d_pair_nbr, d_pair_counts,
                                                               pair_pitch, pair_rows / 4);
     B2MD_CHECK_LAUNCH("b2md_pair_rows");

@@ -29,6 +29,7 @@ print("KE", b2.kinetic_energy_and_temperature(st))
 # native loops
 variants = [dict(pair_rows=False), dict(pair_rows=True, advance=True),
             dict(pair_rows=True, advance=True, queue_depth=8),
+            dict(pair_rows=True, advance=True, prune_delta=0.1),      # pruned pair rows
             dict(thermostat=b2.ThermostatParams(1.2, 20.0, 7))]
 if os.environ.get("SAN_GRAPH") == "1":      # CUDA-graph steps (conditional IF nodes) only
     variants = [dict(graph=4)]

@@ -65,8 +65,9 @@ def compare(st, box, r_list, stride, skin, expect_fused_fraction=None):
     tiles = min(got["pair_nbr"].shape[0], d_pair.shape[0])
     assert torch.equal(got["pair_nbr"][:tiles], d_pair[:tiles])
     assert not got["pair_nbr"][tiles:].any() and not d_pair[tiles:].any()
-    # plain rows: either the reference's row, or untouched (the pair was emitted directly)
-    rows = got["nbr"][:nl.stride, :n].t().cpu().numpy()
+    # plain rows (row-major in this mode: row i at nbr + i * list_rows): either the reference's
+    # row, or untouched (the pair was emitted directly)
+    rows = got["nbr"].reshape(-1)[:n * got["rows"]].reshape(n, got["rows"]).cpu().numpy()
     ref = nl.indices
     cnt = nl.counts
     touched = (rows != -7).any(axis=1)
@@ -138,8 +139,8 @@ def test_fused_build_with_many_particles_per_cell():
     assert torch.equal(got["counts"], counts)
     assert torch.equal(got["pair_counts"], pair_counts)
     assert torch.equal(got["pair_nbr"], pair_nbr)
-    touched = (got["nbr"][:, :n] != -7).any(dim=0).float().mean().item()
-    assert touched < 0.2
+    touched = (got["nbr"].reshape(-1)[:n * got["rows"]].reshape(n, got["rows"]) != -7).any(dim=1)
+    assert touched.float().mean().item() < 0.2
 
 
 def test_fused_build_flags_overflow_and_reports_the_longest_row():
