@@ -189,10 +189,11 @@ def test_fused_build_leaves_ghost_rows_alone():
     assert torch.equal(got["pair_nbr"], pair_nbr)
 
 
-def test_native_loop_is_bit_identical_with_either_list_build(monkeypatch):
+@pytest.mark.parametrize("n,steps", [(262_144, 120), (1_000_000, 80)])
+def test_native_loop_is_bit_identical_with_either_list_build(monkeypatch, n, steps):
     """Whole trajectories: the runner with b2md_build_pair_list (default) and with the
-    two-stage build (B2MD_LIST_PAIRS=0) produce the same bits."""
-    n = 262_144
+    two-stage build (B2MD_LIST_PAIRS=0) produce the same bits -- also at the benchmark's size
+    (39^3 cells, 500 000 pair rows)."""
     out = []
     for mode in ("1", "0"):
         monkeypatch.setenv("B2MD_LIST_PAIRS", mode)
@@ -202,7 +203,7 @@ def test_native_loop_is_bit_identical_with_either_list_build(monkeypatch):
                             force_mode=b2.TRUNCATED, skin=0.3, sample_interval=40,
                             sample_initial=True, reorder="hilbert")
         assert sim.pair_rows
-        sim.run(120)
+        sim.run(steps)
         out.append((np.array([s.total_energy for s in sim.samples]),
                     np.array(st.positions.acquire_read(b2.HOST)),
                     np.array(st.velocities.acquire_read(b2.HOST)), sim.rebuild_count))
