@@ -455,6 +455,7 @@ def run_gpu_arm(args):
 
         rebin()
         launch_list_fused()                       # into pair_rows_alt (fresh, zero-filled)
+        k["nbr"].zero_()                          # the row kernel below reads padding entries
         launch_list_plain()                       # leaves complete per-particle rows
         pair_rows_ref = torch.zeros_like(k["pair_nbr"])
         pair_counts_ref = torch.zeros_like(k["pair_counts"])

@@ -257,8 +257,11 @@ class Simulation:
         # (64-row granules let the persistent step kernel of small systems put 16 lanes on a
         # particle: a trip of it reads 4 x 16 entries of a row)
         rows = _round_up(self._stride, self._row_multiple())
-        # zero-filled: padding entries must stay valid row indices
-        return torch.zeros((rows, pitch), dtype=torch.int32, device=dev.device), pitch
+        # zero-filled: padding entries must stay valid row indices for the row kernels.  With
+        # pair rows the step loop never reads a padding entry of this buffer (it is the list
+        # build's scratch, b2md_build_pair_list): no fill -- 65 us of HBM writes at N = 1 M
+        make = torch.empty if self.pair_rows else torch.zeros
+        return make((rows, pitch), dtype=torch.int32, device=dev.device), pitch
 
     def _row_multiple(self) -> int:
         return 64 if self.state.n < 200_000 else 16
@@ -268,7 +271,9 @@ class Simulation:
         torch = _torch()
         rows = _round_up(self._stride, self._row_multiple())
         pair_pitch = _round_up((dev.n + 1) // 2, 32)
-        return (torch.zeros((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
+        # (no fill: every tile a launch reads -- up to the longest row of its warp -- is written
+        # by the list build first)
+        return (torch.empty((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
                             device=dev.device), pair_pitch, 2 * rows)
 
     def _native_setup(self):
@@ -288,19 +293,21 @@ class Simulation:
         k["current"] = 0
         k["nbr"], pitch = self._alloc_list(dev)
         k["pitch"] = pitch
+        # (buffers below that every rebuild writes in full before anything reads them are not
+        # zero-filled: Simulation() is inside the timed end-to-end call)
         k["counts"] = torch.zeros(pitch, dtype=torch.int32, **d)
         k["boundary"] = torch.zeros(pitch, dtype=torch.uint8, **d)
-        k["ref_pos"] = torch.zeros((pitch, 4), dtype=torch.float32, **d)
-        k["at_build"] = torch.zeros((n, 3), dtype=torch.float64, **d)
-        k["cell_of"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["ref_pos"] = torch.empty((pitch, 4), dtype=torch.float32, **d)
+        k["at_build"] = torch.empty((n, 3), dtype=torch.float64, **d)
+        k["cell_of"] = torch.empty(n, dtype=torch.int32, **d)
         k["cell_start"] = torch.zeros(int(g.n_cells) + 1, dtype=torch.int32, **d)
-        k["cell_particles"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["cell_particles"] = torch.empty(n, dtype=torch.int32, **d)
         k["bin_scratch"] = torch.zeros(int(lib.b2md_bin_scratch_bytes(n, g.n_cells)),
                                        dtype=torch.uint8, **d)
-        k["keys"] = torch.zeros(n, dtype=torch.int64, **d)
-        k["keys_tmp"] = torch.zeros(n, dtype=torch.int64, **d)
-        k["perm"] = torch.zeros(n, dtype=torch.int32, **d)
-        k["perm_tmp"] = torch.zeros(n, dtype=torch.int32, **d)
+        k["keys"] = torch.empty(n, dtype=torch.int64, **d)
+        k["keys_tmp"] = torch.empty(n, dtype=torch.int64, **d)
+        k["perm"] = torch.empty(n, dtype=torch.int32, **d)
+        k["perm_tmp"] = torch.empty(n, dtype=torch.int32, **d)
         k["sort_scratch"] = torch.zeros(int(lib.b2md_sort_scratch_bytes(n)), dtype=torch.uint8, **d)
         k["table"] = np.ascontiguousarray(self.lj.table(), dtype=np.float64)
         if self.lj.ntypes > 1:
@@ -334,7 +341,7 @@ class Simulation:
         if self.advance and not self.graph:
             # second buffer for the position high words: intermediate steps then run as one
             # launch each (force + finalize + integrate, b2md_force_lj[_pairs]_advance)
-            k["pos_hi_alt"] = torch.zeros_like(dev.pos_hi)
+            k["pos_hi_alt"] = torch.empty_like(dev.pos_hi)
             cfg.pos_hi_alt = k["pos_hi_alt"].data_ptr()
             cfg.queue_depth = max(self.queue_depth, 1)
         cfg.list_row_multiple = self._row_multiple()
@@ -354,7 +361,7 @@ class Simulation:
             if self.prune_delta > 0.0 and self.advance and not self.graph and \
                     max(self.queue_depth, 1) == 1:
                 # pruned ("inner") pair rows for the one-launch steps
-                k["pair_nbr_inner"] = torch.zeros_like(k["pair_nbr"])
+                k["pair_nbr_inner"] = torch.empty_like(k["pair_nbr"])
                 k["pair_counts_inner"] = torch.zeros(cfg.pair_pitch, dtype=torch.int32, **d)
                 cfg.pair_nbr_inner = k["pair_nbr_inner"].data_ptr()
                 cfg.pair_counts_inner = k["pair_counts_inner"].data_ptr()
@@ -425,7 +432,7 @@ class Simulation:
                               self._keep["pair_nbr"].data_ptr(), rows2)
                     self._keep["cfg"].pair_rows = rows2
                     if "pair_nbr_inner" in self._keep:
-                        self._keep["pair_nbr_inner"] = _torch().zeros_like(self._keep["pair_nbr"])
+                        self._keep["pair_nbr_inner"] = _torch().empty_like(self._keep["pair_nbr"])
                         _lib.call("b2md_runner_set_inner_pair_list", self._runner,
                                   self._keep["pair_nbr_inner"].data_ptr())
                 continue
