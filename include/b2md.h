@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 104
+#define B2MD_VERSION 105
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -575,6 +575,12 @@ typedef struct b2md_runner_config {
     int32_t *pair_nbr_inner;
     int32_t *pair_counts_inner;
     double prune_delta;
+    /* Optional cudaEvent_t: the velocities (vel[current]) are still being written by work on
+     * another stream (an upload from host memory) that this event follows.  The first list
+     * build (b2md_runner_prepare) then touches positions and images only, and waits for the
+     * event -- and brings the velocities into the new row order -- behind it, so that the
+     * upload overlaps the build.  NULL: everything is ordered by `stream` as usual. */
+    void *vel_ready_event;
 } b2md_runner_config;
 
 enum { B2MD_RUN_DONE = 0, B2MD_RUN_OVERFLOW = 1, B2MD_RUN_SINGULAR = 2 };

@@ -73,6 +73,7 @@ class RunnerConfig(Structure):
         ("persistent_steps", c_int32), ("list_row_multiple", c_int32), ("barrier", c_void_p),
         ("h_status", c_void_p), ("run_stream", c_void_p), ("copy_stream", c_void_p),
         ("pair_nbr_inner", c_void_p), ("pair_counts_inner", c_void_p), ("prune_delta", c_double),
+        ("vel_ready_event", c_void_p),
     ]
 
 

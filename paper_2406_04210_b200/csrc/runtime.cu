@@ -65,6 +65,9 @@ struct b2md_runner {
     bool ahead;               // positions already advanced to the step about to be processed
     int gate_in;              // status word holding the rebuild flag of those positions
     int count_seen;           // advance launches counted by the device so far (word 13)
+    // velocities uploaded on a side stream (cfg.vel_ready_event): the first build gathers
+    // them last, behind the list build, so that the upload overlaps it
+    bool defer_vel, vel_waited;
     // pruned pair rows (cfg.prune_delta > 0): what the next one-launch step may walk
     bool prune_on;
     int inner_state;          // kInnerNeedPrune / kInnerValid / kInnerOuterOnly
@@ -237,12 +240,20 @@ int enqueue_reorder(b2md_runner *r, bool write_back, int64_t *kernels) {
     if ((rc = b2md_sort_pairs_u64(c.keys, c.perm, c.keys_tmp, c.perm_tmp, c.n, key_bits,
                                   c.sort_scratch, s))) return rc;
     *kernels += 2 + ((key_bits + 7) / 8) * (2 + scan_launches(256 * ((c.n + 1023) / 1024)));
-    {
+    if (r->defer_vel && !write_back) {
+        // first build of a runner whose velocities are still arriving over PCIe: only what
+        // the list build needs now; enqueue_rebuild gathers the velocities behind it (forces
+        // and virial hold nothing yet: b2md_runner_prepare evaluates them on the new rows)
+        if ((rc = b2md_gather16(a.pos_hi, b.pos_hi, c.perm, c.n, s))) return rc;
+        if ((rc = b2md_gather16(a.pos_lo, b.pos_lo, c.perm, c.n, s))) return rc;
+        if ((rc = b2md_gather16(a.image, b.image, c.perm, c.n, s))) return rc;
+        *kernels += 3;
+    } else {
         const void *src[5] = {a.pos_hi, a.pos_lo, a.vel, a.force, a.image};
         void *dst[5] = {b.pos_hi, b.pos_lo, b.vel, b.force, b.image};
         if ((rc = b2md_gather_rows(src, dst, a.virial, b.virial, c.perm, c.n, s))) return rc;
+        *kernels += 1;
     }
-    *kernels += 1;
     if (write_back) {
         const size_t row = 16 * (size_t)c.n;
         void *dst[5] = {a.pos_hi, a.pos_lo, a.vel, a.force, a.image};
@@ -295,6 +306,18 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
                 return rc;
             *kernels += 2;
         }
+    }
+    if (r->defer_vel && !write_back) {
+        // the velocities: wait for their upload, then bring them into the new row order
+        if ((rc = check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(c.vel_ready_event), 0),
+                             "velocity upload wait"))) return rc;
+        if (do_reorder) {
+            Set now = live(r), old = spare(r);         // (enqueue_reorder swapped the sets)
+            if ((rc = b2md_gather16(old.vel, now.vel, c.perm, c.n, s))) return rc;
+            *kernels += 1;
+        }
+        r->defer_vel = false;
+        r->vel_waited = true;
     }
     return 0;
 }
@@ -913,6 +936,8 @@ B2MD_EXPORT b2md_runner *b2md_runner_create(const b2md_runner_config *cfg) {
     r->gate_in = kWordRebuildFlag;
     r->count_seen = 0;
     if (r->cfg.queue_depth < 1) r->cfg.queue_depth = 1;
+    r->defer_vel = false;
+    r->vel_waited = cfg->vel_ready_event == nullptr;
     r->prune_on = cfg->prune_delta > 0.0 && cfg->prune_delta < cfg->skin &&
                   0.5 * (cfg->skin - cfg->prune_delta) <= 0.125 && cfg->pair_rows > 0 &&
                   cfg->pair_nbr_inner && cfg->pair_counts_inner && cfg->pos_hi_alt &&
@@ -1051,7 +1076,16 @@ B2MD_EXPORT int b2md_runner_prepare(b2md_runner *r, b2md_run_report *rep) {
     int rc = order_after_caller(r);
     if (rc) return rc;
     if ((rc = begin_call(r))) return rc;
+    r->defer_vel = !r->vel_waited && r->cfg.use_graph == 0;
     if ((rc = rebuild(r, rep))) return rc;
+    if (!r->vel_waited) {
+        // (a path that did not gather: graph mode keeps the row order inside this call)
+        if ((rc = check_cuda(cudaStreamWaitEvent(r->stream,
+                                                 static_cast<cudaEvent_t>(r->cfg.vel_ready_event), 0),
+                             "velocity upload wait"))) return rc;
+        r->defer_vel = false;
+        r->vel_waited = true;
+    }
     if (!r->list_valid) {
         rep->reason = B2MD_RUN_OVERFLOW;
         finish_report(r, rep, before);

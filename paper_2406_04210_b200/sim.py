@@ -276,9 +276,38 @@ class Simulation:
         return (torch.empty((2 * rows // 4, pair_pitch, 4), dtype=torch.int32,
                             device=dev.device), pair_pitch, 2 * rows)
 
+    def _upload_state(self, k):
+        """Make every buffer valid on the device.  Velocities that still have to cross PCIe go
+        last and on a side stream: the first list build needs positions only, so the runner
+        is told to wait for them behind it (b2md_runner_config::vel_ready_event) and the
+        upload overlaps the build.  Returns the event, or None."""
+        torch = _torch()
+        st = self.state
+        vel = st.velocities
+        dev = st.device_state()
+        if vel.valid_on in (COMPUTE, "both") or self.graph:
+            st.sync_to_compute()
+            return None
+        for name, buf in st.buffers().items():
+            if name != "velocities":
+                buf.acquire_read(COMPUTE)
+        main = torch.cuda.current_stream(dev.device)
+        side = k["copy_stream"]
+        side.wait_stream(main)                  # (the device rows exist and hold their defaults)
+        with torch.cuda.stream(side):
+            vel.acquire_read(COMPUTE)
+        k["vel_ready"] = torch.cuda.Event()
+        k["vel_ready"].record(side)
+        return k["vel_ready"]
+
     def _native_setup(self):
         torch = _torch()
-        dev = self.state.sync_to_compute()
+        k = self._keep
+        dev0 = self.state.device_state()
+        k["run_stream"] = torch.cuda.Stream(device=dev0.device)
+        k["copy_stream"] = torch.cuda.Stream(device=dev0.device)
+        vel_ready = self._upload_state(k)
+        dev = self.state.device_state()
         n = dev.n
         r_list = self.lj.max_r_cut + self.skin
         g = grid_shape(self.box, r_list)
@@ -369,9 +398,9 @@ class Simulation:
         # page-locked status mirror and the runner's two streams come from torch's caching
         # host allocator / stream pool: creating them per runner costs 1-7 ms of driver calls
         k["h_status"] = torch.empty(16, dtype=torch.int32).pin_memory()
-        k["run_stream"] = torch.cuda.Stream(device=dev.device)
-        k["copy_stream"] = torch.cuda.Stream(device=dev.device)
         cfg.h_status = k["h_status"].data_ptr()
+        if vel_ready is not None:
+            cfg.vel_ready_event = vel_ready.cuda_event
         cfg.run_stream = k["run_stream"].cuda_stream
         cfg.copy_stream = k["copy_stream"].cuda_stream
         k["cfg"] = cfg
@@ -386,6 +415,9 @@ class Simulation:
                       float(self.thermostat.redraw_probability(self.integrator.dt)),
                       float(self.thermostat.temperature), int(self.thermostat.seed) % (1 << 64))
         self._native_call("b2md_runner_prepare")
+        if vel_ready is not None:
+            # anything the caller enqueues on its own stream from here on sees the velocities
+            torch.cuda.current_stream(dev.device).wait_stream(k["copy_stream"])
 
     def _native_call(self, name, *args):
         """Invoke the runner, handling overflow (grow + resume) and singular pairs."""

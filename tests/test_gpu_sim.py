@@ -315,3 +315,28 @@ def test_orthorhombic_box_and_unequal_masses_track_the_oracle():
     d = unwrapped - (osim.pos + osim.images * edges)
     assert np.max(np.abs(d)) < 5e-3                         # trajectories still together
     sim.close()
+
+
+@pytest.mark.parametrize("n", [4096, 262_144])
+def test_velocity_upload_on_the_side_stream_changes_nothing(n):
+    """Simulation() uploads velocities that are still on the host on a side stream and lets the
+    runner wait for them behind the first list build (b2md_runner_config::vel_ready_event);
+    a state whose velocities are already on the device takes the plain path.  Same bits."""
+    out = []
+    for presync in (False, True):
+        st, box = b2.init_lattice_any(n, 0.75)
+        b2.init_velocities(st, 1.2, 42)
+        if presync:
+            st.sync_to_compute()
+        sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0, 2.5), 0.001,
+                            force_mode=b2.TRUNCATED, skin=0.3, sample_interval=20,
+                            sample_initial=True, reorder="hilbert")
+        assert ("vel_ready" in sim._keep) == (not presync)
+        sim.run(60)
+        out.append((np.array([s.total_energy for s in sim.samples]),
+                    np.array([s.kinetic_energy for s in sim.samples]),
+                    np.array(st.positions.acquire_read(b2.HOST)),
+                    np.array(st.velocities.acquire_read(b2.HOST))))
+        sim.close()
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
