@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 105
+#define B2MD_VERSION 106
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -205,6 +205,7 @@ int b2md_max_displacement(const void *d_pos_hi, const void *d_pos_lo, const void
 #define B2MD_FORCE_GATED 2        /* return at once when d_status->frozen is set */
 #define B2MD_FORCE_SCHEDULED 4    /* pair kernels: d_pair_counts[pair_pitch ...] holds the block
                                      schedule written by b2md_pair_schedule */
+#define B2MD_FORCE_ORDERED 8      /* pair kernels: follow the lane order of b2md_pair_order */
 int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *box,
                   const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch,
                   int32_t stride, const uint8_t *d_boundary, const double *table, int32_t ntypes,
@@ -257,6 +258,21 @@ int b2md_steps_persistent(void *d_pos_a, void *d_pos_b, void *d_pos_lo, void *d_
 int64_t b2md_pair_schedule_len(int64_t n);
 int b2md_pair_schedule(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_counts,
                        int64_t pair_pitch, void *stream);
+
+/* Lane order of the pair kernels (optional; no reference counterpart -- it changes which thread
+ * evaluates the row of forces.py:72-110, not the row).  A warp of the pair kernel walks as many
+ * tiles as its longest row has.  b2md_pair_order sorts the pairs of every 128-thread block by
+ * row length (stable, in units of `unit` adjacent pairs: 1, 2, 4 ...; with face_key the pairs
+ * that may need an image shift sort behind the others) and writes, behind the block schedule
+ * (the buffer size b2md_pair_schedule_len(n) covers it), which pair of the block each thread
+ * takes; rows are padded to the longest row of their new warp.  Launches that pass
+ * B2MD_FORCE_ORDERED follow it; launches that do not remain legal on the same rows.  Per-particle
+ * sums do not depend on the order (a thread owns its pair's row and walks it in ascending
+ * order either way).  Call it after the pair rows are complete (b2md_pair_rows /
+ * b2md_build_pair_list); d_boundary may be NULL when face_key is 0. */
+int b2md_pair_order(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_nbr,
+                    int32_t *d_pair_counts, int64_t pair_pitch, int32_t pair_rows, int32_t unit,
+                    int32_t face_key, void *stream);
 
 int b2md_pair_rows(const int32_t *d_nbr, const int32_t *d_counts, int64_t pitch, int32_t stride,
                    int64_t n_rows, int32_t *d_pair_nbr, int32_t *d_pair_counts,
@@ -551,8 +567,10 @@ typedef struct b2md_runner_config {
     int32_t queue_depth;         /* one-launch steps queued per status read-back (>= 1); small
                                     systems, whose step is shorter than a host round trip,
                                     want several */
-    int32_t pair_schedule;       /* != 0: pair_counts has b2md_pair_schedule_len(n) more entries;
-                                    the runner keeps a block schedule there (see above) */
+    int32_t pair_schedule;       /* != 0: pair_counts has b2md_pair_schedule_len(n) more entries.
+                                    bit 0: the runner keeps a block schedule there (see above);
+                                    bit 1: and a lane order (b2md_pair_order), bit 2 its face_key,
+                                    bits 8-13 its unit (0 = 1) */
     int32_t persistent_steps;    /* > 0: intermediate steps of systems without pair rows run in
                                     batches of up to this many steps per launch of
                                     b2md_steps_persistent (needs pos_hi_alt, barrier and

@@ -145,6 +145,7 @@ _SIGNATURES = {
                                         c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
     "b2md_pair_schedule_len": (c_int64, [c_int64]),
     "b2md_pair_schedule": (c_int32, [_P, c_int64, _P, c_int64, _P]),
+    "b2md_pair_order": (c_int32, [_P, c_int64, _P, _P, c_int64, c_int32, c_int32, c_int32, _P]),
     "b2md_force_lj_pairs": (c_int32, [_P, c_int64, POINTER(Box), _P, _P, c_int64, _P, _P, c_int64,
                                       _P, POINTER(c_double), c_int32, c_int32, _P, _P, _P, _P]),
     "b2md_force_lj_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, POINTER(Box), c_double, _P,

@@ -75,6 +75,7 @@ struct ForceArgs {
     PairParams single;
     int ntypes;
     const int32_t *schedule;    // pair kernel: block executed by blockIdx.x (null = identity)
+    const uint8_t *order;       // pair kernel: pair of the block taken by threadIdx.x (null = identity)
     float4 tab_a[kMaxTypes * kMaxTypes];   // sig2, rc2, c_f, c_u
     float2 tab_b[kMaxTypes * kMaxTypes];   // half_shift, c_w
 };
@@ -1055,7 +1056,12 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     // 1.7x longer; dispatched last (the space-filling curve ends on a face of the box) they
     // were the tail of the launch -- 10 us of 118 at N = 1 M.  The schedule runs them first.
     const unsigned bid = a.schedule ? (unsigned)__ldg(a.schedule + blockIdx.x) : blockIdx.x;
-    const int64_t t_raw = bid * (int64_t)blockDim.x + threadIdx.x;
+    // Lane order (b2md_pair_order): a warp pays for its longest row, 27.7 tiles where the mean
+    // row has 23.3; with the pairs of a block dealt to its warps by row length the warps walk
+    // 24.6.  A thread still owns one pair and walks its row in ascending order: same sums.
+    const unsigned slot = a.order ? (unsigned)a.order[bid * (unsigned)kPairThreads + threadIdx.x]
+                                  : threadIdx.x;
+    const int64_t t_raw = bid * (int64_t)blockDim.x + slot;
     const bool active = t_raw < n_pairs;
     const int64_t t = active ? t_raw : n_pairs - 1;
     const int64_t ia = 2 * t;
@@ -1252,6 +1258,67 @@ k_pair_schedule(const int32_t *__restrict__ flags, int n_blocks, int32_t *__rest
     }
 }
 
+
+// ---- lane order of the pair kernel --------------------------------------------
+// A warp of the pair kernel walks as many tiles as its longest row has.  In particle order
+// that is 27.7 tiles in the molten fluid at N = 1 M against a mean row of 23.3 (row lengths
+// within a block scatter by +-1.6 tiles).  k_pair_order sorts the kPairThreads pairs of every
+// block by row length (stable; in units of `unit` adjacent pairs, so that a unit of 2 keeps
+// 32-byte sectors of the index stream inside one warp) and stores order[block][slot] = pair of
+// the block that thread `slot` takes; warps then hold rows of similar length: 24.6 tiles.
+// With face_key, pairs that may need an image shift (boundary bits 0-2) sort behind all the
+// others, so that the shuffle does not spread them over more warps than before.  Every row is
+// padded (flag-less entries) to the longest row of its NEW warp.  The padding that
+// k_pair_rows / k_pair_fixup wrote for the particle-order warps stays, so launches without
+// B2MD_FORCE_ORDERED remain legal on the same rows.
+__global__ void __launch_bounds__(kPairThreads)
+k_pair_order(const uint8_t *__restrict__ boundary, int64_t n, int4 *__restrict__ pair_nbr,
+             const int32_t *__restrict__ pair_counts, int64_t pair_pitch, int pair_tiles,
+             int unit, int face_key, uint8_t *__restrict__ order) {
+    __shared__ int s_key[kPairThreads];
+    __shared__ int s_tiles[kPairThreads];       // by slot
+    __shared__ int s_gmax[kPairThreads / 32];
+    __shared__ uint8_t s_order[kPairThreads];
+    const int s = threadIdx.x;
+    const int64_t n_pairs = (n + 1) >> 1;
+    const int64_t t = blockIdx.x * (int64_t)kPairThreads + s;
+    const bool active = t < n_pairs;
+    const int tiles = active ? min((pair_counts[t] + 3) >> 2, pair_tiles) : 0;
+    int key = tiles;
+    if (face_key && active && boundary) {
+        const int64_t ia = 2 * t, ib = min(ia + 1, n - 1);
+        if ((boundary[ia] | boundary[ib]) & 7) key |= 1 << 16;
+    }
+    s_key[s] = key;
+    __syncthreads();
+    const int u = s / unit, n_units = kPairThreads / unit;
+    int ku = 0;
+    for (int k = 0; k < unit; ++k) ku = max(ku, s_key[u * unit + k]);
+    int rank = 0;
+    for (int v = 0; v < n_units; ++v) {
+        int kv = 0;
+        for (int k = 0; k < unit; ++k) kv = max(kv, s_key[v * unit + k]);
+        rank += (kv < ku) || (kv == ku && v < u);
+    }
+    const int slot = rank * unit + s % unit;
+    s_order[slot] = (uint8_t)s;
+    s_tiles[slot] = tiles;
+    __syncthreads();
+    const int g = __reduce_max_sync(0xffffffffu, s_tiles[s]);
+    if ((s & 31) == 0) s_gmax[s >> 5] = g;
+    order[blockIdx.x * (int64_t)kPairThreads + s] = s_order[s];
+    __syncthreads();
+    if (active) {
+        int to = s_gmax[slot >> 5];
+        // the idle threads behind the last pair read ITS row (k_force_lj_pair clamps t), for as
+        // many tiles as their own warp walks
+        if (t == n_pairs - 1)
+            for (int w = 0; w < kPairThreads / 32; ++w) to = max(to, s_gmax[w]);
+        int4 *out = pair_nbr + t;
+        for (int q = tiles; q < to; ++q) out[(int64_t)q * pair_pitch] = make_int4(0, 0, 0, 0);
+    }
+}
+
 // ---- all pairs (reference _all_to_all_chunk, forces.py:29-69) --------------------
 // The paper's primary benchmark is N = 2000: one thread per particle is 16 blocks on 148 SMs.
 // A thread-block CLUSTER of kAllPairsSplit blocks therefore shares one block of 128 particles
@@ -1370,6 +1437,7 @@ static int fill_args(ForceArgs &a, const b2md_box *box, const double *table, int
     a.box = make_box_f(box);
     a.ntypes = ntypes;
     a.schedule = nullptr;
+    a.order = nullptr;
     for (int t = 0; t < ntypes * ntypes; ++t) {
         const double eps = table[4 * t], sig2 = table[4 * t + 1], rc2 = table[4 * t + 2],
                      shift = table[4 * t + 3];
@@ -1497,6 +1565,8 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     const unsigned blocks = blocks_for((n + 1) / 2, kPairThreads);
     const bool sig1 = a.single.sig2 == 1.0f;
     if (flags & B2MD_FORCE_SCHEDULED) a.schedule = d_pair_counts + pair_pitch;
+    if (flags & B2MD_FORCE_ORDERED)
+        a.order = reinterpret_cast<const uint8_t *>(d_pair_counts + pair_pitch + 2 * (int64_t)blocks);
     // profiles/exp only: B2MD_EXP_NO_BOUNDARY=1 -> no image shifts anywhere (wrong forces at the
     // faces), B2MD_EXP_VARIANT=v -> every warp runs image-shift variant v
     const int exp_variant = env_choice("B2MD_EXP_VARIANT", -1);
@@ -1547,7 +1617,25 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
 }  // namespace
 
 B2MD_EXPORT int64_t b2md_pair_schedule_len(int64_t n) {
-    return 2 * (int64_t)blocks_for((n + 1) / 2, kPairThreads);    // the schedule + its flag scratch
+    // the schedule + its flag scratch + the lane order (one byte per thread of the pair kernel)
+    return (2 + kPairThreads / 4) * (int64_t)blocks_for((n + 1) / 2, kPairThreads);
+}
+
+B2MD_EXPORT int b2md_pair_order(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_nbr,
+                                int32_t *d_pair_counts, int64_t pair_pitch, int32_t pair_rows,
+                                int32_t unit, int32_t face_key, void *stream) {
+    if (n <= 0 || !d_pair_nbr || !d_pair_counts || pair_pitch < (n + 1) / 2 || pair_rows % 4 != 0 ||
+        unit < 1 || unit > 32 || (unit & (unit - 1)) != 0) {
+        set_error("b2md_pair_order: bad arguments (unit must be a power of two <= 32)");
+        return -1;
+    }
+    const int64_t n_blocks = blocks_for((n + 1) / 2, kPairThreads);
+    uint8_t *order = reinterpret_cast<uint8_t *>(d_pair_counts + pair_pitch + 2 * n_blocks);
+    k_pair_order<<<(unsigned)n_blocks, kPairThreads, 0, as_stream(stream)>>>(
+        d_boundary, n, (int4 *)d_pair_nbr, d_pair_counts, pair_pitch, pair_rows / 4, unit,
+        face_key ? 1 : 0, order);
+    B2MD_CHECK_LAUNCH("b2md_pair_order");
+    return 0;
 }
 
 B2MD_EXPORT int b2md_pair_schedule(const uint8_t *d_boundary, int64_t n, int32_t *d_pair_counts,

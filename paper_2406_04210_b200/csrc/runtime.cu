@@ -131,13 +131,20 @@ int read_status(b2md_runner *r) {
     return check_cuda(cudaStreamSynchronize(r->stream), "status sync");
 }
 
+// b2md_runner_config::pair_schedule: bit 0 block schedule, bit 1 lane order
+int pair_flags(const b2md_runner_config &c) {
+    if (c.pair_rows <= 0) return 0;
+    return ((c.pair_schedule & 1) ? B2MD_FORCE_SCHEDULED : 0) |
+           ((c.pair_schedule & 2) ? B2MD_FORCE_ORDERED : 0);
+}
+
 // thermo = false on steps whose per-particle energies cannot be observed
 int launch_force(b2md_runner *r, bool thermo, bool gated = false) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
     r->launches += 1;
     const int flags = (thermo ? 0 : B2MD_FORCE_SKIP_THERMO) | (gated ? B2MD_FORCE_GATED : 0) |
-                      (c.pair_rows > 0 && c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0);
+                      pair_flags(c);
     if (c.pair_rows > 0)
         return b2md_force_lj_pairs(a.pos_hi, c.n, &c.box, c.pair_nbr, c.pair_counts,
                                    c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
@@ -191,7 +198,7 @@ int launch_advance(b2md_runner *r, int prune_mode = 0) {
         return b2md_force_lj_pairs_advance_pruned(
             in, out, a.pos_lo, a.vel, a.image, c.n, &c.box, c.dt, c.ref_pos, r->half_skin2,
             c.pair_nbr, c.pair_counts, c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
-            r->table.data(), c.ntypes, c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0, r->gate_in,
+            r->table.data(), c.ntypes, pair_flags(c), r->gate_in,
             gate_out, next_gate(r, gate_out), prune_mode, c.pair_nbr_inner, c.pair_counts_inner,
             c.pair_rows, c.r_cut, c.skin, c.prune_delta, c.status, r->stream);
     if (c.pair_rows <= 0)
@@ -203,7 +210,7 @@ int launch_advance(b2md_runner *r, int prune_mode = 0) {
                                        c.ref_pos, r->half_skin2, c.pair_nbr, c.pair_counts,
                                        c.pair_pitch, c.nbr, c.counts, c.pitch, c.boundary,
                                        r->table.data(), c.ntypes,
-                                       c.pair_schedule ? B2MD_FORCE_SCHEDULED : 0, r->gate_in,
+                                       pair_flags(c), r->gate_in,
                                        gate_out, c.status, r->stream);
 }
 
@@ -301,10 +308,17 @@ int enqueue_rebuild(b2md_runner *r, bool do_reorder, bool write_back, int64_t *k
     *kernels += 1 + 3 + scan_launches(r->grid.n_cells) + 2 + 1;
     if (c.pair_rows > 0) {
         *kernels += 1;
-        if (c.pair_schedule) {
+        if (c.pair_schedule & 1) {
             if ((rc = b2md_pair_schedule(c.boundary, c.n, c.pair_counts, c.pair_pitch, s)))
                 return rc;
             *kernels += 2;
+        }
+        if (c.pair_schedule & 2) {
+            const int unit = (c.pair_schedule >> 8) & 63;
+            if ((rc = b2md_pair_order(c.boundary, c.n, c.pair_nbr, c.pair_counts, c.pair_pitch,
+                                      c.pair_rows, unit ? unit : 1, (c.pair_schedule >> 2) & 1, s)))
+                return rc;
+            *kernels += 1;
         }
     }
     if (r->defer_vel && !write_back) {

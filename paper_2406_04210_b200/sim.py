@@ -384,7 +384,9 @@ class Simulation:
             # pair counts, then the block schedule of the pair kernel (b2md_pair_schedule)
             k["pair_counts"] = torch.zeros(
                 cfg.pair_pitch + int(lib.b2md_pair_schedule_len(n)), dtype=torch.int32, **d)
-            cfg.pair_schedule = 0 if os.environ.get("B2MD_PAIR_SCHEDULE") == "0" else 1
+            # bit 0: block schedule, bit 1: lane order (b2md_pair_order), bit 2: its face key,
+            # bits 8-13: its unit
+            cfg.pair_schedule = int(os.environ.get("B2MD_PAIR_SCHEDULE", "1"))
             cfg.pair_nbr = k["pair_nbr"].data_ptr()
             cfg.pair_counts = k["pair_counts"].data_ptr()
             if self.prune_delta > 0.0 and self.advance and not self.graph and \
