@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 106
+#define B2MD_VERSION 107
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -656,6 +656,28 @@ int b2md_runner_set_thermostat(b2md_runner *r, double probability, double temper
                                uint64_t seed);
 /* Step counter (SignalEngine.step_count) of the first step of the next b2md_runner_run. */
 int b2md_runner_set_step(b2md_runner *r, int64_t first_step);
+
+/* ------------------------------------------------- native loop, all-to-all forces
+ * Simulation.run with force_mode = "all_to_all", the reference's default (sim.py:62-102:
+ * integrate -> compute_forces_all_to_all -> finalize [-> andersen_thermostat] per step,
+ * core.py:262-279 for the loop).  n_steps MD steps are enqueued on `stream` without a host
+ * round trip per step -- there is no list and no rebuild decision; finalize of step s and
+ * integrate of step s + 1 share one pass over the state unless the thermostat sits between
+ * them -- and the status block is read back every 512 steps and at the end.  Same kernels
+ * and order of operations as the operator-by-operator loop: bit-identical trajectories.
+ * On return the velocities carry both half-kicks and d_force_f4 / d_virial hold the forces,
+ * per-particle energies and virial of the final positions.  thermo_probability = min(rate *
+ * dt, 1), 0 = no thermostat; first_step = SignalEngine.step_count before the call (index of
+ * the thermostat stream).  h_status: 64 bytes of page-locked host memory.  A coincident
+ * pair (forces.py:113-116) ends the call with report->reason = B2MD_RUN_SINGULAR and the
+ * pair in report->singular; the state is then not meaningful.  Only steps_done, reason,
+ * kernel_launches, singular and gpu_ms of the report are filled. */
+int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, void *d_force_f4,
+                       void *d_image_i4, float *d_virial, int64_t n, const b2md_box *box,
+                       const double *table, int32_t ntypes, double dt, int64_t n_steps,
+                       double thermo_probability, double thermo_temperature,
+                       uint64_t thermo_seed, int64_t first_step, b2md_status *d_status,
+                       void *h_status, void *stream, b2md_run_report *report);
 
 #ifdef __cplusplus
 }

@@ -1327,12 +1327,57 @@ k_pair_order(const uint8_t *__restrict__ boundary, int64_t n, int4 *__restrict__
 // distributed shared memory by block 0 of the cluster in the fixed order r = 0 .. S-1 -- no
 // atomics, no scratch buffer, bitwise reproducible.
 constexpr int kAllPairsSplit = 8;           // portable cluster size
+// below these sizes: k_force_all_pairs_small with 8 / 4 warps per tile of 32 particles
+constexpr int64_t kAllPairsEightWarps = 12288, kAllPairsFourWarps = 65536;
 
+// `zeros` = partners at zero distance.  A particle meets itself exactly once (identical
+// coordinates give an exact zero), so a total other than 1 means a coincident pair: the rare
+// slow path (all_pairs_report_singular) then finds the partner.  Cheaper than telling "self"
+// from "singular" for every pair: one predicate and one add instead of 64-bit index compares.
 struct AllPairsPartial {
     float fx, fy, fz, u, w;
     int cnt;
-    long long first_bad;
+    int zeros;
+    int pad;
 };
+
+// forces.py:113-116 for the all-pairs kernels: lowest j != i at zero distance from particle i.
+__device__ __noinline__ void all_pairs_report_singular(int i, const float4 pi,
+                                                       const float4 *__restrict__ pos, int n,
+                                                       const BoxF &b, b2md_status *status) {
+    for (int j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const float4 pj = pos[j];
+        const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+        const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+        const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+        if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) == 0.0f) {
+            atomicMin((unsigned long long *)&status->singular,
+                      ((unsigned long long)(unsigned)i << 32) | (unsigned)j);
+            return;
+        }
+    }
+}
+
+// One pair of the all-pairs scan (forces.py:41-66): the pair contributes iff r2 != 0.
+template <bool TABLE>
+__device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const float4 pi,
+                                                const float4 pj, const BoxF &b,
+                                                const ForceArgs &a, const float4 *s_tab_a,
+                                                const float2 *s_tab_b, int ti_row) {
+    const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
+    const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
+    const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    const bool valid = r2 != 0.0f;
+    zeros += valid ? 0 : 1;
+    if (TABLE) {
+        const int tt = ti_row + __float_as_int(pj.w);
+        lj_pair_table<true>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
+    } else {
+        lj_pair_single<true>(acc, dx, dy, dz, r2, valid, a.single);
+    }
+}
 
 template <bool TABLE>
 __global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(kForceThreads)
@@ -1357,57 +1402,41 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
     const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
     const BoxF &b = a.box;
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
-    long long first_bad = -1;
-    for (int64_t base = (int64_t)rank * kForceThreads; base < n;
-         base += (int64_t)kAllPairsSplit * kForceThreads) {
+    int zeros = 0;
+    const int ni = (int)n;                       // (row indices are 32-bit everywhere)
+    for (int base = (int)rank * kForceThreads; base < ni; base += kAllPairsSplit * kForceThreads) {
         __syncthreads();
-        const int64_t jl = base + threadIdx.x;
-        tile[threadIdx.x] = pos[jl < n ? jl : n - 1];
+        const int jl = base + (int)threadIdx.x;
+        tile[threadIdx.x] = pos[jl < ni ? jl : ni - 1];
         __syncthreads();
-        const int lim = (int)min((int64_t)kForceThreads, n - base);
+        const int lim = min(kForceThreads, ni - base);
 #pragma unroll 4
-        for (int t = 0; t < lim; ++t) {
-            const float4 pj = tile[t];
-            const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-            const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-            const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const bool self = (base + t) == i;
-            if (!self && r2 == 0.0f && first_bad < 0) first_bad = base + t;
-            const bool valid = !self && r2 != 0.0f;
-            if (TABLE) {
-                const int tt = ti_row + __float_as_int(pj.w);
-                lj_pair_table<true>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
-            } else {
-                lj_pair_single<true>(acc, dx, dy, dz, r2, valid, a.single);
-            }
-        }
+        for (int t = 0; t < lim; ++t)
+            all_pairs_entry<TABLE>(acc, zeros, pi, tile[t], b, a, s_tab_a, s_tab_b, ti_row);
     }
-    AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, first_bad};
+    AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
     s_part[threadIdx.x] = mine;
     // cluster barrier (release / acquire): every block's partial sums are in its shared memory
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (rank == 0 && active) {
         RowAcc sum = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
-        long long bad = -1;
+        int zeros_all = 0;
         const unsigned local = (unsigned)__cvta_generic_to_shared(&s_part[threadIdx.x]);
 #pragma unroll
         for (unsigned r = 0; r < (unsigned)kAllPairsSplit; ++r) {      // fixed order
             unsigned remote;
             asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
             float fx, fy, fz, u, w;
-            int cnt;
-            long long fb;
+            int cnt, zr;
             asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(fx) : "r"(remote));
             asm volatile("ld.shared::cluster.f32 %0, [%1+4];" : "=f"(fy) : "r"(remote));
             asm volatile("ld.shared::cluster.f32 %0, [%1+8];" : "=f"(fz) : "r"(remote));
             asm volatile("ld.shared::cluster.f32 %0, [%1+12];" : "=f"(u) : "r"(remote));
             asm volatile("ld.shared::cluster.f32 %0, [%1+16];" : "=f"(w) : "r"(remote));
             asm volatile("ld.shared::cluster.s32 %0, [%1+20];" : "=r"(cnt) : "r"(remote));
-            asm volatile("ld.shared::cluster.s64 %0, [%1+24];" : "=l"(fb) : "r"(remote));
+            asm volatile("ld.shared::cluster.s32 %0, [%1+24];" : "=r"(zr) : "r"(remote));
             sum.fx += fx; sum.fy += fy; sum.fz += fz; sum.u += u; sum.w += w; sum.cnt += cnt;
-            // tiles are dealt round-robin: the smallest index over all blocks is the first j
-            if (fb >= 0 && (bad < 0 || fb < bad)) bad = fb;
+            zeros_all += zr;
         }
         float fx, fy, fz, u, w;
         if (TABLE) {
@@ -1420,9 +1449,109 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
         }
         force[i] = make_float4(fx, fy, fz, u);
         if (virial) virial[i] = w;
-        if (bad >= 0)
-            atomicMin((unsigned long long *)&status->singular,
-                      ((unsigned long long)(unsigned)i << 32) | (unsigned)bad);
+        if (zeros_all != 1) all_pairs_report_singular((int)i, pi, pos, (int)n, b, status);
+    }
+    // nobody leaves while block 0 may still read its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Small systems (the paper's N = 2000).  With one thread per particle i a thread walks N / 8
+// partners one after the other and a scheduler holds less than one warp: the launch is as long
+// as that dependent chain (33 us at N = 2000 for 8 us of arithmetic).  Here the WARPS warps of
+// a block share ONE tile of 32 particles i and split every staged tile of 32 WARPS partners
+// between them, on top of the 8-way split over the cluster: 8 WARPS times the warps, chains
+// 8 WARPS times shorter.  Partial sums are combined in fixed order -- warps 0 .. WARPS-1
+// through shared memory, then blocks 0 .. 7 through distributed shared memory -- so results
+// are bitwise reproducible.  The shape depends on n alone: a system always takes the same
+// summation order.
+template <bool TABLE, int WARPS>
+__global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(32 * WARPS)
+k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
+                        const __grid_constant__ ForceArgs a, float4 *__restrict__ force,
+                        float *__restrict__ virial, b2md_status *status) {
+    constexpr int kTile = 32 * WARPS;
+    __shared__ float4 tile[kTile];
+    __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
+    __shared__ AllPairsPartial s_part[kTile];           // [warp][lane]
+    __shared__ AllPairsPartial s_sum[32];               // the block's total per particle i
+    if (TABLE) {
+        for (int t = threadIdx.x; t < a.ntypes * a.ntypes; t += blockDim.x) {
+            s_tab_a[t] = a.tab_a[t];
+            s_tab_b[t] = a.tab_b[t];
+        }
+    }
+    unsigned rank;                                   // block rank inside the cluster
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i_raw = (blockIdx.x / kAllPairsSplit) * 32ll + lane;
+    const bool active = i_raw < n;
+    const int64_t i = active ? i_raw : n - 1;
+    const float4 pi = pos[i];
+    const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
+    const BoxF &b = a.box;
+    RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+    int zeros = 0;
+    const int ni = (int)n;                       // (row indices are 32-bit everywhere)
+    const int my = warp * 32;                    // this warp's slice of the staged tile
+    for (int base = (int)rank * kTile; base < ni; base += kAllPairsSplit * kTile) {
+        __syncthreads();
+        const int jl = base + (int)threadIdx.x;
+        tile[threadIdx.x] = pos[jl < ni ? jl : ni - 1];
+        __syncthreads();
+        const int lim = max(0, min(32, ni - (base + warp * 32)));
+#pragma unroll 4
+        for (int t = 0; t < lim; ++t)
+            all_pairs_entry<TABLE>(acc, zeros, pi, tile[my + t], b, a, s_tab_a, s_tab_b, ti_row);
+    }
+    AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
+    s_part[threadIdx.x] = mine;
+    __syncthreads();
+    if (warp == 0) {
+        AllPairsPartial tot = s_part[lane];
+#pragma unroll
+        for (int w = 1; w < WARPS; ++w) {                           // fixed order
+            const AllPairsPartial q = s_part[w * 32 + lane];
+            tot.fx += q.fx; tot.fy += q.fy; tot.fz += q.fz; tot.u += q.u; tot.w += q.w;
+            tot.cnt += q.cnt;
+            tot.zeros += q.zeros;
+        }
+        s_sum[lane] = tot;
+    }
+    // cluster barrier (release / acquire): every block's sums are in its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank == 0 && warp == 0 && active) {
+        RowAcc sum = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+        int zeros_all = 0;
+        const unsigned local = (unsigned)__cvta_generic_to_shared(&s_sum[lane]);
+#pragma unroll
+        for (unsigned r = 0; r < (unsigned)kAllPairsSplit; ++r) {      // fixed order
+            unsigned remote;
+            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+            float fx, fy, fz, u, w;
+            int cnt, zr;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(fx) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+4];" : "=f"(fy) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+8];" : "=f"(fz) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+12];" : "=f"(u) : "r"(remote));
+            asm volatile("ld.shared::cluster.f32 %0, [%1+16];" : "=f"(w) : "r"(remote));
+            asm volatile("ld.shared::cluster.s32 %0, [%1+20];" : "=r"(cnt) : "r"(remote));
+            asm volatile("ld.shared::cluster.s32 %0, [%1+24];" : "=r"(zr) : "r"(remote));
+            sum.fx += fx; sum.fy += fy; sum.fz += fz; sum.u += u; sum.w += w; sum.cnt += cnt;
+            zeros_all += zr;
+        }
+        float fx, fy, fz, u, w;
+        if (TABLE) {
+            fx = sum.fx; fy = sum.fy; fz = sum.fz; u = sum.u; w = sum.w;
+        } else {
+            const PairParams &p = a.single;
+            fx = p.c_f * sum.fx; fy = p.c_f * sum.fy; fz = p.c_f * sum.fz;
+            u = fmaf(p.c_u, sum.u, p.half_shift * (float)sum.cnt);
+            w = p.c_w * sum.w;
+        }
+        force[i] = make_float4(fx, fy, fz, u);
+        if (virial) virial[i] = w;
+        if (zeros_all != 1) all_pairs_report_singular((int)i, pi, pos, (int)n, b, status);
     }
     // nobody leaves while block 0 may still read its shared memory
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1521,14 +1650,33 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     ForceArgs a;
     int rc = fill_args(a, box, table, ntypes);
     if (rc) return rc;
-    const unsigned blocks = blocks_for(n, kForceThreads) * kAllPairsSplit;   // clusters of 8
     cudaStream_t s = as_stream(stream);
-    if (ntypes == 1)
-        k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, n, a, (float4 *)d_force_f4, d_virial, d_status);
-    else
-        k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(
-            (const float4 *)d_pos_hi, n, a, (float4 *)d_force_f4, d_virial, d_status);
+    const float4 *pos = (const float4 *)d_pos_hi;
+    float4 *force = (float4 *)d_force_f4;
+    // Kernel shape by size (measured on B200, kernel time under ncu, profiles/README.md):
+    // N = 2000: 32.8 us with one thread per particle i, 13.6 us with 8 warps per 32 particles;
+    // N = 8192: 179 / 136 us; N = 32 768: 2.11 / 1.99 ms (4 warps); N = 131 072: 30.3 / 30.7 ms.
+    // The choice depends on n alone, so a system always takes the same summation order.
+#define B2MD_LAUNCH_SMALL(TABLE, WARPS)                                                        \
+    k_force_all_pairs_small<TABLE, WARPS>                                                     \
+        <<<blocks_for(n, 32) * kAllPairsSplit, 32 * WARPS, 0, s>>>(pos, n, a, force, d_virial, \
+                                                                   d_status)
+    if (n < kAllPairsEightWarps) {
+        if (ntypes == 1) B2MD_LAUNCH_SMALL(false, 8);
+        else B2MD_LAUNCH_SMALL(true, 8);
+    } else if (n < kAllPairsFourWarps) {
+        if (ntypes == 1) B2MD_LAUNCH_SMALL(false, 4);
+        else B2MD_LAUNCH_SMALL(true, 4);
+    } else {
+        const unsigned blocks = blocks_for(n, kForceThreads) * kAllPairsSplit;   // clusters of 8
+        if (ntypes == 1)
+            k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(pos, n, a, force, d_virial,
+                                                                      d_status);
+        else
+            k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(pos, n, a, force, d_virial,
+                                                                     d_status);
+    }
+#undef B2MD_LAUNCH_SMALL
     B2MD_CHECK_LAUNCH("b2md_force_lj_all_pairs");
     return 0;
 }

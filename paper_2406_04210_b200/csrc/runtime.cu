@@ -22,6 +22,7 @@
 // status->frozen: the remaining launches of the batch return immediately, the host
 // reads how many steps really completed and continues exactly like the ungraphed
 // overflow case (grow the stride, rebuild, resume the interrupted step).
+#include <algorithm>
 #include <new>
 #include <vector>
 
@@ -1175,4 +1176,109 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
     rep->reason = r->h_status->singular != ~0ull ? B2MD_RUN_SINGULAR : B2MD_RUN_DONE;
     finish_report(r, rep, before);
     return 0;
+}
+
+// ---- native loop of the all-to-all force mode ------------------------------------
+// Simulation.run with force_mode = "all_to_all" (the reference's default, sim.py:62-102):
+// integrate -> compute_forces_all_to_all -> finalize [-> thermostat] per step.  No list, no
+// rebuild flag, nothing the host has to look at between steps: the whole call is enqueued
+// without a round trip (finalize of step s and integrate of step s + 1 share one pass over the
+// state unless the thermostat sits between them) and the status block -- the singular-pair
+// word -- is read once per chunk of kAllPairsChunk steps.  Same kernels, same order of
+// operations as the operator loop: bit-identical trajectories.
+constexpr int64_t kAllPairsChunk = 512;
+
+B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, void *d_force_f4,
+                                   void *d_image_i4, float *d_virial, int64_t n,
+                                   const b2md_box *box, const double *table, int32_t ntypes,
+                                   double dt, int64_t n_steps, double thermo_probability,
+                                   double thermo_temperature, uint64_t thermo_seed,
+                                   int64_t first_step, b2md_status *d_status, void *h_status,
+                                   void *stream, b2md_run_report *rep) {
+    if (!d_pos_hi || !d_pos_lo || !d_vel || !d_force_f4 || !d_image_i4 || !box || !table ||
+        !d_status || !h_status || !rep || n < 1 || n_steps < 0 || !(thermo_probability >= 0.0)) {
+        set_error("b2md_run_all_pairs: bad arguments");
+        return -1;
+    }
+    *rep = b2md_run_report();
+    cudaStream_t s = as_stream(stream);
+    const bool thermostatted = thermo_probability > 0.0;
+    const double p = thermo_probability > 1.0 ? 1.0 : thermo_probability;
+    b2md_status *h = static_cast<b2md_status *>(h_status);
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc;
+    if ((rc = check_cuda(cudaEventCreate(&ev[0]), "event create"))) return rc;
+    if ((rc = check_cuda(cudaEventCreate(&ev[1]), "event create"))) {
+        cudaEventDestroy(ev[0]);
+        return rc;
+    }
+    auto leave = [&](int code) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        return code;
+    };
+    if ((rc = b2md_status_reset(d_status, stream))) return leave(rc);
+    if ((rc = check_cuda(cudaEventRecord(ev[0], s), "event record"))) return leave(rc);
+    bool pending_kick = false;          // forces of the last step not yet applied to the velocities
+    while (rep->steps_done < n_steps) {
+        const int64_t chunk = std::min<int64_t>(kAllPairsChunk, n_steps - rep->steps_done);
+        for (int64_t q = 0; q < chunk; ++q) {
+            if (pending_kick)
+                rc = b2md_vv_finalize_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n,
+                                                box, dt, nullptr, 0.0, d_status, stream);
+            else
+                rc = b2md_vv_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n, box, dt,
+                                       nullptr, 0.0, d_status, stream);
+            if (rc) return leave(rc);
+            if ((rc = b2md_force_lj_all_pairs(d_pos_hi, n, box, table, ntypes, d_force_f4, d_virial,
+                                              d_status, stream))) return leave(rc);
+            rep->kernel_launches += 2;
+            pending_kick = true;
+            if (thermostatted) {
+                if ((rc = b2md_vv_finalize(d_vel, d_force_f4, n, dt, stream))) return leave(rc);
+                if ((rc = b2md_andersen(d_vel, d_pos_lo, n, thermo_seed,
+                                        (uint64_t)(first_step + rep->steps_done + q), p,
+                                        thermo_temperature, nullptr, stream))) return leave(rc);
+                rep->kernel_launches += 2;
+                pending_kick = false;
+            }
+        }
+        rep->steps_done += chunk;
+        const bool last = rep->steps_done >= n_steps;
+        if (last && pending_kick) {
+            if ((rc = b2md_vv_finalize(d_vel, d_force_f4, n, dt, stream))) return leave(rc);
+            rep->kernel_launches += 1;
+            pending_kick = false;
+        }
+        if (last && (rc = check_cuda(cudaEventRecord(ev[1], s), "event record"))) return leave(rc);
+        if ((rc = check_cuda(cudaMemcpyAsync(h, d_status, sizeof(b2md_status),
+                                             cudaMemcpyDeviceToHost, s), "status read-back")))
+            return leave(rc);
+        if ((rc = check_cuda(cudaStreamSynchronize(s), "status sync"))) return leave(rc);
+        if (h->singular != ~0ull) {
+            // a coincident pair (forces.py:113-116): the steps enqueued behind it ran on
+            // non-finite forces; stop here and let the caller raise
+            if (pending_kick) {
+                if ((rc = b2md_vv_finalize(d_vel, d_force_f4, n, dt, stream))) return leave(rc);
+                rep->kernel_launches += 1;
+            }
+            if (!last && (rc = check_cuda(cudaEventRecord(ev[1], s), "event record")))
+                return leave(rc);
+            if ((rc = check_cuda(cudaStreamSynchronize(s), "drain"))) return leave(rc);
+            break;
+        }
+    }
+    if (n_steps == 0) {
+        if ((rc = check_cuda(cudaEventRecord(ev[1], s), "event record"))) return leave(rc);
+        if ((rc = check_cuda(cudaMemcpyAsync(h, d_status, sizeof(b2md_status),
+                                             cudaMemcpyDeviceToHost, s), "status read-back")))
+            return leave(rc);
+        if ((rc = check_cuda(cudaStreamSynchronize(s), "status sync"))) return leave(rc);
+    }
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, ev[0], ev[1]) == cudaSuccess) rep->gpu_ms = ms;
+    rep->singular = h->singular;
+    rep->reason = h->singular != ~0ull ? B2MD_RUN_SINGULAR : B2MD_RUN_DONE;
+    rep->list_valid = 1;
+    return leave(0);
 }

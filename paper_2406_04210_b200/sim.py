@@ -33,7 +33,8 @@ from . import _lib
 from .backend import BackendSelector
 from .core import COMPUTE, DeviceState, ParticleState, SignalEngine, SimBox
 from .errors import ConfigError, NeighborOverflowError, SingularPairError
-from .forces import compute_forces_all_to_all, compute_forces_truncated, use_pair_rows
+from .forces import (_table_ptr, compute_forces_all_to_all, compute_forces_truncated,
+                     use_pair_rows)
 from .integrate import IntegratorParams, andersen_thermostat, vv_finalize, vv_integrate
 from .neighbor import (HILBERT_SUB_BITS, NeighborList, _round_up, bin_particles,
                        build_neighbor_list, grid_shape, needs_rebuild, reorder_hilbert)
@@ -134,10 +135,14 @@ class Simulation:
         self.graph_steps = 0
         # (a thermostatted native loop launches integrate / force / finalize / thermostat
         # separately: the thermostat is the reference's second finalize slot, sim.py:86-87)
-        self.native = (force_mode == TRUNCATED) if native is None else bool(native)
+        # all-to-all forces (the reference's default force mode) have their own native loop,
+        # b2md_run_all_pairs: no list, nothing to decide between steps, so a call is enqueued
+        # whole.  native=False keeps the operator-by-operator loop (one ctypes call and one
+        # status read-back per operator: ~90 us per step of host time at N = 2000).
+        self.native_all_pairs = force_mode == ALL_TO_ALL and (native is None or bool(native))
+        self.native = (force_mode == TRUNCATED) if native is None else \
+            (bool(native) and force_mode == TRUNCATED)
         self._thermostatted = thermostatted
-        if self.native and force_mode != TRUNCATED:
-            raise ConfigError("the native step loop drives truncated forces only")
         if not self.native and self.reorder == "cell":
             raise ConfigError("reorder='cell' is implemented by the native step loop only")
 
@@ -554,10 +559,58 @@ class Simulation:
         self.wasted_force_launches = 0
         self._rebuild_base = self._rebuild_total
 
+    def _run_native_all_pairs(self, n_steps: int):
+        """Simulation.run for force_mode = "all_to_all" through b2md_run_all_pairs: the steps
+        between two samples are one call (bit-identical to the operator loop)."""
+        eng = self.engine
+        eng._check_ready(n_steps)
+        if n_steps == 0:
+            return
+        torch = _torch()
+        st = self.state
+        st.sync_to_compute()
+        eng.emit_initial_sample()
+        dev = st.device_state()
+        tab, tab_ptr, nt = _table_ptr(self.lj, st)
+        if "h_status" not in self._keep:
+            self._keep["h_status"] = torch.empty(64, dtype=torch.uint8).pin_memory()
+        p = self.thermostat.redraw_probability(self.integrator.dt) if self._thermostatted else 0.0
+        temperature = float(self.thermostat.temperature) if self._thermostatted else 1.0
+        seed = int(self.thermostat.seed) % (1 << 64) if self._thermostatted else 0
+        left = n_steps
+        while left > 0:
+            to_sample = eng.sample_interval - (eng.step_count % eng.sample_interval)
+            chunk = min(left, to_sample)
+            rep = _lib.RunReport()
+            t0 = time.perf_counter()
+            _lib.call("b2md_run_all_pairs", dev.pos_hi.data_ptr(), dev.pos_lo.data_ptr(),
+                      dev.vel.data_ptr(), dev.force.data_ptr(), dev.image.data_ptr(),
+                      dev.virial.data_ptr(), dev.n, self.box.c_box(), tab_ptr, nt,
+                      float(self.integrator.dt), chunk, float(p), temperature, seed,
+                      eng.step_count, dev.status.data_ptr(), self._keep["h_status"].data_ptr(),
+                      dev.stream, ctypes.byref(rep))
+            wall = time.perf_counter() - t0
+            self.force_seconds += min(1e-3 * rep.gpu_ms, wall)
+            self.kernel_launches += rep.kernel_launches
+            st.mark_compute_written("positions", "images", "velocities", "forces",
+                                    "per_particle_potential", "virial")
+            if rep.reason == _lib.RUN_SINGULAR:
+                i, j = rep.singular >> 32, rep.singular & 0xFFFFFFFF
+                if not dev.identity_order:
+                    ids = dev.particle_ids()
+                    i, j = sorted((int(ids[i]), int(ids[j])))
+                raise SingularPairError(int(i), int(j))
+            eng.step_count += chunk
+            left -= chunk
+            if eng.step_count % eng.sample_interval == 0:
+                eng.emit("sample")
+
     def run(self, n_steps: int):
         if getattr(self, "_closed", False):
             raise RuntimeError("this Simulation was closed")
-        if self.native:
+        if self.native_all_pairs:
+            self._run_native_all_pairs(n_steps)
+        elif self.native:
             self._run_native(n_steps)
         else:
             self.engine.run_steps(n_steps)

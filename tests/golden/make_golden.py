@@ -300,6 +300,39 @@ def trajectory_case():
          lat256_edges=box256.edge_lengths)
 
 
+# ------------------------------------------------ all-to-all loop (default mode)
+def all2all_trajectory_case():
+    """Simulation.run in the reference's DEFAULT force mode (sim.py:62-102, all_to_all,
+    untruncated pair potential as in the all2all-2k preset, bench.py:147-151), at a size the
+    reference finishes in seconds: an NVE run and a thermostatted one (second finalize slot,
+    sim.py:86-87) from the same start."""
+    n, rho, T, dt, steps, every = 300, 0.8, 1.0, 0.002, 200, 20
+    out = {}
+    for tag, rate in (("nve", 0.0), ("nvt", 5.0)):
+        st, box = ref.init_lattice_any(n, rho)
+        ref.init_velocities(st, T, 42)
+        if tag == "nve":
+            out["pos0"] = np.array(st.positions.acquire_read(HOST))
+            out["vel0"] = np.array(st.velocities.acquire_read(HOST))
+            out["edges"] = box.edge_lengths
+        lj = ref.make_shifted(1.0, 1.0)                   # r_cut = inf: the bare potential
+        thermostat = ref.ThermostatParams(temperature=T, rate=rate, seed=7) if rate else None
+        sim = ref.Simulation(st, box, lj, dt, thermostat=thermostat, sample_interval=every,
+                             sample_initial=True)
+        sim.run(steps)
+        s = sim.samples
+        out[tag + "_step"] = np.array([x.step for x in s])
+        out[tag + "_pe"] = np.array([x.potential_energy for x in s])
+        out[tag + "_ke"] = np.array([x.kinetic_energy for x in s])
+        out[tag + "_momentum"] = np.array([x.total_momentum for x in s])
+        out[tag + "_pos_end"] = np.array(st.positions.acquire_read(HOST))
+        out[tag + "_vel_end"] = np.array(st.velocities.acquire_read(HOST))
+        out[tag + "_forces_end"] = np.array(st.forces.acquire_read(HOST))
+    save("all2all_trajectory", n=np.int64(n), density=np.float64(rho), dt=np.float64(dt),
+         steps=np.int64(steps), every=np.int64(every), temperature=np.float64(T),
+         rate=np.float64(5.0), seed=np.int64(7), **out)
+
+
 # ---------------------------------------------------------- rng / thermostat
 def thermostat_case():
     from mdbench import rng
@@ -348,11 +381,15 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "harness":
         harness_csv_case()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "all2all":
+        all2all_trajectory_case()
+        sys.exit(0)
     neighbor_cases()
     rebuild_cases()
     force_cases()
     integrate_cases()
     observable_cases()
     trajectory_case()
+    all2all_trajectory_case()
     thermostat_case()
     harness_csv_case()

@@ -221,6 +221,49 @@ def test_nve_trajectory_bit_exact():
     assert sim.stride == int(G["stride_end"])
 
 
+def _oracle_all2all_run(G, rate):
+    """Simulation.run in all_to_all mode (sim.py:62-102) restated with the oracle's
+    operators: integrate -> all-pairs forces -> finalize [-> thermostat]."""
+    n = int(G["n"])
+    edges, dt = G["edges"], float(G["dt"])
+    table = orc.pair_table(1.0, 1.0, np.inf)
+    masses = np.ones(n)
+    pos, vel = G["pos0"].copy(), G["vel0"].copy()
+    images = np.zeros((n, 3), np.int64)
+    f, pe, _ = orc.forces_all_pairs(pos, edges, table, threads=2)
+    samples = []
+
+    def sample(step):
+        t = orc.thermo(vel, masses, pe)
+        samples.append((step, t["pe"], t["ke"], t["momentum"]))
+    sample(0)
+    for step in range(int(G["steps"])):
+        pos, images, vel = orc.vv_integrate(pos, images, vel, f, masses, edges, dt)
+        f, pe, _ = orc.forces_all_pairs(pos, edges, table, threads=2)
+        vel = orc.vv_finalize(vel, f, masses, dt)
+        if rate:
+            vel, _ = orc.andersen_thermostat(vel, masses, float(G["temperature"]), rate,
+                                             int(G["seed"]), dt, step)
+        if (step + 1) % int(G["every"]) == 0:
+            sample(step + 1)
+    return samples, pos, vel, f
+
+
+@pytest.mark.parametrize("tag", ["nve", "nvt"])
+def test_all_to_all_loop_bit_exact(tag):
+    """The reference's default force mode, NVE and with the Andersen thermostat as second
+    finalize slot: every sample and the end state of the oracle loop equal the reference's."""
+    G = load_golden("all2all_trajectory")
+    samples, pos, vel, f = _oracle_all2all_run(G, float(G["rate"]) if tag == "nvt" else 0.0)
+    assert [x[0] for x in samples] == list(G[tag + "_step"])
+    assert np.array_equal([x[1] for x in samples], G[tag + "_pe"])
+    assert np.allclose([x[2] for x in samples], G[tag + "_ke"], rtol=1e-15, atol=0)
+    assert np.array_equal(np.array([x[3] for x in samples]), G[tag + "_momentum"])
+    assert np.array_equal(pos, G[tag + "_pos_end"])
+    assert np.array_equal(vel, G[tag + "_vel_end"])
+    assert np.array_equal(f, G[tag + "_forces_end"])
+
+
 # ----------------------------------------------------------- rng / thermostat
 def test_random_streams_and_thermostat_bit_exact():
     G = load_golden("thermostat")
