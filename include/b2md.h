@@ -424,6 +424,18 @@ int b2md_vv_finalize_integrate(void *d_pos_hi, void *d_pos_lo, void *d_vel,
  * b2md_stream_words exposes raw words / uniforms / normals [offset, offset+count). */
 int b2md_andersen(void *d_vel, const void *d_ids_pos_lo, int64_t n, uint64_t seed, uint64_t step,
                   double probability, double temperature, int32_t *d_redrawn, void *stream);
+/* The finalize slots of a thermostatted step in ONE pass (sim.py:86-87): vv_finalize
+ * (integrate.py:73-79), then andersen_thermostat at `step` (integrate.py:82-107; logical ids
+ * from d_pos_lo.w), and with integrate_next != 0 also vv_integrate of the next step
+ * (integrate.py:58-70 + core.py:72-93, displacement check as b2md_vv_integrate when
+ * d_ref_pos_f4 != NULL).  Bit-identical to b2md_vv_finalize + b2md_andersen
+ * [+ b2md_vv_integrate]; used by the native loops, which would otherwise spend four launches
+ * on a thermostatted step. */
+int b2md_vv_finalize_andersen(void *d_pos_hi, void *d_pos_lo, void *d_vel, const void *d_force_f4,
+                              void *d_image_i4, int64_t n, const b2md_box *box, double dt,
+                              uint64_t seed, uint64_t step, double probability,
+                              double temperature, int32_t integrate_next, void *d_ref_pos_f4,
+                              double half_skin2, b2md_status *d_status, void *stream);
 int b2md_stream_words(uint64_t seed, uint64_t stream_id, uint64_t step, int64_t word_offset,
                       int64_t count, uint64_t *d_raw, double *d_uniform, double *d_normal,
                       void *stream);

@@ -200,6 +200,9 @@ _SIGNATURES = {
     "b2md_runner_prune_count": (c_int64, [c_void_p, POINTER(c_int64)]),
     "b2md_runner_set_thermostat": (c_int32, [c_void_p, c_double, c_double, c_uint64]),
     "b2md_runner_set_step": (c_int32, [c_void_p, c_int64]),
+    "b2md_vv_finalize_andersen": (c_int32, [_P, _P, _P, _P, _P, c_int64, _P, c_double, c_uint64,
+                                            c_uint64, c_double, c_double, c_int32, _P, c_double,
+                                            _P, _P]),
     "b2md_run_all_pairs": (c_int32, [_P, _P, _P, _P, _P, _P, c_int64, _P, _P, c_int32, c_double,
                                      c_int64, c_double, c_double, c_uint64, c_int64, _P, _P, _P,
                                      _P]),

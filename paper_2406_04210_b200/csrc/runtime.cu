@@ -522,15 +522,23 @@ int begin_call(b2md_runner *r) {
 }
 
 // Second half-kick and the thermostat slot of step number `step` (sim.py:100-102).
-int finish_thermostat_step(b2md_runner *r, int64_t step) {
+// The finalize slots of a thermostatted step (sim.py:86-87: vv_finalize, then the thermostat)
+// in one launch; with integrate_next the same pass also integrates the next step (the runner
+// is then "ahead", exactly as after b2md_vv_integrate).  Bit-identical to the separate launches.
+int finish_thermostat_step(b2md_runner *r, int64_t step, bool integrate_next = false) {
     const b2md_runner_config &c = r->cfg;
     Set a = live(r);
-    int rc = b2md_vv_finalize(a.vel, a.force, c.n, c.dt, r->stream);
-    if (rc) return rc;
-    rc = b2md_andersen(a.vel, a.pos_lo, c.n, r->thermo_seed, (uint64_t)step, r->thermo_p,
-                       r->thermo_t, nullptr, r->stream);
-    r->launches += 2;
+    const int rc = b2md_vv_finalize_andersen(a.pos_hi, a.pos_lo, a.vel, a.force, a.image, c.n,
+                                             &c.box, c.dt, r->thermo_seed, (uint64_t)step,
+                                             r->thermo_p, r->thermo_t, integrate_next ? 1 : 0,
+                                             integrate_next ? c.ref_pos : nullptr, r->half_skin2,
+                                             c.status, r->stream);
+    r->launches += 1;
     r->pending_kick = false;
+    if (integrate_next) {
+        r->ahead = true;
+        r->gate_in = kWordRebuildFlag;
+    }
     return rc;
 }
 
@@ -706,8 +714,10 @@ int plain_step(b2md_runner *r, b2md_run_report *rep, bool thermo, int64_t before
     } else {
         r->ahead = false;
         r->pending_kick = true;
+        // (`thermo` = this is the step the caller can observe, the last one of the call: the
+        // next step is integrated by the next call)
         if (thermostatted(r) &&
-            (rc = finish_thermostat_step(r, r->first_step + rep->steps_done))) return rc;
+            (rc = finish_thermostat_step(r, r->first_step + rep->steps_done, !thermo))) return rc;
     }
     rep->steps_done += 1;
     return 0;
@@ -1220,27 +1230,38 @@ B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, 
     if ((rc = b2md_status_reset(d_status, stream))) return leave(rc);
     if ((rc = check_cuda(cudaEventRecord(ev[0], s), "event record"))) return leave(rc);
     bool pending_kick = false;          // forces of the last step not yet applied to the velocities
+    bool ahead = false;                 // the next step is already integrated (thermostatted loop)
     while (rep->steps_done < n_steps) {
         const int64_t chunk = std::min<int64_t>(kAllPairsChunk, n_steps - rep->steps_done);
         for (int64_t q = 0; q < chunk; ++q) {
-            if (pending_kick)
-                rc = b2md_vv_finalize_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n,
-                                                box, dt, nullptr, 0.0, d_status, stream);
-            else
-                rc = b2md_vv_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n, box, dt,
-                                       nullptr, 0.0, d_status, stream);
-            if (rc) return leave(rc);
+            if (!ahead) {
+                if (pending_kick)
+                    rc = b2md_vv_finalize_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4,
+                                                    d_image_i4, n, box, dt, nullptr, 0.0, d_status,
+                                                    stream);
+                else
+                    rc = b2md_vv_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n,
+                                           box, dt, nullptr, 0.0, d_status, stream);
+                if (rc) return leave(rc);
+                rep->kernel_launches += 1;
+            }
+            ahead = false;
             if ((rc = b2md_force_lj_all_pairs(d_pos_hi, n, box, table, ntypes, d_force_f4, d_virial,
                                               d_status, stream))) return leave(rc);
-            rep->kernel_launches += 2;
+            rep->kernel_launches += 1;
             pending_kick = true;
             if (thermostatted) {
-                if ((rc = b2md_vv_finalize(d_vel, d_force_f4, n, dt, stream))) return leave(rc);
-                if ((rc = b2md_andersen(d_vel, d_pos_lo, n, thermo_seed,
-                                        (uint64_t)(first_step + rep->steps_done + q), p,
-                                        thermo_temperature, nullptr, stream))) return leave(rc);
-                rep->kernel_launches += 2;
+                // finalize + thermostat (+ integrate of the next step unless this is the
+                // step the caller observes) in one pass
+                const bool more = rep->steps_done + q + 1 < n_steps;
+                if ((rc = b2md_vv_finalize_andersen(d_pos_hi, d_pos_lo, d_vel, d_force_f4,
+                                                    d_image_i4, n, box, dt, thermo_seed,
+                                                    (uint64_t)(first_step + rep->steps_done + q),
+                                                    p, thermo_temperature, more ? 1 : 0, nullptr,
+                                                    0.0, d_status, stream))) return leave(rc);
+                rep->kernel_launches += 1;
                 pending_kick = false;
+                ahead = more;
             }
         }
         rep->steps_done += chunk;

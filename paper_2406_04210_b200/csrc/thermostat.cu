@@ -13,6 +13,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "integrate.cuh"
 
 namespace b2md {
 
@@ -105,6 +106,20 @@ __device__ double ndtri_f64(double y0) {
     return negate ? -x : x;
 }
 
+// The thermostat's decision and draw for logical particle i (integrate.py:96-104): true if
+// the velocity v (w = mass) was redrawn.
+__device__ __forceinline__ bool andersen_redraw(float4 &v, uint64_t i, int64_t n, uint64_t seed,
+                                                uint64_t step, double p, double temperature) {
+    const double u = word_to_uniform(stream_word(seed, 0, step, i));
+    if (!(u < p)) return false;                       // integrate.py:96 `redraw = u < p`
+    const double scale = sqrt(__ddiv_rn(temperature, (double)v.w));   // sqrt(T / m)
+    const uint64_t base = (uint64_t)n + 3 * i;
+    v.x = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base))), scale);
+    v.y = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base + 1))), scale);
+    v.z = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base + 2))), scale);
+    return true;
+}
+
 __global__ void k_andersen(float4 *__restrict__ vel, const float4 *__restrict__ ids, int64_t n,
                            uint64_t seed, uint64_t step, double p, double temperature,
                            int32_t *__restrict__ redrawn) {
@@ -112,20 +127,64 @@ __global__ void k_andersen(float4 *__restrict__ vel, const float4 *__restrict__ 
     int hit = 0;
     if (r < n) {
         const uint64_t i = ids ? (uint64_t)(uint32_t)__float_as_int(ids[r].w) : (uint64_t)r;
-        const double u = word_to_uniform(stream_word(seed, 0, step, i));
-        if (u < p) {                                  // integrate.py:96 `redraw = u < p`
+        float4 v = vel[r];
+        if (andersen_redraw(v, i, n, seed, step, p, temperature)) {
             hit = 1;
-            float4 v = vel[r];
-            const double scale = sqrt(__ddiv_rn(temperature, (double)v.w));   // sqrt(T / m)
-            const uint64_t base = (uint64_t)n + 3 * i;
-            v.x = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base))), scale);
-            v.y = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base + 1))), scale);
-            v.z = (float)__dmul_rn(ndtri_f64(word_to_uniform(stream_word(seed, 0, step, base + 2))), scale);
             vel[r] = v;
         }
     }
     hit = warp_sum_i(hit);
     if ((threadIdx.x & 31) == 0 && hit && redrawn) atomicAdd(redrawn, hit);
+}
+
+// The finalize slots of a thermostatted step in one pass over the velocities (sim.py:86-87):
+// vv_finalize (second half-kick with the new forces, integrate.py:73-79), then the thermostat;
+// with INTEGRATE also vv_integrate of the NEXT step (first half-kick with the same forces,
+// drift, wrap, image counters, displacement check -- the body of k_integrate<1>).  Per particle
+// the operations and their order are those of the separate launches: bit-identical.
+constexpr int kFusedThreads = 256;
+
+template <bool INTEGRATE>
+__global__ void __launch_bounds__(kFusedThreads)
+k_finalize_andersen(float4 *__restrict__ pos_hi, float4 *__restrict__ pos_lo,
+                    float4 *__restrict__ vel, const float4 *__restrict__ force,
+                    int4 *__restrict__ image, int64_t n, const StepConst c,
+                    float4 *__restrict__ ref_pos, b2md_status *status, uint64_t seed,
+                    uint64_t step, double p, double temperature) {
+    __shared__ float s_max[kFusedThreads / 32];
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float d2 = 0.0f;
+    if (r < n) {
+        float4 v = vel[r];
+        const float4 f = force[r];
+        kick(v, f, c.half_dt);                                        // vv_finalize
+        float4 l = pos_lo[r];                                         // (w = logical id)
+        const uint64_t i = (uint64_t)(uint32_t)__float_as_int(l.w);
+        andersen_redraw(v, i, n, seed, step, p, temperature);
+        if (INTEGRATE) {
+            float4 h = pos_hi[r];
+            float4 ref = ref_pos ? ref_pos[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ref0 = ref;
+            d2 = advance_regs<1>(r, h, l, v, ref, ref_pos != nullptr, f, image, c);
+            pos_hi[r] = h;
+            pos_lo[r] = l;
+            if (ref_pos && (ref.x != ref0.x || ref.y != ref0.y || ref.z != ref0.z)) ref_pos[r] = ref;
+        }
+        vel[r] = v;
+    }
+    if (INTEGRATE && ref_pos) {
+        d2 = warp_max(d2);
+        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            float m = threadIdx.x < kFusedThreads / 32 ? s_max[threadIdx.x] : 0.0f;
+            m = warp_max(m);
+            if (threadIdx.x == 0 && m > 0.0f) {
+                atomicMax(&status->max_disp2_bits, __float_as_uint(m));
+                if (m > c.half_skin2) status->rebuild_flag = 1;
+            }
+        }
+    }
 }
 
 __global__ void k_stream_words(uint64_t seed, uint64_t stream, uint64_t step, int64_t offset,
@@ -160,6 +219,34 @@ B2MD_EXPORT int b2md_andersen(void *d_vel, const void *d_ids_pos_lo, int64_t n, 
     k_andersen<<<blocks_for(n, 128), 128, 0, s>>>((float4 *)d_vel, (const float4 *)d_ids_pos_lo, n,
                                                   seed, step, probability, temperature, d_redrawn);
     B2MD_CHECK_LAUNCH("b2md_andersen");
+    return 0;
+}
+
+B2MD_EXPORT int b2md_vv_finalize_andersen(void *d_pos_hi, void *d_pos_lo, void *d_vel,
+                                          const void *d_force_f4, void *d_image_i4, int64_t n,
+                                          const b2md_box *box, double dt, uint64_t seed,
+                                          uint64_t step, double probability, double temperature,
+                                          int32_t integrate_next, void *d_ref_pos_f4,
+                                          double half_skin2, b2md_status *d_status, void *stream) {
+    if (n <= 0 || !box || !(dt > 0.0) || !d_pos_lo || !d_vel || !d_force_f4 ||
+        !(temperature > 0.0) || !(probability >= 0.0) ||
+        (integrate_next && (!d_pos_hi || !d_image_i4)) || (d_ref_pos_f4 && !d_status)) {
+        set_error("b2md_vv_finalize_andersen: bad arguments");
+        return -1;
+    }
+    const StepConst c = make_step(box, dt, half_skin2);
+    cudaStream_t s = as_stream(stream);
+    const unsigned blocks = blocks_for(n, kFusedThreads);
+    if (integrate_next)
+        k_finalize_andersen<true><<<blocks, kFusedThreads, 0, s>>>(
+            (float4 *)d_pos_hi, (float4 *)d_pos_lo, (float4 *)d_vel, (const float4 *)d_force_f4,
+            (int4 *)d_image_i4, n, c, (float4 *)d_ref_pos_f4, d_status, seed, step, probability,
+            temperature);
+    else
+        k_finalize_andersen<false><<<blocks, kFusedThreads, 0, s>>>(
+            (float4 *)d_pos_hi, (float4 *)d_pos_lo, (float4 *)d_vel, (const float4 *)d_force_f4,
+            (int4 *)d_image_i4, n, c, nullptr, d_status, seed, step, probability, temperature);
+    B2MD_CHECK_LAUNCH("b2md_vv_finalize_andersen");
     return 0;
 }
 

@@ -43,9 +43,10 @@ def test_native_loop_is_bit_identical_to_the_operator_loop(tag):
     for a, b in zip(out[True][0], out[False][0]):
         assert np.array_equal(a, b)
     assert out[True][1] == out[False][1]
-    # NVE: integrate + force, then (finalize + integrate) + force per step, one finalize at the
-    # end of every call (a call ends at each sample); NVT: four launches per step
-    assert out[True][2] == (2 * 200 + 11 if tag == "nve" else 4 * 200)
+    # two launches per step -- all pairs, and one pass over the state: finalize + integrate (NVE)
+    # or finalize + thermostat + integrate (NVT) -- plus, per call (a call ends at each sample),
+    # the first integrate on its own and the last finalize without the integrate
+    assert out[True][2] == 2 * 200 + 11
 
 
 @pytest.mark.parametrize("tag", ["nve", "nvt"])
