@@ -1029,7 +1029,10 @@ __device__ __noinline__ void pair_row_loop_outlined(RowAcc &A, RowAcc &B, const 
 
 // ADVANCE: 0 = forces only, 1 = one-launch step, 2 = one-launch step that also stores the
 // slab halo into the neighbour ranks' ghost rows (AdvanceArgs::halo_*)
-template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE, bool PRUNE = false>
+// ORDERED: the lane order (b2md_pair_order) is its own instantiation -- with the lookup in the
+// common kernel, even switched off, ptxas allocated the table variant's loops differently and
+// Kob-Andersen N = 262 144 went from 0.0955 to 0.111 ms per step.
+template <bool TABLE, bool THERMO, bool SIG1, int ADVANCE, bool PRUNE = false, bool ORDERED = false>
 __global__ void __launch_bounds__(kPairThreads, PRUNE ? 6 : B2MD_PAIR_MIN_BLOCKS)
 k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                 const int4 *__restrict__ pair_nbr, const int32_t *__restrict__ pair_counts,
@@ -1059,7 +1062,7 @@ k_force_lj_pair(const float4 *__restrict__ pos, int64_t n, const __grid_constant
     // Lane order (b2md_pair_order): a warp pays for its longest row, 27.7 tiles where the mean
     // row has 23.3; with the pairs of a block dealt to its warps by row length the warps walk
     // 24.6.  A thread still owns one pair and walks its row in ascending order: same sums.
-    const unsigned slot = a.order ? (unsigned)a.order[bid * (unsigned)kPairThreads + threadIdx.x]
+    const unsigned slot = ORDERED ? (unsigned)a.order[bid * (unsigned)kPairThreads + threadIdx.x]
                                   : threadIdx.x;
     const int64_t t_raw = bid * (int64_t)blockDim.x + slot;
     const bool active = t_raw < n_pairs;
@@ -1701,11 +1704,19 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
     const bool thermo = (flags & B2MD_FORCE_SKIP_THERMO) == 0;
     AdvanceArgs adv = {};
     if (advance) adv = *advance;
+#define B2MD_PAIR_ARGS                                                                        \
+    (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch, d_nbr,   \
+        d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,                \
+        ((flags & B2MD_FORCE_GATED) ? 1 : 0) | exp_bits, adv
 #define B2MD_LAUNCH_PAIR(TABLE, THERMO, SIG1, ADVANCE)                                        \
-    k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE><<<blocks, kPairThreads, 0, s>>>(           \
-        (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
-        d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
-        ((flags & B2MD_FORCE_GATED) ? 1 : 0) | exp_bits, adv)
+    do {                                                                                      \
+        if (a.order)                                                                          \
+            k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE, false, true>                        \
+                <<<blocks, kPairThreads, 0, s>>>(B2MD_PAIR_ARGS);                             \
+        else                                                                                  \
+            k_force_lj_pair<TABLE, THERMO, SIG1, ADVANCE>                                     \
+                <<<blocks, kPairThreads, 0, s>>>(B2MD_PAIR_ARGS);                             \
+    } while (0)
     // Measured on B200 at N = 1 M (profiles/README.md): 8 CTAs/SM of 128 threads; 4 to 12
     // CTAs/SM, 32/64-thread CTAs, position gathers one trip ahead, L2 prefetch of the
     // index stream, L1 cache-policy hints, per-SM or per-warp work queues were all neutral
@@ -1731,10 +1742,14 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
         }
     } else if (advance && adv.prune_mode == kPruneNow) {
 #define B2MD_LAUNCH_PRUNE(TABLE, SIG1)                                                        \
-    k_force_lj_pair<TABLE, false, SIG1, 1, true><<<blocks, kPairThreads, 0, s>>>(             \
-        (const float4 *)d_pos_hi, n, a, (const int4 *)d_pair_nbr, d_pair_counts, pair_pitch,  \
-        d_nbr, d_counts, pitch, d_boundary, (float4 *)d_force_f4, d_virial, d_status,         \
-        ((flags & B2MD_FORCE_GATED) ? 1 : 0) | exp_bits, adv)
+    do {                                                                                      \
+        if (a.order)                                                                          \
+            k_force_lj_pair<TABLE, false, SIG1, 1, true, true>                                \
+                <<<blocks, kPairThreads, 0, s>>>(B2MD_PAIR_ARGS);                             \
+        else                                                                                  \
+            k_force_lj_pair<TABLE, false, SIG1, 1, true>                                      \
+                <<<blocks, kPairThreads, 0, s>>>(B2MD_PAIR_ARGS);                             \
+    } while (0)
         if (ntypes == 1) {
             if (sig1) B2MD_LAUNCH_PRUNE(false, true);
             else B2MD_LAUNCH_PRUNE(false, false);
@@ -1758,6 +1773,7 @@ int launch_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const int
         else B2MD_LAUNCH_PAIR(true, false, false, 0);
     }
 #undef B2MD_LAUNCH_PAIR
+#undef B2MD_PAIR_ARGS
     int rc2 = check_cuda(cudaPeekAtLastError(), name);
     return rc2;
 }
