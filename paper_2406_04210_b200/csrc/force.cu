@@ -1344,17 +1344,49 @@ struct AllPairsPartial {
     int pad;
 };
 
+// Fixed-point coordinates of the all-pairs kernels: a coordinate x in [0, L) becomes the 32-bit
+// integer round(x 2^32 / L), so that the wrapped difference of two of them IS the minimum
+// image (forces.py:45-50: d - L rint(d / L)) -- one integer subtract, one conversion and one
+// multiply per axis where the exact fp32 sequence (delta<true>: split box length, shifted
+// operands) takes ten instructions.  Resolution L 2^-32 (3e-9 sigma at N = 2000, finer than the
+// fp32 high words the kernel is given); the difference is exact, its conversion rounds to 24
+// bits of the DISTANCE, so close pairs lose nothing to the size of the box.
+struct FixedBox {
+    double to_fixed[3];       // 2^32 / L
+    float scale[3];           // L / 2^32
+};
+
+inline FixedBox make_fixed_box(const b2md_box *box) {
+    FixedBox f;
+    for (int c = 0; c < 3; ++c) {
+        f.to_fixed[c] = 4294967296.0 / box->edge[c];
+        f.scale[c] = (float)(box->edge[c] / 4294967296.0);
+    }
+    return f;
+}
+
+// (x, y, z, w) -> fixed-point x, y, z (mod 2^32: a coordinate equal to L is 0), w kept
+__device__ __forceinline__ int4 to_fixed4(const float4 p, const FixedBox &fb) {
+    int4 q;
+    q.x = (int)(unsigned)__double2ll_rn((double)p.x * fb.to_fixed[0]);
+    q.y = (int)(unsigned)__double2ll_rn((double)p.y * fb.to_fixed[1]);
+    q.z = (int)(unsigned)__double2ll_rn((double)p.z * fb.to_fixed[2]);
+    q.w = __float_as_int(p.w);
+    return q;
+}
+
+__device__ __forceinline__ float fixed_delta(int a, int b, float scale) {
+    return __int2float_rn((int)((unsigned)a - (unsigned)b)) * scale;
+}
+
 // forces.py:113-116 for the all-pairs kernels: lowest j != i at zero distance from particle i.
-__device__ __noinline__ void all_pairs_report_singular(int i, const float4 pi,
+__device__ __noinline__ void all_pairs_report_singular(int i, const int4 qi,
                                                        const float4 *__restrict__ pos, int n,
-                                                       const BoxF &b, b2md_status *status) {
+                                                       const FixedBox &fb, b2md_status *status) {
     for (int j = 0; j < n; ++j) {
         if (j == i) continue;
-        const float4 pj = pos[j];
-        const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-        const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-        const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
-        if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) == 0.0f) {
+        const int4 qj = to_fixed4(pos[j], fb);
+        if (qi.x == qj.x && qi.y == qj.y && qi.z == qj.z) {
             atomicMin((unsigned long long *)&status->singular,
                       ((unsigned long long)(unsigned)i << 32) | (unsigned)j);
             return;
@@ -1364,18 +1396,18 @@ __device__ __noinline__ void all_pairs_report_singular(int i, const float4 pi,
 
 // One pair of the all-pairs scan (forces.py:41-66): the pair contributes iff r2 != 0.
 template <bool TABLE>
-__device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const float4 pi,
-                                                const float4 pj, const BoxF &b,
+__device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const int4 qi,
+                                                const int4 qj, const FixedBox &fb,
                                                 const ForceArgs &a, const float4 *s_tab_a,
                                                 const float2 *s_tab_b, int ti_row) {
-    const float dx = delta<true>(pi.x, pj.x, b.L_hi[0], b.L_lo[0], b.invL[0]);
-    const float dy = delta<true>(pi.y, pj.y, b.L_hi[1], b.L_lo[1], b.invL[1]);
-    const float dz = delta<true>(pi.z, pj.z, b.L_hi[2], b.L_lo[2], b.invL[2]);
+    const float dx = fixed_delta(qi.x, qj.x, fb.scale[0]);
+    const float dy = fixed_delta(qi.y, qj.y, fb.scale[1]);
+    const float dz = fixed_delta(qi.z, qj.z, fb.scale[2]);
     const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
     const bool valid = r2 != 0.0f;
     zeros += valid ? 0 : 1;
     if (TABLE) {
-        const int tt = ti_row + __float_as_int(pj.w);
+        const int tt = ti_row + qj.w;
         lj_pair_table<true>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
     } else {
         lj_pair_single<true>(acc, dx, dy, dz, r2, valid, a.single);
@@ -1385,8 +1417,9 @@ __device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const f
 template <bool TABLE>
 __global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(kForceThreads)
 k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
-                  float4 *__restrict__ force, float *__restrict__ virial, b2md_status *status) {
-    __shared__ float4 tile[kForceThreads];
+                  const __grid_constant__ FixedBox fb, float4 *__restrict__ force,
+                  float *__restrict__ virial, b2md_status *status) {
+    __shared__ int4 tile[kForceThreads];
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ AllPairsPartial s_part[kForceThreads];
@@ -1401,21 +1434,20 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
     const int64_t i_raw = (blockIdx.x / kAllPairsSplit) * (int64_t)blockDim.x + threadIdx.x;
     const bool active = i_raw < n;
     const int64_t i = active ? i_raw : n - 1;
-    const float4 pi = pos[i];
-    const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
-    const BoxF &b = a.box;
+    const int4 qi = to_fixed4(pos[i], fb);
+    const int ti_row = TABLE ? qi.w * a.ntypes : 0;
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     int zeros = 0;
     const int ni = (int)n;                       // (row indices are 32-bit everywhere)
     for (int base = (int)rank * kForceThreads; base < ni; base += kAllPairsSplit * kForceThreads) {
         __syncthreads();
         const int jl = base + (int)threadIdx.x;
-        tile[threadIdx.x] = pos[jl < ni ? jl : ni - 1];
+        tile[threadIdx.x] = to_fixed4(pos[jl < ni ? jl : ni - 1], fb);
         __syncthreads();
         const int lim = min(kForceThreads, ni - base);
 #pragma unroll 4
         for (int t = 0; t < lim; ++t)
-            all_pairs_entry<TABLE>(acc, zeros, pi, tile[t], b, a, s_tab_a, s_tab_b, ti_row);
+            all_pairs_entry<TABLE>(acc, zeros, qi, tile[t], fb, a, s_tab_a, s_tab_b, ti_row);
     }
     AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
     s_part[threadIdx.x] = mine;
@@ -1452,7 +1484,7 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
         }
         force[i] = make_float4(fx, fy, fz, u);
         if (virial) virial[i] = w;
-        if (zeros_all != 1) all_pairs_report_singular((int)i, pi, pos, (int)n, b, status);
+        if (zeros_all != 1) all_pairs_report_singular((int)i, qi, pos, (int)n, fb, status);
     }
     // nobody leaves while block 0 may still read its shared memory
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1470,10 +1502,11 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
 template <bool TABLE, int WARPS>
 __global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(32 * WARPS)
 k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
-                        const __grid_constant__ ForceArgs a, float4 *__restrict__ force,
-                        float *__restrict__ virial, b2md_status *status) {
+                        const __grid_constant__ ForceArgs a, const __grid_constant__ FixedBox fb,
+                        float4 *__restrict__ force, float *__restrict__ virial,
+                        b2md_status *status) {
     constexpr int kTile = 32 * WARPS;
-    __shared__ float4 tile[kTile];
+    __shared__ int4 tile[kTile];
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ AllPairsPartial s_part[kTile];           // [warp][lane]
@@ -1490,9 +1523,8 @@ k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
     const int64_t i_raw = (blockIdx.x / kAllPairsSplit) * 32ll + lane;
     const bool active = i_raw < n;
     const int64_t i = active ? i_raw : n - 1;
-    const float4 pi = pos[i];
-    const int ti_row = TABLE ? __float_as_int(pi.w) * a.ntypes : 0;
-    const BoxF &b = a.box;
+    const int4 qi = to_fixed4(pos[i], fb);
+    const int ti_row = TABLE ? qi.w * a.ntypes : 0;
     RowAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
     int zeros = 0;
     const int ni = (int)n;                       // (row indices are 32-bit everywhere)
@@ -1500,12 +1532,12 @@ k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
     for (int base = (int)rank * kTile; base < ni; base += kAllPairsSplit * kTile) {
         __syncthreads();
         const int jl = base + (int)threadIdx.x;
-        tile[threadIdx.x] = pos[jl < ni ? jl : ni - 1];
+        tile[threadIdx.x] = to_fixed4(pos[jl < ni ? jl : ni - 1], fb);
         __syncthreads();
         const int lim = max(0, min(32, ni - (base + warp * 32)));
 #pragma unroll 4
         for (int t = 0; t < lim; ++t)
-            all_pairs_entry<TABLE>(acc, zeros, pi, tile[my + t], b, a, s_tab_a, s_tab_b, ti_row);
+            all_pairs_entry<TABLE>(acc, zeros, qi, tile[my + t], fb, a, s_tab_a, s_tab_b, ti_row);
     }
     AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
     s_part[threadIdx.x] = mine;
@@ -1554,7 +1586,7 @@ k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
         }
         force[i] = make_float4(fx, fy, fz, u);
         if (virial) virial[i] = w;
-        if (zeros_all != 1) all_pairs_report_singular((int)i, pi, pos, (int)n, b, status);
+        if (zeros_all != 1) all_pairs_report_singular((int)i, qi, pos, (int)n, fb, status);
     }
     // nobody leaves while block 0 may still read its shared memory
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1656,14 +1688,15 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     cudaStream_t s = as_stream(stream);
     const float4 *pos = (const float4 *)d_pos_hi;
     float4 *force = (float4 *)d_force_f4;
+    const FixedBox fb = make_fixed_box(box);
     // Kernel shape by size (measured on B200, kernel time under ncu, profiles/README.md):
     // N = 2000: 32.8 us with one thread per particle i, 13.6 us with 8 warps per 32 particles;
     // N = 8192: 179 / 136 us; N = 32 768: 2.11 / 1.99 ms (4 warps); N = 131 072: 30.3 / 30.7 ms.
     // The choice depends on n alone, so a system always takes the same summation order.
 #define B2MD_LAUNCH_SMALL(TABLE, WARPS)                                                        \
     k_force_all_pairs_small<TABLE, WARPS>                                                     \
-        <<<blocks_for(n, 32) * kAllPairsSplit, 32 * WARPS, 0, s>>>(pos, n, a, force, d_virial, \
-                                                                   d_status)
+        <<<blocks_for(n, 32) * kAllPairsSplit, 32 * WARPS, 0, s>>>(pos, n, a, fb, force,      \
+                                                                   d_virial, d_status)
     if (n < kAllPairsEightWarps) {
         if (ntypes == 1) B2MD_LAUNCH_SMALL(false, 8);
         else B2MD_LAUNCH_SMALL(true, 8);
@@ -1673,11 +1706,11 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     } else {
         const unsigned blocks = blocks_for(n, kForceThreads) * kAllPairsSplit;   // clusters of 8
         if (ntypes == 1)
-            k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(pos, n, a, force, d_virial,
-                                                                      d_status);
+            k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(pos, n, a, fb, force,
+                                                                      d_virial, d_status);
         else
-            k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(pos, n, a, force, d_virial,
-                                                                     d_status);
+            k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(pos, n, a, fb, force,
+                                                                     d_virial, d_status);
     }
 #undef B2MD_LAUNCH_SMALL
     B2MD_CHECK_LAUNCH("b2md_force_lj_all_pairs");
