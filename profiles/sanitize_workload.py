@@ -54,5 +54,21 @@ sim = b2.Simulation(st2, box, b2.PairTable.kob_andersen(), 0.002, force_mode=b2.
 sim.run(60); print("KA E", sim.measure().total_energy); sim.close()
 st, box = lattice(500, rho=0.8)
 sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0), 0.002, force_mode=b2.ALL_TO_ALL)
-sim.run(20); print("all-pairs E", sim.measure().total_energy)
+sim.run(20); print("all-pairs E", sim.measure().total_energy); sim.close()
+# ... its thermostatted loop (finalize + thermostat + integrate in one pass), the table variant,
+# and the 4-warp / one-thread-per-particle shapes of the all-pairs kernel (one evaluation each)
+st, box = lattice(500, rho=0.8)
+sim = b2.Simulation(st, box, b2.make_shifted(1.0, 1.0), 0.002,
+                    thermostat=b2.ThermostatParams(1.0, 20.0, 3))
+sim.run(20); print("all-pairs NVT E", sim.measure().total_energy); sim.close()
+st, box = lattice(600, rho=1.2)
+sp = (np.random.default_rng(2).permutation(600) < 120).astype(np.int32)
+st2 = b2.ParticleState(np.array(st.positions.acquire_read(b2.HOST)),
+                       velocities=np.array(st.velocities.acquire_read(b2.HOST)), species=sp)
+sim = b2.Simulation(st2, box, b2.PairTable.kob_andersen(), 0.002)
+sim.run(10); print("all-pairs KA E", sim.measure().total_energy); sim.close()
+if os.environ.get("SAN_BIG_ALL_PAIRS", "1") == "1":
+    st, box = lattice(12500, rho=0.8)
+    b2.compute_forces_all_to_all(st, b2.make_shifted(1.0, 1.0), box)
+    print("all-pairs 12500 PE", b2.potential_energy_total(st))
 print("SANITIZE_WORKLOAD_DONE")
