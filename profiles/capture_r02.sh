@@ -31,6 +31,18 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
     -o $o/allkernels -f python profiles/profile_step.py --melt 330 --steps 70 \
     --profiler-range > $o/prof_allkernels.log 2>&1
 python profiles/kernel_roofline.py $o/allkernels.ncu-rep > $o/kernel_roofline.txt 2>&1
+# the all-pairs kernel of the paper's N = 2000 benchmark (warp-split shape, fixed-point min-image)
+# and of a large system (one thread per particle), and the config table
+ncu --set full --clock-control none --import-source on -k regex:k_force_all_pairs -s 20 -c 1 \
+    -o $o/allpairs2k python profiles/exp/all_pairs_steps.py 2000 > $o/prof_allpairs2k.log 2>&1
+python profiles/ncu_summary.py $o/allpairs2k.ncu-rep > $o/ncu_all_pairs_n2000.txt 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_force_all_pairs -s 2 -c 1 \
+    -o $o/allpairs131k python profiles/exp/all_pairs_roofline.py 131072 > $o/prof_allpairs131k.log 2>&1
+python profiles/ncu_summary.py $o/allpairs131k.ncu-rep > $o/ncu_all_pairs_n131072.txt 2>&1
+python profiles/run_configs.py --which 1,2,3,4,A,5 > $o/configs.jsonl 2> $o/configs.err
+python profiles/exp/all_pairs_preset.py > $o/all_pairs_preset.jsonl 2>&1
+python profiles/exp/all_pairs_steps.py 256 2000 4096 8000 > $o/all_pairs_steps.jsonl 2>&1
+python profiles/exp/all_pairs_roofline.py 16384 32768 131072 > $o/all_pairs_roofline.jsonl 2>&1
 # the reports themselves exceed what gpurun copies back (64 MiB): keep the summaries
 rm -f $o/*.ncu-rep
 tail -c 1500 $o/bench_1gpu_steps20.json; cat $o/kernel_roofline.txt | tail -40
