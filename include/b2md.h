@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define B2MD_VERSION 107
+#define B2MD_VERSION 108
 
 /* Device-side status block (64 bytes).  Reset with b2md_status_reset. */
 typedef struct b2md_status {
@@ -673,9 +673,10 @@ int b2md_runner_set_step(b2md_runner *r, int64_t first_step);
  * Simulation.run with force_mode = "all_to_all", the reference's default (sim.py:62-102:
  * integrate -> compute_forces_all_to_all -> finalize [-> andersen_thermostat] per step,
  * core.py:262-279 for the loop).  n_steps MD steps are enqueued on `stream` without a host
- * round trip per step -- there is no list and no rebuild decision; finalize of step s and
- * integrate of step s + 1 share one pass over the state unless the thermostat sits between
- * them -- and the status block is read back every 512 steps and at the end.  Same kernels
+ * round trip per step -- there is no list and no rebuild decision -- and the status block is
+ * read back every 512 steps and at the end.  d_pos_hi_alt (may be NULL): a second buffer for
+ * the position high words; with it an intermediate step without thermostat is ONE launch
+ * (b2md_force_lj_all_pairs_advance), the final positions are copied back to d_pos_hi.  Same kernels
  * and order of operations as the operator-by-operator loop: bit-identical trajectories.
  * On return the velocities carry both half-kicks and d_force_f4 / d_virial hold the forces,
  * per-particle energies and virial of the final positions.  thermo_probability = min(rate *
@@ -688,8 +689,19 @@ int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, void *d_forc
                        void *d_image_i4, float *d_virial, int64_t n, const b2md_box *box,
                        const double *table, int32_t ntypes, double dt, int64_t n_steps,
                        double thermo_probability, double thermo_temperature,
-                       uint64_t thermo_seed, int64_t first_step, b2md_status *d_status,
-                       void *h_status, void *stream, b2md_run_report *report);
+                       uint64_t thermo_seed, int64_t first_step, void *d_pos_hi_alt,
+                       b2md_status *d_status, void *h_status, void *stream,
+                       b2md_run_report *report);
+/* compute_forces_all_to_all + vv_finalize + vv_integrate of the next step in one launch (the
+ * intermediate steps of b2md_run_all_pairs when d_pos_hi_alt != NULL; forces.py:129-138,
+ * integrate.py:58-79): the thread that holds a particle's total force advances it.  Reads
+ * d_pos_hi, writes the new high words to d_pos_hi_out (a different buffer); d_pos_lo, d_vel
+ * and d_image_i4 are updated in place; forces are not stored.  Bit-identical to the separate
+ * launches. */
+int b2md_force_lj_all_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out, void *d_pos_lo,
+                                    void *d_vel, void *d_image_i4, int64_t n,
+                                    const b2md_box *box, const double *table, int32_t ntypes,
+                                    double dt, b2md_status *d_status, void *stream);
 
 #ifdef __cplusplus
 }

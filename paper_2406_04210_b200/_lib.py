@@ -205,7 +205,9 @@ _SIGNATURES = {
                                             _P, _P]),
     "b2md_run_all_pairs": (c_int32, [_P, _P, _P, _P, _P, _P, c_int64, _P, _P, c_int32, c_double,
                                      c_int64, c_double, c_double, c_uint64, c_int64, _P, _P, _P,
-                                     _P]),
+                                     _P, _P]),
+    "b2md_force_lj_all_pairs_advance": (c_int32, [_P, _P, _P, _P, _P, c_int64, _P, _P, c_int32,
+                                                  c_double, _P, _P]),
 }
 
 #: entry points that report errors through their int return value

@@ -1395,7 +1395,7 @@ __device__ __noinline__ void all_pairs_report_singular(int i, const int4 qi,
 }
 
 // One pair of the all-pairs scan (forces.py:41-66): the pair contributes iff r2 != 0.
-template <bool TABLE>
+template <bool TABLE, bool THERMO = true>
 __device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const int4 qi,
                                                 const int4 qj, const FixedBox &fb,
                                                 const ForceArgs &a, const float4 *s_tab_a,
@@ -1408,17 +1408,29 @@ __device__ __forceinline__ void all_pairs_entry(RowAcc &acc, int &zeros, const i
     zeros += valid ? 0 : 1;
     if (TABLE) {
         const int tt = ti_row + qj.w;
-        lj_pair_table<true>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
+        lj_pair_table<THERMO>(acc, dx, dy, dz, r2, valid, s_tab_a[tt], s_tab_b[tt]);
     } else {
-        lj_pair_single<true>(acc, dx, dy, dz, r2, valid, a.single);
+        lj_pair_single<THERMO>(acc, dx, dy, dz, r2, valid, a.single);
     }
 }
 
-template <bool TABLE>
+// ADVANCE variants of the all-pairs kernels (the intermediate steps of b2md_run_all_pairs): the
+// thread that holds a particle's total force also applies vv_finalize of this step and
+// vv_integrate of the next (integrate.py:58-79, the body of k_integrate<2>) -- one launch per
+// MD step, forces never stored.  Every block of the launch reads the old positions, so the new
+// high words go to a second buffer.
+struct AllPairsAdvance {
+    float4 *pos_out, *pos_lo, *vel;
+    int4 *image;
+    StepConst step;
+};
+
+template <bool TABLE, bool ADVANCE = false>
 __global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(kForceThreads)
 k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_constant__ ForceArgs a,
                   const __grid_constant__ FixedBox fb, float4 *__restrict__ force,
-                  float *__restrict__ virial, b2md_status *status) {
+                  float *__restrict__ virial, b2md_status *status,
+                  const __grid_constant__ AllPairsAdvance adv) {
     __shared__ int4 tile[kForceThreads];
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
     __shared__ float2 s_tab_b[TABLE ? kMaxTypes * kMaxTypes : 1];
@@ -1447,7 +1459,7 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
         const int lim = min(kForceThreads, ni - base);
 #pragma unroll 4
         for (int t = 0; t < lim; ++t)
-            all_pairs_entry<TABLE>(acc, zeros, qi, tile[t], fb, a, s_tab_a, s_tab_b, ti_row);
+            all_pairs_entry<TABLE, !ADVANCE>(acc, zeros, qi, tile[t], fb, a, s_tab_a, s_tab_b, ti_row);
     }
     AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
     s_part[threadIdx.x] = mine;
@@ -1482,8 +1494,15 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
             u = fmaf(p.c_u, sum.u, p.half_shift * (float)sum.cnt);
             w = p.c_w * sum.w;
         }
-        force[i] = make_float4(fx, fy, fz, u);
-        if (virial) virial[i] = w;
+        if (ADVANCE) {
+            float4 h = pos[i];
+            advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo, adv.vel, adv.image,
+                                adv.step, nullptr);
+            adv.pos_out[i] = h;
+        } else {
+            force[i] = make_float4(fx, fy, fz, u);
+            if (virial) virial[i] = w;
+        }
         if (zeros_all != 1) all_pairs_report_singular((int)i, qi, pos, (int)n, fb, status);
     }
     // nobody leaves while block 0 may still read its shared memory
@@ -1499,12 +1518,12 @@ k_force_all_pairs(const float4 *__restrict__ pos, int64_t n, const __grid_consta
 // through shared memory, then blocks 0 .. 7 through distributed shared memory -- so results
 // are bitwise reproducible.  The shape depends on n alone: a system always takes the same
 // summation order.
-template <bool TABLE, int WARPS>
+template <bool TABLE, int WARPS, bool ADVANCE = false>
 __global__ void __cluster_dims__(kAllPairsSplit, 1, 1) __launch_bounds__(32 * WARPS)
 k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
                         const __grid_constant__ ForceArgs a, const __grid_constant__ FixedBox fb,
                         float4 *__restrict__ force, float *__restrict__ virial,
-                        b2md_status *status) {
+                        b2md_status *status, const __grid_constant__ AllPairsAdvance adv) {
     constexpr int kTile = 32 * WARPS;
     __shared__ int4 tile[kTile];
     __shared__ float4 s_tab_a[TABLE ? kMaxTypes * kMaxTypes : 1];
@@ -1537,7 +1556,7 @@ k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
         const int lim = max(0, min(32, ni - (base + warp * 32)));
 #pragma unroll 4
         for (int t = 0; t < lim; ++t)
-            all_pairs_entry<TABLE>(acc, zeros, qi, tile[my + t], fb, a, s_tab_a, s_tab_b, ti_row);
+            all_pairs_entry<TABLE, !ADVANCE>(acc, zeros, qi, tile[my + t], fb, a, s_tab_a, s_tab_b, ti_row);
     }
     AllPairsPartial mine = {acc.fx, acc.fy, acc.fz, acc.u, acc.w, acc.cnt, zeros, 0};
     s_part[threadIdx.x] = mine;
@@ -1584,8 +1603,15 @@ k_force_all_pairs_small(const float4 *__restrict__ pos, int64_t n,
             u = fmaf(p.c_u, sum.u, p.half_shift * (float)sum.cnt);
             w = p.c_w * sum.w;
         }
-        force[i] = make_float4(fx, fy, fz, u);
-        if (virial) virial[i] = w;
+        if (ADVANCE) {
+            float4 h = pos[i];
+            advance_particle<2>(i, h, make_float4(fx, fy, fz, u), adv.pos_lo, adv.vel, adv.image,
+                                adv.step, nullptr);
+            adv.pos_out[i] = h;
+        } else {
+            force[i] = make_float4(fx, fy, fz, u);
+            if (virial) virial[i] = w;
+        }
         if (zeros_all != 1) all_pairs_report_singular((int)i, qi, pos, (int)n, fb, status);
     }
     // nobody leaves while block 0 may still read its shared memory
@@ -1678,10 +1704,13 @@ B2MD_EXPORT int b2md_force_lj(const void *d_pos_hi, int64_t n, const b2md_box *b
     return 0;
 }
 
-B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
-                                        const double *table, int32_t ntypes, void *d_force_f4,
-                                        float *d_virial, b2md_status *d_status, void *stream) {
-    if (n <= 0 || !d_status) { set_error("b2md_force_lj_all_pairs: bad arguments"); return -1; }
+namespace {
+
+// adv == nullptr: forces, energies, virial stored; else the ADVANCE variant (nothing stored)
+int launch_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box, const double *table,
+                     int32_t ntypes, void *d_force_f4, float *d_virial, b2md_status *d_status,
+                     const AllPairsAdvance *advance, void *stream, const char *name) {
+    if (n <= 0 || !d_status || !d_pos_hi) { set_error("%s: bad arguments", name); return -1; }
     ForceArgs a;
     int rc = fill_args(a, box, table, ntypes);
     if (rc) return rc;
@@ -1689,32 +1718,67 @@ B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b
     const float4 *pos = (const float4 *)d_pos_hi;
     float4 *force = (float4 *)d_force_f4;
     const FixedBox fb = make_fixed_box(box);
+    AllPairsAdvance adv = {};
+    if (advance) adv = *advance;
     // Kernel shape by size (measured on B200, kernel time under ncu, profiles/README.md):
     // N = 2000: 32.8 us with one thread per particle i, 13.6 us with 8 warps per 32 particles;
     // N = 8192: 179 / 136 us; N = 32 768: 2.11 / 1.99 ms (4 warps); N = 131 072: 30.3 / 30.7 ms.
     // The choice depends on n alone, so a system always takes the same summation order.
-#define B2MD_LAUNCH_SMALL(TABLE, WARPS)                                                        \
-    k_force_all_pairs_small<TABLE, WARPS>                                                     \
+#define B2MD_LAUNCH_SMALL(TABLE, WARPS, ADVANCE)                                               \
+    k_force_all_pairs_small<TABLE, WARPS, ADVANCE>                                            \
         <<<blocks_for(n, 32) * kAllPairsSplit, 32 * WARPS, 0, s>>>(pos, n, a, fb, force,      \
-                                                                   d_virial, d_status)
-    if (n < kAllPairsEightWarps) {
-        if (ntypes == 1) B2MD_LAUNCH_SMALL(false, 8);
-        else B2MD_LAUNCH_SMALL(true, 8);
-    } else if (n < kAllPairsFourWarps) {
-        if (ntypes == 1) B2MD_LAUNCH_SMALL(false, 4);
-        else B2MD_LAUNCH_SMALL(true, 4);
+                                                                   d_virial, d_status, adv)
+#define B2MD_LAUNCH_BIG(TABLE, ADVANCE)                                                        \
+    k_force_all_pairs<TABLE, ADVANCE>                                                         \
+        <<<blocks_for(n, kForceThreads) * kAllPairsSplit, kForceThreads, 0, s>>>(             \
+            pos, n, a, fb, force, d_virial, d_status, adv)
+#define B2MD_LAUNCH_BY_SIZE(TABLE, ADVANCE)                                                    \
+    do {                                                                                      \
+        if (n < kAllPairsEightWarps) B2MD_LAUNCH_SMALL(TABLE, 8, ADVANCE);                    \
+        else if (n < kAllPairsFourWarps) B2MD_LAUNCH_SMALL(TABLE, 4, ADVANCE);                \
+        else B2MD_LAUNCH_BIG(TABLE, ADVANCE);                                                 \
+    } while (0)
+    if (advance) {
+        if (ntypes == 1) B2MD_LAUNCH_BY_SIZE(false, true);
+        else B2MD_LAUNCH_BY_SIZE(true, true);
     } else {
-        const unsigned blocks = blocks_for(n, kForceThreads) * kAllPairsSplit;   // clusters of 8
-        if (ntypes == 1)
-            k_force_all_pairs<false><<<blocks, kForceThreads, 0, s>>>(pos, n, a, fb, force,
-                                                                      d_virial, d_status);
-        else
-            k_force_all_pairs<true><<<blocks, kForceThreads, 0, s>>>(pos, n, a, fb, force,
-                                                                     d_virial, d_status);
+        if (ntypes == 1) B2MD_LAUNCH_BY_SIZE(false, false);
+        else B2MD_LAUNCH_BY_SIZE(true, false);
     }
+#undef B2MD_LAUNCH_BY_SIZE
+#undef B2MD_LAUNCH_BIG
 #undef B2MD_LAUNCH_SMALL
-    B2MD_CHECK_LAUNCH("b2md_force_lj_all_pairs");
+    B2MD_CHECK_LAUNCH(name);
     return 0;
+}
+
+}  // namespace
+
+B2MD_EXPORT int b2md_force_lj_all_pairs(const void *d_pos_hi, int64_t n, const b2md_box *box,
+                                        const double *table, int32_t ntypes, void *d_force_f4,
+                                        float *d_virial, b2md_status *d_status, void *stream) {
+    return launch_all_pairs(d_pos_hi, n, box, table, ntypes, d_force_f4, d_virial, d_status,
+                            nullptr, stream, "b2md_force_lj_all_pairs");
+}
+
+B2MD_EXPORT int b2md_force_lj_all_pairs_advance(const void *d_pos_hi, void *d_pos_hi_out,
+                                                void *d_pos_lo, void *d_vel, void *d_image_i4,
+                                                int64_t n, const b2md_box *box,
+                                                const double *table, int32_t ntypes, double dt,
+                                                b2md_status *d_status, void *stream) {
+    if (!d_pos_hi_out || d_pos_hi_out == d_pos_hi || !d_pos_lo || !d_vel || !d_image_i4 ||
+        !box || !(dt > 0.0)) {
+        set_error("b2md_force_lj_all_pairs_advance: bad arguments");
+        return -1;
+    }
+    AllPairsAdvance adv;
+    adv.pos_out = (float4 *)d_pos_hi_out;
+    adv.pos_lo = (float4 *)d_pos_lo;
+    adv.vel = (float4 *)d_vel;
+    adv.image = (int4 *)d_image_i4;
+    adv.step = make_step(box, dt, 1e30);
+    return launch_all_pairs(d_pos_hi, n, box, table, ntypes, nullptr, nullptr, d_status, &adv,
+                            stream, "b2md_force_lj_all_pairs_advance");
 }
 
 namespace {

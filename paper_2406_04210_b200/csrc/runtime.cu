@@ -1192,10 +1192,13 @@ B2MD_EXPORT int b2md_runner_run(b2md_runner *r, int64_t n_steps, int32_t finaliz
 // Simulation.run with force_mode = "all_to_all" (the reference's default, sim.py:62-102):
 // integrate -> compute_forces_all_to_all -> finalize [-> thermostat] per step.  No list, no
 // rebuild flag, nothing the host has to look at between steps: the whole call is enqueued
-// without a round trip (finalize of step s and integrate of step s + 1 share one pass over the
-// state unless the thermostat sits between them) and the status block -- the singular-pair
-// word -- is read once per chunk of kAllPairsChunk steps.  Same kernels, same order of
-// operations as the operator loop: bit-identical trajectories.
+// without a round trip and the status block -- the singular-pair word -- is read once per chunk
+// of kAllPairsChunk steps.  With a second buffer for the position high words an intermediate
+// step is ONE launch (b2md_force_lj_all_pairs_advance: force + finalize + integrate of the next
+// step by the thread that holds the particle's total force); without it finalize of step s and
+// integrate of step s + 1 share one pass over the state; a thermostatted step is the force
+// kernel plus b2md_vv_finalize_andersen.  Same operations in the same order as the operator
+// loop: bit-identical trajectories.
 constexpr int64_t kAllPairsChunk = 512;
 
 B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, void *d_force_f4,
@@ -1203,8 +1206,8 @@ B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, 
                                    const b2md_box *box, const double *table, int32_t ntypes,
                                    double dt, int64_t n_steps, double thermo_probability,
                                    double thermo_temperature, uint64_t thermo_seed,
-                                   int64_t first_step, b2md_status *d_status, void *h_status,
-                                   void *stream, b2md_run_report *rep) {
+                                   int64_t first_step, void *d_pos_hi_alt, b2md_status *d_status,
+                                   void *h_status, void *stream, b2md_run_report *rep) {
     if (!d_pos_hi || !d_pos_lo || !d_vel || !d_force_f4 || !d_image_i4 || !box || !table ||
         !d_status || !h_status || !rep || n < 1 || n_steps < 0 || !(thermo_probability >= 0.0)) {
         set_error("b2md_run_all_pairs: bad arguments");
@@ -1230,23 +1233,38 @@ B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, 
     if ((rc = b2md_status_reset(d_status, stream))) return leave(rc);
     if ((rc = check_cuda(cudaEventRecord(ev[0], s), "event record"))) return leave(rc);
     bool pending_kick = false;          // forces of the last step not yet applied to the velocities
-    bool ahead = false;                 // the next step is already integrated (thermostatted loop)
+    bool ahead = false;                 // the next step is already integrated
+    // One launch per intermediate step (b2md_force_lj_all_pairs_advance) when the caller lends
+    // a second buffer for the position high words: they ping-pong between the two.
+    const bool fuse = d_pos_hi_alt != nullptr && d_pos_hi_alt != d_pos_hi && !thermostatted;
+    void *cur = d_pos_hi, *other = d_pos_hi_alt;
     while (rep->steps_done < n_steps) {
         const int64_t chunk = std::min<int64_t>(kAllPairsChunk, n_steps - rep->steps_done);
         for (int64_t q = 0; q < chunk; ++q) {
             if (!ahead) {
                 if (pending_kick)
-                    rc = b2md_vv_finalize_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4,
+                    rc = b2md_vv_finalize_integrate(cur, d_pos_lo, d_vel, d_force_f4,
                                                     d_image_i4, n, box, dt, nullptr, 0.0, d_status,
                                                     stream);
                 else
-                    rc = b2md_vv_integrate(d_pos_hi, d_pos_lo, d_vel, d_force_f4, d_image_i4, n,
+                    rc = b2md_vv_integrate(cur, d_pos_lo, d_vel, d_force_f4, d_image_i4, n,
                                            box, dt, nullptr, 0.0, d_status, stream);
                 if (rc) return leave(rc);
                 rep->kernel_launches += 1;
             }
             ahead = false;
-            if ((rc = b2md_force_lj_all_pairs(d_pos_hi, n, box, table, ntypes, d_force_f4, d_virial,
+            if (fuse && rep->steps_done + q + 1 < n_steps) {
+                // force(s) + finalize(s) + integrate(s + 1) in one launch
+                if ((rc = b2md_force_lj_all_pairs_advance(cur, other, d_pos_lo, d_vel, d_image_i4, n,
+                                                          box, table, ntypes, dt, d_status, stream)))
+                    return leave(rc);
+                rep->kernel_launches += 1;
+                std::swap(cur, other);
+                ahead = true;
+                pending_kick = false;
+                continue;
+            }
+            if ((rc = b2md_force_lj_all_pairs(cur, n, box, table, ntypes, d_force_f4, d_virial,
                                               d_status, stream))) return leave(rc);
             rep->kernel_launches += 1;
             pending_kick = true;
@@ -1271,6 +1289,12 @@ B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, 
             rep->kernel_launches += 1;
             pending_kick = false;
         }
+        if (last && cur != d_pos_hi) {
+            if ((rc = check_cuda(cudaMemcpyAsync(d_pos_hi, cur, (size_t)n * 4 * sizeof(float),
+                                                 cudaMemcpyDeviceToDevice, s), "position copy")))
+                return leave(rc);
+            std::swap(cur, other);
+        }
         if (last && (rc = check_cuda(cudaEventRecord(ev[1], s), "event record"))) return leave(rc);
         if ((rc = check_cuda(cudaMemcpyAsync(h, d_status, sizeof(b2md_status),
                                              cudaMemcpyDeviceToHost, s), "status read-back")))
@@ -1283,6 +1307,10 @@ B2MD_EXPORT int b2md_run_all_pairs(void *d_pos_hi, void *d_pos_lo, void *d_vel, 
                 if ((rc = b2md_vv_finalize(d_vel, d_force_f4, n, dt, stream))) return leave(rc);
                 rep->kernel_launches += 1;
             }
+            if (cur != d_pos_hi &&
+                (rc = check_cuda(cudaMemcpyAsync(d_pos_hi, cur, (size_t)n * 4 * sizeof(float),
+                                                 cudaMemcpyDeviceToDevice, s), "position copy")))
+                return leave(rc);
             if (!last && (rc = check_cuda(cudaEventRecord(ev[1], s), "event record")))
                 return leave(rc);
             if ((rc = check_cuda(cudaStreamSynchronize(s), "drain"))) return leave(rc);

@@ -574,6 +574,10 @@ class Simulation:
         tab, tab_ptr, nt = _table_ptr(self.lj, st)
         if "h_status" not in self._keep:
             self._keep["h_status"] = torch.empty(64, dtype=torch.uint8).pin_memory()
+        # second buffer for the position high words: intermediate steps are one launch each
+        alt = self._keep.get("pos_alt")
+        if alt is None or alt.shape != dev.pos_hi.shape or alt.device != dev.pos_hi.device:
+            alt = self._keep["pos_alt"] = torch.empty_like(dev.pos_hi)
         p = self.thermostat.redraw_probability(self.integrator.dt) if self._thermostatted else 0.0
         temperature = float(self.thermostat.temperature) if self._thermostatted else 1.0
         seed = int(self.thermostat.seed) % (1 << 64) if self._thermostatted else 0
@@ -587,7 +591,8 @@ class Simulation:
                       dev.vel.data_ptr(), dev.force.data_ptr(), dev.image.data_ptr(),
                       dev.virial.data_ptr(), dev.n, self.box.c_box(), tab_ptr, nt,
                       float(self.integrator.dt), chunk, float(p), temperature, seed,
-                      eng.step_count, dev.status.data_ptr(), self._keep["h_status"].data_ptr(),
+                      eng.step_count, alt.data_ptr(), dev.status.data_ptr(),
+                      self._keep["h_status"].data_ptr(),
                       dev.stream, ctypes.byref(rep))
             wall = time.perf_counter() - t0
             self.force_seconds += min(1e-3 * rep.gpu_ms, wall)

@@ -43,10 +43,11 @@ def test_native_loop_is_bit_identical_to_the_operator_loop(tag):
     for a, b in zip(out[True][0], out[False][0]):
         assert np.array_equal(a, b)
     assert out[True][1] == out[False][1]
-    # two launches per step -- all pairs, and one pass over the state: finalize + integrate (NVE)
-    # or finalize + thermostat + integrate (NVT) -- plus, per call (a call ends at each sample),
-    # the first integrate on its own and the last finalize without the integrate
-    assert out[True][2] == 2 * 200 + 11
+    # NVE: one launch per intermediate step (all pairs + finalize + integrate), and per call (a
+    # call ends at each sample) the first integrate, the last force evaluation and its finalize;
+    # NVT: all pairs, then finalize + thermostat + integrate in one pass -- two launches per
+    # step -- plus the first integrate of every call
+    assert out[True][2] == (200 + 2 * 11 if tag == "nve" else 2 * 200 + 11)
 
 
 @pytest.mark.parametrize("tag", ["nve", "nvt"])

@@ -15,7 +15,7 @@ from conftest import GOLDEN, ROOT, load_golden
 
 def test_library_exports_every_declared_symbol():
     lib = _lib.load()
-    assert lib.b2md_version() == 107
+    assert lib.b2md_version() == 108
     header = open(os.path.join(ROOT, "include", "b2md.h")).read()
     declared = set(re.findall(r"\b(b2md_[a-z0-9_]+)\(", header))
     declared -= {"b2md_box", "b2md_grid", "b2md_status"}
