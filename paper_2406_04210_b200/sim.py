@@ -636,6 +636,8 @@ class Simulation:
                 for name, t in live.items():
                     setattr(dev, name, t)
             self._keep = {}
+        elif self.native_all_pairs:
+            self._keep = {}          # pinned status block, second position buffer
         self._nlist = None
         self._closed = True
         for slots in self.engine._slots.values():
