@@ -96,3 +96,83 @@ def test_singular_pair_surfaces_through_the_native_loop():
         sim.run(3)
     assert (err.value.i, err.value.j) == (17, 93)
     sim.close()
+
+
+# ---- the other shapes of the all-pairs kernel (chosen from n alone) ---------------------
+def _all_pairs_vs_oracle(n, lj):
+    """Untruncated potential: every particle sums n - 1 pair terms in fp32, so the bounds are
+    the stated 1e-5 on the L2 error of the forces and, per particle, 1e-4 relative to the rms
+    force / 2e-4 on energies and virial (measured at N = 12 500, profiles/exp/
+    all_pairs_accuracy.py: L2 5.1e-7, M1 1.4e-5, M3 4.1e-5, energy 7.5e-5 -- the exact-fp32
+    min-image kernel this one replaced: 3.6e-7, 1.4e-5, 2.1e-5, 7.5e-5)."""
+    from helpers import fluid_state, force_error_metrics, scalar_rel_error
+    from oracle import oracle as orc
+    pos, _, edge = fluid_state(n, density=0.8, seed=5)
+    pos = quantize_f32(pos)
+    st = b2.ParticleState(pos)
+    b2.compute_forces_all_to_all(st, lj, b2.SimBox.cubic(edge))
+    rf, rpe, rw = orc.forces_all_pairs(pos, [edge] * 3, lj.table(), threads=orc.host_threads())
+    f = np.array(st.forces.acquire_read(b2.HOST))
+    m = force_error_metrics(f, rf)
+    m["L2"] = float(np.linalg.norm(f - rf) / np.linalg.norm(rf))
+    assert m["L2"] <= 1e-5 and m["M3"] <= 1e-4 and m["M1"] <= 1e-4, m
+    assert scalar_rel_error(st.per_particle_potential.acquire_read(b2.HOST), rpe) <= 2e-4
+    assert scalar_rel_error(st.virial.acquire_read(b2.HOST), rw) <= 2e-4
+    return m
+
+
+def test_four_warp_shape_matches_the_oracle():
+    """12 288 <= N < 65 536: four warps per tile of 32 particles (fixed-point min-image)."""
+    _all_pairs_vs_oracle(12500, b2.make_shifted(1.0, 1.0))
+
+
+def test_one_thread_per_particle_shape_matches_the_list_kernels():
+    """N >= 65 536: one thread per particle in blocks of 128.  The oracle's all-pairs scan
+    takes minutes there; with a cutoff the all-pairs result must equal the neighbour-list
+    result (itself pinned to the oracle at this size by test_gpu_bench_sizes.py) up to the
+    fp32 summation order."""
+    from helpers import fluid_state, force_error_metrics, scalar_rel_error
+    n = 66000
+    pos, _, edge = fluid_state(n, density=0.75, seed=9)
+    pos = quantize_f32(pos)
+    box = b2.SimBox.cubic(edge)
+    lj = b2.make_shifted(1.0, 1.0, 2.5)
+    a, b = b2.ParticleState(pos), b2.ParticleState(pos)
+    b2.compute_forces_all_to_all(a, lj, box)
+    grid = b2.bin_particles(b, box, 2.8)
+    nl = b2.build_neighbor_list(b, grid, 2.8, 128, r_cut=2.5)
+    assert not nl.overflow
+    b2.compute_forces_truncated(b, lj, box, nl)
+    fa, fb = a.forces.acquire_read(b2.HOST), b.forces.acquire_read(b2.HOST)
+    m = force_error_metrics(fa, fb)
+    m["L2"] = float(np.linalg.norm(np.array(fa) - np.array(fb)) / np.linalg.norm(fb))
+    # (the jittered lattice has a few close contacts with forces of order 10^3: errors are
+    # judged against the particle's own force, M1, and in the L2 norm)
+    assert m["L2"] <= 1e-5 and m["M1"] <= 1e-5, m
+    # energies / virial: per particle, against its own value plus the typical sum of the
+    # magnitudes of its ~50 pair terms (a total near zero is a cancellation, not a scale)
+    for name, scale in (("per_particle_potential", 10.0), ("virial", 100.0)):
+        x = np.array(getattr(a, name).acquire_read(b2.HOST))
+        y = np.array(getattr(b, name).acquire_read(b2.HOST))
+        assert np.max(np.abs(x - y) / (np.abs(y) + scale)) <= 1e-5, name
+
+
+def test_pair_table_loop_is_bit_identical_to_the_operator_loop():
+    """Kob-Andersen tables through the all-to-all loop (table variants of the kernels,
+    one-launch steps included)."""
+    from helpers import fluid_state
+    n = 700
+    pos, vel, edge = fluid_state(n, density=1.2, temperature=0.8, seed=3, jitter=0.02)
+    species = (np.random.default_rng(4).permutation(n) < n // 5).astype(np.int32)
+    out = {}
+    for native in (True, False):
+        st = b2.ParticleState(quantize_f32(pos), velocities=quantize_f32(vel), species=species)
+        sim = b2.Simulation(st, b2.SimBox.cubic(edge), b2.PairTable.kob_andersen(), 0.001,
+                            sample_interval=25, native=native)
+        sim.run(60)
+        out[native] = host_state(sim) + [np.array([s.total_energy for s in sim.samples])]
+        sim.close()
+    for x, y in zip(out[True], out[False]):
+        assert np.array_equal(x, y)
+    e = out[True][-1]
+    assert np.all(np.isfinite(e)) and np.max(np.abs(e - e[0])) <= 1e-3 * abs(e[0])      # (sane run)
